@@ -1,0 +1,240 @@
+"""Pins for the fp64 oracle against things other than itself (SURVEY §8(c)
+"What pins each part", items 1-6): closed forms, brute force in Decimal,
+a library routine (torch SDPA in fp64), and invariants.  CPU only."""
+import math
+from decimal import Decimal, getcontext
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from neo_inputs import (KIND_K, KIND_V, VARIANT_SINK, bf16_bits_to_f64, f32_to_bf16_bits,
+                        kv_bits, q_bits)
+
+SEED = 0x4E454F
+
+
+def rand_bits(rng, shape, scale=1.0):
+    return f32_to_bf16_bits((rng.standard_normal(shape) * scale).astype(np.float32))
+
+
+def widen(b):
+    return bf16_bits_to_f64(b)
+
+
+# 1. a 1-token context returns v exactly
+@pytest.mark.parametrize("hq,hkv", [(4, 4), (8, 2), (32, 8)])
+def test_single_token_returns_v(hq, hkv):
+    rng = np.random.default_rng(1)
+    q = rand_bits(rng, (hq, 128))
+    k = rand_bits(rng, (1, hkv, 128))
+    v = rand_bits(rng, (1, hkv, 128))
+    out = oracle.decode_attention(q, k, v, 1 / math.sqrt(128))
+    G = hq // hkv
+    for h in range(hq):
+        assert np.array_equal(out[h], widen(v[0, h // G]))
+
+
+# 2. identical keys give the mean of V
+def test_identical_keys_give_mean_of_v():
+    rng = np.random.default_rng(2)
+    n, hkv, hq = 5000, 2, 8
+    q = rand_bits(rng, (hq, 128))
+    krow = rand_bits(rng, (1, hkv, 128))
+    k = np.repeat(krow, n, axis=0)
+    v = rand_bits(rng, (n, hkv, 128))
+    out = oracle.decode_attention(q, k, v, 0.088)
+    vm = widen(v).mean(axis=0)
+    for h in range(hq):
+        np.testing.assert_allclose(out[h], vm[h // 4], rtol=0, atol=1e-13)
+
+
+# 3. one-hot dominant score returns that row: q = 1, k_j = 4, others 0 => s_j = 45.25
+def test_one_hot_dominant_score():
+    n, j = 16384, 9876
+    q = np.full((1, 128), 0x3F80, dtype=np.uint16)            # bf16 1.0
+    k = np.zeros((n, 1, 128), dtype=np.uint16)
+    k[j] = 0x4080                                              # bf16 4.0
+    rng = np.random.default_rng(3)
+    v = rand_bits(rng, (n, 1, 128))
+    out = oracle.decode_attention(q, k, v, 1 / math.sqrt(128))
+    # remaining weight: (n-1) e^{-45.25} ~ 3.6e-16 of the total
+    np.testing.assert_allclose(out[0], widen(v[j, 0]), rtol=0, atol=1e-14)
+
+
+# 4. constant V, any keys -> that constant
+def test_constant_v():
+    rng = np.random.default_rng(4)
+    n = 777
+    q = rand_bits(rng, (4, 128), 3.0)
+    k = rand_bits(rng, (n, 1, 128))
+    vrow = rand_bits(rng, (1, 1, 128))
+    v = np.repeat(vrow, n, axis=0)
+    out = oracle.decode_attention(q, k, v, 1 / math.sqrt(128))
+    for h in range(4):
+        np.testing.assert_allclose(out[h], widen(vrow[0, 0]), rtol=1e-14, atol=1e-15)
+
+
+# 5. brute force: Decimal at 50 digits, naive softmax without max subtraction
+def _decimal_attention(q, k, v, scale, G):
+    getcontext().prec = 50
+    hq, d = q.shape
+    n = k.shape[0]
+    out = np.zeros((hq, d))
+    sc = Decimal(scale)
+    for h in range(hq):
+        g = h // G
+        e = []
+        for t in range(n):
+            s = sum(Decimal(float(q[h, i])) * Decimal(float(k[t, g, i])) for i in range(d))
+            e.append((s * sc).exp())
+        den = sum(e)
+        for i in range(d):
+            out[h, i] = float(sum(e[t] * Decimal(float(v[t, g, i])) for t in range(n)) / den)
+    return out
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_brute_force_decimal(trial):
+    rng = np.random.default_rng(100 + trial)
+    n = int(rng.integers(1, 9))
+    d = int(rng.integers(1, 9))
+    hkv = int(rng.integers(1, 3))
+    G = int(rng.choice([1, 2, 4]))
+    hq = hkv * G
+    q = rand_bits(rng, (hq, d), 2.0)
+    k = rand_bits(rng, (n, hkv, d), 2.0)
+    v = rand_bits(rng, (n, hkv, d))
+    scale = float(np.float32(1 / math.sqrt(d)))
+    got = oracle.decode_attention(q, k, v, scale)
+    ref = _decimal_attention(widen(q), widen(k), widen(v), scale, G)
+    np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-15)
+
+
+# library routine: torch SDPA in fp64 with HF repeat_kv (g = h // G) semantics
+@pytest.mark.parametrize("hq,hkv,n", [(32, 8, 300), (64, 8, 129), (32, 32, 17), (8, 1, 1000)])
+def test_against_torch_sdpa_fp64(hq, hkv, n):
+    rng = np.random.default_rng(hq * 1000 + n)
+    q = rand_bits(rng, (hq, 128))
+    k = rand_bits(rng, (n, hkv, 128))
+    v = rand_bits(rng, (n, hkv, 128))
+    scale = 1 / math.sqrt(128)
+    got = oracle.decode_attention(q, k, v, scale)
+    G = hq // hkv
+    tq = torch.from_numpy(widen(q))[:, None, :]                       # [Hq][1][D]
+    tk = torch.from_numpy(widen(k)).permute(1, 0, 2).repeat_interleave(G, 0)   # [Hq][n][D]
+    tv = torch.from_numpy(widen(v)).permute(1, 0, 2).repeat_interleave(G, 0)
+    ref = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, scale=scale)[:, 0].numpy()
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-13)
+
+
+# 6a. token-permutation invariance
+def test_token_permutation_invariance():
+    rng = np.random.default_rng(6)
+    n = 1000
+    q = rand_bits(rng, (8, 128), 2.0)
+    k = rand_bits(rng, (n, 2, 128))
+    v = rand_bits(rng, (n, 2, 128))
+    perm = rng.permutation(n)
+    a = oracle.decode_attention(q, k, v, 0.09)
+    b = oracle.decode_attention(q, k[perm], v[perm], 0.09)
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-14)
+
+
+# 6b. weights are non-negative and sum to 1
+def test_weights_sum_to_one():
+    rng = np.random.default_rng(7)
+    q = rand_bits(rng, (8, 128), 8.0)
+    k = rand_bits(rng, (513, 2, 128))
+    w = oracle.softmax_weights(q, k, 1 / math.sqrt(128))
+    assert (w >= 0).all()
+    np.testing.assert_allclose(w.sum(axis=1), 1.0, rtol=0, atol=1e-12)
+
+
+# 6c. partition independence + merge identity / commutativity
+def test_partition_independence_and_merge():
+    rng = np.random.default_rng(8)
+    n, hq, hkv = 2000, 8, 2
+    q = rand_bits(rng, (hq, 128), 4.0)
+    k = rand_bits(rng, (n, hkv, 128))
+    v = rand_bits(rng, (n, hkv, 128))
+    scale = 1 / math.sqrt(128)
+    full = oracle.decode_attention(q, k, v, scale)
+    for trial in range(5):
+        cuts = np.sort(rng.choice(np.arange(1, n), size=int(rng.integers(1, 12)), replace=False))
+        bounds = [0, *cuts.tolist(), n]
+        for h in (0, 5):
+            parts = [oracle.partial(q, k, v, h, bounds[i], bounds[i + 1], scale)
+                     for i in range(len(bounds) - 1)]
+            ms, ls, accs = zip(*parts)
+            merged = oracle.merge(ms, ls, np.stack(accs))
+            np.testing.assert_allclose(merged, full[h], rtol=1e-12, atol=1e-14)
+            perm = rng.permutation(len(parts))
+            merged_p = oracle.merge(np.array(ms)[perm], np.array(ls)[perm], np.stack(accs)[perm])
+            np.testing.assert_allclose(merged_p, merged, rtol=1e-12, atol=1e-14)
+    # identity: a single partial returns acc / l
+    m, l, acc = oracle.partial(q, k, v, 3, 0, n, scale)
+    np.testing.assert_allclose(oracle.merge([m], [l], acc[None]), acc / l, rtol=0, atol=0)
+    np.testing.assert_allclose(acc / l, full[3], rtol=1e-13, atol=1e-15)
+
+
+# 6d. GQA mapping g = floor(h / G) via KV heads with disjoint supports
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_gqa_disjoint_supports(G):
+    rng = np.random.default_rng(9 + G)
+    hkv, d, n = 4, 128, 64
+    hq = hkv * G
+    blk = d // hkv
+    q = rand_bits(rng, (hq, d))
+    k = rand_bits(rng, (n, hkv, d))
+    v = np.zeros((n, hkv, d), dtype=np.uint16)
+    for g in range(hkv):
+        v[:, g, g * blk:(g + 1) * blk] = rand_bits(rng, (n, blk))
+    out = oracle.decode_attention(q, k, v, 0.1)
+    for h in range(hq):
+        g = h // G
+        support = np.nonzero(out[h])[0]
+        assert support.min() >= g * blk and support.max() < (g + 1) * blk
+        single = oracle.decode_attention(q[h:h + 1], k[:, g:g + 1], v[:, g:g + 1], 0.1)
+        np.testing.assert_array_equal(out[h], single[0])
+
+
+def test_empty_context_is_zero():
+    q = np.full((4, 128), 0x3F80, dtype=np.uint16)
+    out = oracle.decode_attention(q, np.zeros((0, 1, 128), np.uint16), np.zeros((0, 1, 128), np.uint16), 0.1)
+    assert (out == 0).all()
+
+
+def test_shape_error():
+    q = np.zeros((3, 128), dtype=np.uint16)
+    k = np.zeros((4, 2, 128), dtype=np.uint16)
+    with pytest.raises(ValueError):
+        oracle.decode_attention(q, k, k, 0.1)
+
+
+# generator-built sink inputs: the dominant token-0 logit makes the output close to v_0
+def test_sink_variant_dominates():
+    hq, hkv, n = 32, 8, 300
+    q = q_bits(SEED, 0, [3], hq, 128)[0]
+    k = kv_bits(SEED, 0, KIND_K, 3, 0, n, hkv, 128, variant=VARIANT_SINK, hq_total=hq)
+    v = kv_bits(SEED, 0, KIND_V, 3, 0, n, hkv, 128)
+    w = oracle.softmax_weights(q, k, 1 / math.sqrt(128))
+    assert np.median(w[:, 0]) > 0.5
+
+
+# swap definition: brute-force loop over every element vs the numpy indexing
+def test_gather_pages_definition():
+    rng = np.random.default_rng(11)
+    L, NP, H, P, D = 3, 10, 2, 4, 8
+    pool = rng.integers(0, 65535, size=(L, 2, NP, H, P, D), dtype=np.uint16)
+    ids = [7, 2, 9]
+    rec = oracle.gather_pages(pool, ids, 1, 3)
+    assert rec.shape == (3, 2, 2, H, P, D)
+    for i, pid in enumerate(ids):
+        for l in range(1, 3):
+            for kv in range(2):
+                assert np.array_equal(rec[i, l - 1, kv], pool[l, kv, pid])
+    host = rng.integers(0, 65535, size=(6, L, 2, H, P, D), dtype=np.uint16)
+    hr = oracle.host_record(host, [5, 0], 0, 2)
+    assert np.array_equal(hr[0], host[5, 0:2]) and np.array_equal(hr[1], host[0, 0:2])
