@@ -1,0 +1,485 @@
+#!/usr/bin/env python
+"""bench.py -- NEO's GPU hot path on B200: batched paged GQA decode attention
+(+ KV page swap for c3) over synthetic LLaMa-shaped batches.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl neo|reference]
+
+One STEP = one decode iteration's attention for the whole model: one
+neo_decode_attn call per layer ("the GPU attention kernel is only invoked
+once per iteration" per layer), over the workload's batch, every layer reading
+its own KV pool (inputs >> 126 MB L2, so no flush is needed).
+
+Prints ONE JSON line (rank 0).  value = KV bytes read by all ranks / max-over-
+ranks device time, in GB/s (BASELINE.json metric); attended tokens/s rides
+along.  --impl reference times the fp64 CPU oracle on this box's host cores on a
+bounded sample of the same workload (no reference implementation exists; see
+DESIGN.md "Reference arm").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-attention KV GB/s (% of B200 HBM peak) and attended tokens/s @1/2/4/8 GPUs"
+NOMINAL_HBM_GBS = 8184.0          # 3996 MHz x 2 x 8192 bit / 8
+FALLBACK_HBM_GBS = 6650.0         # B200_PROFILING.md fallback
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c2", help="c1..c5 (BASELINE.json configs), c2s = skewed c2")
+    p.add_argument("--impl", default="neo", choices=["neo", "reference"])
+    p.add_argument("--chunk", type=int, default=0, help="split-K chunk tokens (0 = library default)")
+    p.add_argument("--fraction", type=float, default=1.0, help="c5: GPU-resident fraction f")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-swap", action="store_true", help="c3: skip the concurrent swap-out")
+    p.add_argument("--graph", action="store_true", help="capture the step's launches in a CUDA graph")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i] and "Not" not in r[5 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------- setup
+
+
+def shard_plan(wl, rank, world, fraction):
+    """(ctx_all, req_ids, kv_heads, q_heads, scaling, parallelism) for this rank."""
+    from paper_2411_01142_b200.shard import head_shard, lpt_assign
+    import neo_inputs as ni
+    if wl.name == "c4":                                   # tensor parallel by KV head
+        kvh, qh = head_shard(wl.hq, wl.hkv, rank, world)
+        return wl.contexts(), None, kvh, qh, "strong", f"tp{world} (kv-head sharded)"
+    if wl.name == "c5":                                   # GPU-resident share split by LPT (strong)
+        ctx = wl.contexts()
+        n_gpu = int(round(fraction * len(ctx)))
+        resident = np.arange(n_gpu)                       # first f*1024 by id
+        parts = lpt_assign(ctx[resident], world)
+        return ctx, resident[parts[rank]], None, None, "strong", f"dp{world} (LPT by request)"
+    # c1, c2, c3: weak scaling -- every rank serves its own full batch of distinct requests
+    if world == 1:
+        return wl.contexts(), None, None, None, "weak", "dp1"
+    k, a = wl.ctx_kind, wl.ctx_args
+    n = wl.batch * world
+    if k == "fixed":
+        ctx = np.full(n, a[0], dtype=np.int32)
+    elif k == "uniform":
+        ctx = ni.ctx_uniform(wl.seed, n, a[0])
+    elif k == "range":
+        ctx = ni.ctx_range(wl.seed, n, a[0], a[1])
+    elif k == "lognormal":
+        ctx = ni.ctx_lognormal(wl.seed, n, *a)
+    else:
+        ctx = ni.ctx_loguniform(wl.seed, n, *a)
+    return ctx, np.arange(rank * wl.batch, (rank + 1) * wl.batch), None, None, "weak", f"dp{world} (by request)"
+
+
+def layers_per_step(wl):
+    return wl.num_layers
+
+
+# --------------------------------------------------------------------- neo arm
+
+
+def run_neo(args):
+    import torch
+    import torch.distributed as dist
+
+    from neo_inputs.gpu import GpuBatch
+    from neo_inputs.workloads import WORKLOADS
+    from paper_2411_01142_b200 import neo
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and rank == 0:
+        print(f"note: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = WORKLOADS[args.config]
+    ctx_all, req_ids, kvh, qh, scaling, par = shard_plan(wl, rank, world, args.fraction)
+    gb = GpuBatch(wl, ctx=ctx_all, req_ids=req_ids, kv_heads=kvh, q_heads=qh)
+    L = layers_per_step(wl)
+    stream = torch.cuda.current_stream()
+    chunk = args.chunk or neo.default_chunk(gb.B, gb.hkv, gb.max_seq_len)
+    ws = neo.make_workspace(gb.B, gb.hq, gb.hkv, gb.max_seq_len, chunk)
+    out = torch.empty(L, gb.B, gb.hq, 128, dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+
+    def step(events=None):
+        for l in range(L):
+            k, v = gb.layer(l)
+            neo.decode_attn(gb.q[l % gb.layers], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=out[l],
+                            chunk_tokens=chunk, workspace=ws, stream=stream)
+            if events is not None:
+                events[l].record(stream)
+
+    graph = None
+    if args.graph:
+        step()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step() if graph is None else graph.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    per = [[torch.cuda.Event(enable_timing=True) for _ in range(L)] for _ in range(args.steps)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev0.record(stream)
+    for s in range(args.steps):
+        starts[s].record(stream)
+        if graph is None:
+            step(per[s])
+        else:
+            graph.replay()
+            per[s][-1].record(stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    t_ms = ev0.elapsed_time(ev1)
+    # per-launch durations of the attention kernel (back-to-back launches on one stream)
+    launch_ms = []
+    for s in range(args.steps):
+        if graph is None:
+            prev = starts[s]
+            for l in range(L):
+                launch_ms.append(prev.elapsed_time(per[s][l]))
+                prev = per[s][l]
+        else:
+            launch_ms.append(starts[s].elapsed_time(per[s][-1]) / L)
+    t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    kv_local = gb.kv_bytes_per_call() * L * args.steps
+    tok_local = int(gb.ctx.astype(np.int64).sum()) * L * args.steps
+    tot = torch.tensor([kv_local, tok_local], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if scaling == "strong" and wl.name == "c4":
+            # head sharding: each (request, token, layer) is attended once over all ranks
+            tok = torch.tensor([float(tok_local)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tot[:1], op=dist.ReduceOp.SUM)
+            tot[1] = tok[0]
+        else:
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    t_max = float(t.item()) / 1e3
+    kv_total, tok_total = float(tot[0].item()), float(tot[1].item())
+    value = kv_total / t_max / 1e9
+    avg_launch = float(np.mean(launch_ms)) / 1e3
+    hbm_peak, peak_src = peaks()
+    algo = gb.kv_bytes_per_call() + gb.other_bytes_per_call()
+    achieved = algo / avg_launch / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config)
+        except Exception:
+            traffic = None
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, gb, L, chunk, ws, stream, world, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(gb, target_s=10.0)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(value, 2),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(t_max * 1e3 / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": scaling,
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (counter-based generator, LLaMa shapes; no weights needed)",
+            "attended_tokens_per_s": round(tok_total / t_max, 1),
+            "pct_of_measured_hbm": round(100 * value / world / hbm_peak, 2),
+            "pct_of_nominal_hbm": round(100 * value / world / NOMINAL_HBM_GBS, 2),
+            "config": {
+                "workload": f"{wl.name}: {wl.model} {wl.note}",
+                "batch": int(gb.B if wl.name == "c4" else gb.B * world) if wl.name != "c5" else int(
+                    round(args.fraction * len(ctx_all))),
+                "batch_per_rank": gb.B,
+                "q_heads": wl.hq, "kv_heads": wl.hkv, "head_dim": 128, "page_size": wl.page_size,
+                "seq_len_mean": round(float(gb.ctx.mean()), 1), "seq_len_min": int(gb.ctx.min()),
+                "seq_len_max": int(gb.ctx.max()),
+                "layers_per_step": L, "distinct_layer_pools": gb.layers,
+                "chunk_tokens": chunk, "parallelism": par,
+                "l2": f"inputs {gb.layers * gb.kv_bytes_per_call() / 1e9:.1f} GB of KV cycled per step >> 126 MB L2; "
+                      "no flush" if gb.layers * gb.kv_bytes_per_call() > 1e9 else "L2 not flushed (small config)",
+                "cuda_graph": bool(graph is not None),
+            },
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                         "kernel": "decode_attn_kernel", "avg_launch_us": round(avg_launch * 1e6, 2),
+                         "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
+            "gpu_launches": L * args.steps,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
+    """The same metric end to end through the public API: per step, H2D of the
+    step's inputs (q of every layer, block table, seq_lens) from pinned host,
+    L attention calls, D2H of every layer's output into pinned host."""
+    import torch
+
+    from paper_2411_01142_b200 import neo
+    q_host = torch.empty((L, gb.B, gb.hq, 128), dtype=torch.bfloat16).pin_memory()
+    for l in range(L):
+        q_host[l].copy_(gb.q[l % gb.layers])
+    bt_host = gb.block_table.cpu().pin_memory()
+    sl_host = gb.seq_lens.cpu().pin_memory()
+    out_host = torch.empty((L, gb.B, gb.hq, 128), dtype=torch.bfloat16).pin_memory()
+    q_dev = torch.empty_like(q_host, device="cuda")
+    bt_dev = torch.empty_like(bt_host, device="cuda")
+    sl_dev = torch.empty_like(sl_host, device="cuda")
+    out_dev = torch.empty_like(out_host, device="cuda")
+
+    def step():
+        q_dev.copy_(q_host, non_blocking=True)
+        bt_dev.copy_(bt_host, non_blocking=True)
+        sl_dev.copy_(sl_host, non_blocking=True)
+        for l in range(L):
+            k, v = gb.layer(l)
+            neo.decode_attn(q_dev[l], k, v, bt_dev, sl_dev, gb.max_seq_len, out=out_dev[l], chunk_tokens=chunk,
+                            workspace=ws, stream=stream)
+        out_host.copy_(out_dev, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+    kv = torch.tensor([float(gb.kv_bytes_per_call() * L * args.steps)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(kv, op=dist.ReduceOp.SUM)
+    h2d = q_host.numel() * 2 + bt_host.numel() * 4 + sl_host.numel() * 4
+    return {"value": round(float(kv.item()) / float(t.item()) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_host.numel() * 2),
+            "ms_per_step": round(float(t.item()) * 1e3 / args.steps, 4)}
+
+
+# ------------------------------------------------------------- CPU oracle legs
+
+
+def ncores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample_inputs(wl, ctx, req_ids, layer, heads=None, qheads=None):
+    import neo_inputs as ni
+    qs, ks, vs = [], [], []
+    kvh = np.arange(*(heads or (0, wl.hkv)))
+    qh = np.arange(*(qheads or (0, wl.hq)))
+    for b in req_ids:
+        n = int(ctx[b])
+        qs.append(ni.q_bits(wl.seed, layer, [int(b)], wl.hq, 128, heads=qh)[0])
+        ks.append(ni.kv_bits(wl.seed, layer, ni.KIND_K, int(b), 0, n, wl.hkv, 128, heads=kvh))
+        vs.append(ni.kv_bits(wl.seed, layer, ni.KIND_V, int(b), 0, n, wl.hkv, 128, heads=kvh))
+    return np.stack(qs), ks, vs
+
+
+def cpu_baseline(gb, target_s=10.0):
+    """The fp64 oracle (as it stands) on this box's host cores over a bounded
+    sample of the same workload: requests of layer 0, threads over requests."""
+    import oracle
+    wl = gb.wl
+    ids_local = np.arange(gb.B)
+    gids = gb.req_ids
+    nth = ncores()
+    ctx_g = np.zeros(int(gids.max()) + 1, dtype=np.int64)
+    ctx_g[gids] = gb.ctx
+    # calibrate on a few requests, then size the sample for ~target_s
+    cal = gids[:max(1, min(len(gids), nth))]
+    q, k, v = oracle_sample_inputs(wl, ctx_g, cal, 0, gb.kv_heads, gb.q_heads)
+    t0 = time.time()
+    oracle.decode_attention_batch(q, k, v, 1 / math.sqrt(128), nthreads=nth)
+    dt = max(time.time() - t0, 1e-3)
+    tok_per_s = float(ctx_g[cal].sum()) / dt
+    want_tokens = tok_per_s * target_s
+    cum = np.cumsum(gb.ctx)
+    n = int(min(len(ids_local), max(len(cal), np.searchsorted(cum, want_tokens) + 1)))
+    sample = gids[:n]
+    q, k, v = oracle_sample_inputs(wl, ctx_g, sample, 0, gb.kv_heads, gb.q_heads)
+    t0 = time.time()
+    oracle.decode_attention_batch(q, k, v, 1 / math.sqrt(128), nthreads=nth)
+    dt = time.time() - t0
+    toks = int(ctx_g[sample].sum())
+    kvb = toks * gb.hkv * 128 * 2 * 2
+    return {"value": round(kvb / dt / 1e9, 4), "unit": "GB/s", "cores": nth, "kind": "oracle",
+            "sample": f"{n} of {gb.B} requests of layer 0 ({toks} tokens, {kvb / 1e9:.2f} GB of KV), fp64 C, "
+                      f"pthreads over requests; {cpu_model()}",
+            "attended_tokens_per_s": round(toks / dt, 1), "seconds": round(dt, 2)}
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle, timed on the host cores, on the same
+    config/metric; each step a bounded sample of the workload (layer = step % L)."""
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    import oracle
+    from neo_inputs.workloads import WORKLOADS
+    wl = WORKLOADS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", args.gpus))
+    ctx_all, req_ids, kvh, qh, scaling, par = shard_plan(wl, 0, 1, args.fraction)
+    ids = np.arange(len(ctx_all)) if req_ids is None else req_ids
+    nth = ncores()
+    total_budget = 150.0
+    per_step = max(0.5, total_budget / max(1, args.steps + args.warmup))
+    cal = ids[:max(1, min(len(ids), nth))]
+    q, k, v = oracle_sample_inputs(wl, ctx_all, cal, 0, kvh, qh)
+    t0 = time.time()
+    oracle.decode_attention_batch(q, k, v, 1 / math.sqrt(128), nthreads=nth)
+    tok_rate = float(ctx_all[cal].sum()) / max(time.time() - t0, 1e-3)
+    cum = np.cumsum(ctx_all[ids])
+    n = int(min(len(ids), max(len(cal), np.searchsorted(cum, tok_rate * per_step) + 1)))
+    sample = ids[:n]
+    hkv = wl.hkv if kvh is None else kvh[1] - kvh[0]
+    L = layers_per_step(wl)
+    inputs = [oracle_sample_inputs(wl, ctx_all, sample, l, kvh, qh) for l in range(min(L, 2))]
+    for s in range(args.warmup):
+        q, k, v = inputs[s % len(inputs)]
+        oracle.decode_attention_batch(q, k, v, 1 / math.sqrt(128), nthreads=nth)
+    t0 = time.time()
+    for s in range(args.steps):
+        q, k, v = inputs[s % len(inputs)]
+        oracle.decode_attention_batch(q, k, v, 1 / math.sqrt(128), nthreads=nth)
+    dt = time.time() - t0
+    toks = int(ctx_all[sample].sum()) * args.steps
+    kvb = toks * hkv * 128 * 2 * 2
+    value = kvb / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 3),
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (same generator and workload as the neo arm)",
+        "attended_tokens_per_s": round(toks / dt, 1),
+        "config": {"workload": f"{wl.name}: {wl.model} {wl.note}", "parallelism": "host cores (no GPU)",
+                   "sample_requests": int(n), "batch": int(len(ids))},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": nth, "kind": "oracle",
+                         "sample": f"{n} of {len(ids)} requests per step (one layer), fp64 C oracle, {cpu_model()}"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_neo(args)
+
+
+if __name__ == "__main__":
+    main()

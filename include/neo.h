@@ -1,0 +1,205 @@
+/*
+ * neo.h -- C ABI of libneo, the B200 (sm_100a) hot path of NEO
+ * (arXiv 2411.01142, "NEO: Saving GPU Memory Crisis with CPU Offloading for
+ * Online LLM Inference").  Citations: P:n = PAPER.md line n, S:n = SPEC.md
+ * line n.
+ *
+ * What crosses this boundary:
+ *   - a paged KV cache split into a GPU-cache (HBM) and a CPU-cache (pinned
+ *     host memory); every prefilled request lives entirely in one of them
+ *     (Sec 3.1 "partial offloading");
+ *   - one batched decode-attention call per layer per iteration covering the
+ *     whole GPU sub-batch (attention semantics P:97-98);
+ *   - the page swap that moves a request's KV between the two caches for a
+ *     range of layers (P:240 layer-wise swapping, P:285-288 scheduling steps
+ *     2, 3, 5; PCIe-bound per P:121).
+ *
+ * Conventions (all calls):
+ *   - Every call returns neo_status.  NEO_OK = 0.  neo_last_error() returns a
+ *     thread-local human-readable message for the last failing call.
+ *   - All-or-nothing: a non-OK return has enqueued no GPU work and changed no
+ *     pool state (mirrors S:262, S:292 atomicity).
+ *   - Ownership: the CALLER allocates and owns every device buffer (pool, q,
+ *     out, workspace, staging) and the pinned host pool; the library never
+ *     allocates or frees device memory.  Pointers must stay valid until the
+ *     work enqueued on them has completed.  A pool handle owns only host-side
+ *     free lists and is single-writer.
+ *   - Asynchrony: attention and swap calls validate host-visible arguments,
+ *     enqueue on the given stream and return without synchronising.  Device
+ *     contents (seq_lens, block-table ids) are validated only when the
+ *     environment variable NEO_DEBUG_VALIDATE=1 is set; that path synchronises
+ *     the stream.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - No C++ exception crosses the ABI.
+ *   - Element type of q, out and the KV pages is bf16 (IEEE binary16 brain
+ *     float, passed as raw 16-bit words); arithmetic is fp32 (DESIGN.md c7).
+ */
+#ifndef NEO_H_
+#define NEO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define NEO_API __attribute__((visibility("default")))
+#else
+#define NEO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NEO_OK = 0,
+  NEO_ERR_INVALID_ARG = 1,  /* null/misaligned pointer, bad shape, bad id, range error */
+  NEO_ERR_OUT_OF_PAGES = 2, /* allocation cannot be satisfied; nothing allocated       */
+  NEO_ERR_UNSUPPORTED = 3,  /* head_dim != 128, page_size not a multiple of 16, G > 8  */
+  NEO_ERR_CUDA = 4,         /* a CUDA runtime/driver call failed                        */
+  NEO_ERR_INTERNAL = 5
+} neo_status;
+
+enum { NEO_GPU = 0, NEO_HOST = 1 };
+
+/* Thread-local message describing the last non-OK return on this thread. */
+NEO_API const char* neo_last_error(void);
+NEO_API const char* neo_version(void);
+
+/* ------------------------------------------------------------------ KV pool
+ * Geometry of one model's KV cache ("paged KV cache similar to vLLM").
+ *
+ * GPU-cache layout (layer-major), bf16:
+ *     gpu[L][2 (K,V)][num_gpu_pages][Hkv][P][D]
+ *   so one (page, kv-head) block is a contiguous P*D*2-byte run (4 KiB at
+ *   P=16, D=128) and a layer's K view is [num_gpu_pages][Hkv][P][D] with
+ *   page_stride = Hkv*P*D elements.
+ * CPU-cache layout (page-major, each page self-contained across layers), bf16:
+ *     host[num_host_pages][L][2 (K,V)][Hkv][P][D]
+ *   i.e. the same per-(layer, K|V) byte layout, ready for a CPU attention
+ *   kernel over host pages (out of scope here). */
+typedef struct {
+  int32_t num_layers;   /* L  >= 1                      */
+  int32_t num_kv_heads; /* Hkv >= 1 (local to this rank) */
+  int32_t head_dim;     /* D, must be 128                */
+  int32_t page_size;    /* P tokens per page, multiple of 16 (16 or 32 typical) */
+  int64_t num_gpu_pages;
+  int64_t num_host_pages;
+} neo_kv_geometry;
+
+typedef struct neo_kv_pool neo_kv_pool;
+
+/* Bytes the caller must provide for the two caches of `geo`. */
+NEO_API neo_status neo_kv_pool_bytes(const neo_kv_geometry* geo, size_t* gpu_bytes, size_t* host_bytes);
+
+/* Create a pool over caller-owned memory.  gpu_kv_base: device pointer,
+ * >= gpu_bytes, 16-byte aligned.  host_kv_base: PINNED host pointer (page-locked
+ * via cudaHostAlloc / torch pin_memory), >= host_bytes, 16-byte aligned; may be
+ * NULL iff num_host_pages == 0.  The handle is written to *out. */
+NEO_API neo_status neo_kv_pool_create(const neo_kv_geometry* geo, void* gpu_kv_base, size_t gpu_bytes,
+                                      void* host_kv_base, size_t host_bytes, neo_kv_pool** out);
+NEO_API void neo_kv_pool_destroy(neo_kv_pool* pool);
+
+/* Allocate n_pages page ids in `where` (NEO_GPU or NEO_HOST) into the host
+ * array page_ids_out[n_pages].  All-or-nothing: NEO_ERR_OUT_OF_PAGES leaves the
+ * pool unchanged (S:255-263 allocate; S:265-273 extend = alloc(1)).  Host ids
+ * are returned as one ascending contiguous run when one exists, so a swap is a
+ * single strided memcpy.  n_pages == 0 is a no-op. */
+NEO_API neo_status neo_kv_alloc(neo_kv_pool* pool, int32_t where, int32_t n_pages, int32_t* page_ids_out);
+
+/* Return pages to `where`.  Every id must be currently allocated there and
+ * appear once; otherwise NEO_ERR_INVALID_ARG and nothing is freed
+ * (S:285-288 release). */
+NEO_API neo_status neo_kv_free(neo_kv_pool* pool, int32_t where, int32_t n_pages, const int32_t* page_ids);
+
+/* Number of free pages in `where` (conservation: free + allocated = capacity). */
+NEO_API neo_status neo_kv_free_count(const neo_kv_pool* pool, int32_t where, int64_t* n_free);
+
+/* Device pointers of layer `layer`'s K and V page arrays and their page stride
+ * in elements, for neo_decode_attn. */
+NEO_API neo_status neo_kv_layer_view(const neo_kv_pool* pool, int32_t layer, void** k_pages, void** v_pages,
+                                     int64_t* page_stride_elems);
+
+/* --------------------------------------------------------- decode attention
+ * One decode step of GQA attention for a batch of GPU-resident requests
+ * (P:97-98):
+ *
+ *   for b < batch, h < Hq:   g = floor(h / G), G = Hq / Hkv        (DESIGN c2)
+ *     out[b][h][:] = sum_t softmax_t(scale * q[b][h] . K_b[t][g]) * V_b[t][g][:]
+ *   over ALL t < seq_lens[b] (the caller has already appended this step's token;
+ *   no causal mask, no window; DESIGN c3).  K_b[t] lives at token t % P of
+ *   physical page block_table[b][t / P].
+ *
+ * Arguments:
+ *   q           [batch][Hq][D] bf16, device, 16-byte aligned.
+ *   k_pages,
+ *   v_pages     device; page p, kv-head g starts at element p*page_stride + g*P*D
+ *               and holds [P][D] bf16 (token-major).  16-byte aligned, page_stride
+ *               a multiple of 8 elements and >= Hkv*P*D.
+ *   num_pages   pages addressable through k_pages/v_pages (ids must be < num_pages).
+ *   block_table [batch][max_blocks] int32, device.  Entries at or beyond
+ *               ceil(seq_lens[b]/P) are never read (may be -1); a physical page may
+ *               appear in several rows (read-only sharing; DESIGN c10).
+ *   seq_lens    [batch] int32, device, each in [0, min(max_seq_len, max_blocks*P)].
+ *               0 yields a zero output row (DESIGN c4).
+ *   out         [batch][Hq][D] bf16, device (fp32 -> bf16 round-to-nearest-even).
+ *   max_seq_len host-known upper bound of seq_lens (sizes the grid).
+ *   scale       softmax scale, typically 1/sqrt(D) (DESIGN c1).
+ *   chunk_tokens split-K chunk length C (multiple of 16 and of P, <= 512), or 0 for
+ *               the library default neo_decode_attn_default_chunk().  The result for
+ *               request b depends only on (its inputs, C): outputs are bitwise
+ *               deterministic run to run (fixed merge order, no float atomics).
+ *   workspace   device scratch of >= neo_decode_attn_workspace_bytes(...) bytes,
+ *               initialised ONCE with neo_decode_attn_workspace_init(); the kernel
+ *               leaves it re-usable.  One workspace per concurrently running stream.
+ * Errors: NEO_ERR_INVALID_ARG (nulls, misalignment, Hq % Hkv != 0, max_seq_len >
+ * max_blocks*P, workspace too small); NEO_ERR_UNSUPPORTED (D != 128, P % 16 != 0,
+ * G > 8, C invalid); NEO_ERR_CUDA.  batch == 0 is a no-op. */
+NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+                                   int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
+                                   const int32_t* seq_lens, void* out, int32_t batch, int32_t num_q_heads,
+                                   int32_t num_kv_heads, int32_t head_dim, int32_t page_size, int32_t max_seq_len,
+                                   float scale, int32_t chunk_tokens, void* workspace, size_t workspace_bytes,
+                                   void* stream);
+
+/* Default split-K chunk length for a call shape (deterministic in its inputs). */
+NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
+
+/* Workspace bytes for a call shape (chunk_tokens 0 = default). */
+NEO_API neo_status neo_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                                                   int32_t head_dim, int32_t max_seq_len, int32_t chunk_tokens,
+                                                   size_t* bytes);
+
+/* Zero the workspace's completion counters (enqueued on `stream`).  Call once
+ * after allocating a workspace. */
+NEO_API neo_status neo_decode_attn_workspace_init(void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------ swap
+ * Swap-out (GPU-cache -> CPU-cache) of n_pages pages for layers
+ * [layer_begin, layer_end):
+ *   host[host_page_ids[i]][l][kv] = gpu[l][kv][gpu_page_ids[i]]  for every i, l, kv
+ * bit-exactly.  gpu_page_ids must be allocated in NEO_GPU, host_page_ids in
+ * NEO_HOST (host arrays, n_pages entries each, no duplicates).  A gather kernel
+ * packs the pages into `staging` (device, 16-byte aligned) and cudaMemcpyAsync
+ * moves them device->host, all on `stream`; staging smaller than the whole
+ * transfer is reused chunk by chunk (it must hold at least one page's layer
+ * range: neo_kv_swap_staging_bytes(pool, 1, ...)).  The call does NOT free the
+ * GPU pages: record an event on `stream` and free them after it completes.  The
+ * caller orders the call after the kernels that wrote those pages.
+ * Swap-in is the mirror image (host -> staging -> scatter into gpu_page_ids,
+ * which may differ from the ids the request had before). */
+NEO_API neo_status neo_kv_swap_out(neo_kv_pool* pool, int32_t n_pages, const int32_t* gpu_page_ids,
+                                   const int32_t* host_page_ids, int32_t layer_begin, int32_t layer_end,
+                                   void* staging, size_t staging_bytes, void* stream);
+NEO_API neo_status neo_kv_swap_in(neo_kv_pool* pool, int32_t n_pages, const int32_t* host_page_ids,
+                                  const int32_t* gpu_page_ids, int32_t layer_begin, int32_t layer_end,
+                                  void* staging, size_t staging_bytes, void* stream);
+
+/* Staging bytes that let a swap of n_pages over the layer range run in one chunk. */
+NEO_API neo_status neo_kv_swap_staging_bytes(const neo_kv_pool* pool, int32_t n_pages, int32_t layer_begin,
+                                             int32_t layer_end, size_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NEO_H_ */

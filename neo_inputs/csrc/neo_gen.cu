@@ -122,9 +122,11 @@ __global__ void values_kernel(uint64_t seed, uint32_t tid, const uint64_t* idx, 
 
 }  // namespace
 
+#define GEN_API __attribute__((visibility("default")))
+
 extern "C" {
 
-int neo_gen_fill_kv(void* k_pages, void* v_pages, int64_t page_stride, const int32_t* block_table,
+GEN_API int neo_gen_fill_kv(void* k_pages, void* v_pages, int64_t page_stride, const int32_t* block_table,
                     int32_t max_blocks, const int32_t* seq_lens, int32_t batch, int32_t b_offset,
                     int32_t hkv, int32_t g_offset, int32_t hkv_total, int32_t hq_total, int32_t d,
                     int32_t page_size, uint64_t seed, int32_t layer, int32_t variant,
@@ -138,7 +140,7 @@ int neo_gen_fill_kv(void* k_pages, void* v_pages, int64_t page_stride, const int
   return (int)cudaGetLastError();
 }
 
-int neo_gen_fill_q(void* q, int32_t batch, int32_t b_offset, int32_t hq, int32_t h_offset,
+GEN_API int neo_gen_fill_q(void* q, int32_t batch, int32_t b_offset, int32_t hq, int32_t h_offset,
                    int32_t hq_total, int32_t d, uint64_t seed, int32_t layer, int32_t variant,
                    void* stream) {
   if (batch <= 0) return 0;
@@ -147,7 +149,7 @@ int neo_gen_fill_q(void* q, int32_t batch, int32_t b_offset, int32_t hq, int32_t
   return (int)cudaGetLastError();
 }
 
-int neo_gen_values(uint64_t seed, uint32_t tid, const uint64_t* idx, int64_t n, uint16_t* out,
+GEN_API int neo_gen_values(uint64_t seed, uint32_t tid, const uint64_t* idx, int64_t n, uint16_t* out,
                    void* stream) {
   if (n <= 0) return 0;
   values_kernel<<<256, 256, 0, (cudaStream_t)stream>>>(seed, tid, idx, n, out);

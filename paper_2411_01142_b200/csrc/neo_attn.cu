@@ -1,0 +1,473 @@
+// Split-K paged GQA decode attention for sm_100a (NEO's GPU attention, P:246,
+// P:303; flash-decoding partition + aggregate).
+//
+// Work unit = (request b, kv-head g, chunk c of C tokens), one WARP per unit,
+// kWarps independent warps per CTA.  Each warp runs its own kStages-deep ring
+// of TMA tensor loads (cp.async.bulk.tensor, 128B swizzle, L2 evict_first)
+// completing on per-stage mbarriers; one 16-token tile = the K block and V block
+// of one (page, kv-head), 4 KiB each.
+//
+// Math per tile (fp32 accumulate of exact bf16 products):
+//   S^T[16 tok x 8 heads] = K_tile[16 x 128] . Q^T[128 x 8]        8x mma.m16n8k16
+//   online softmax in the exp2 domain (scale*log2e folded into the scores)
+//   O^T[128 x 8] += V^T[128 x 16] . P^T[16 x 8]                    8x2 mma.m16n8k16
+// P is split into bf16 hi + lo parts (two MMAs) so the P.V product keeps ~16
+// mantissa bits (a bf16-only P fails the tolerance).
+// Fragments are read straight from the swizzled tiles with LDS.128; the token
+// permutation PI and the dim assignment below make every read conflict-free
+// (checked by tools/check_banks.py).  P goes from the S^T accumulator layout to
+// the B-operand layout with movmatrix.trans (no shared-memory round trip).
+//
+// Single-chunk units write the bf16 output directly; multi-chunk units write an
+// fp32 partial (acc, m, l) to the workspace, and the LAST warp to finish a
+// (b, g) -- detected with a per-(b, g) counter -- merges the partials in chunk
+// order (deterministic, no float atomics) and resets the counter.
+#include <cuda_bf16.h>
+
+#include "neo_internal.cuh"
+
+namespace neo {
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kStages = 4;
+constexpr int kStageBytes = 2 * kTileBytes;
+constexpr int kSmemBytes = kWarps * kStages * kStageBytes + 1024;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct KArgs {
+  const uint16_t* q;
+  uint16_t* out;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  float* ws_acc;
+  float2* ws_ml;
+  int32_t* ws_cnt;
+  int32_t batch, hq, hkv, G, page_size, max_blocks, chunk_tiles, max_chunks;
+  float scale_log2;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void tma_load_tile(uint32_t dst, const CUtensorMap* tm, int tok, int g, int page,
+                                              uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(0), "r"(0), "r"(tok), "r"(g), "r"(page), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint32_t word(const uint4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// Byte offset of 16-byte chunk `c` (0..15) of token `t` inside a tile that TMA
+// wrote with box {64, 2, 16} and CU_TENSOR_MAP_SWIZZLE_128B: 128-byte row
+// R = 2t + c/8, chunk slot (c % 8) XOR (R % 8).
+__device__ __forceinline__ uint32_t swz(int t, int c) {
+  const int R = 2 * t + (c >> 3);
+  return static_cast<uint32_t>(R * 128 + (((c & 7) ^ (R & 7)) << 4));
+}
+
+// Token held by MMA row rho (0..7); rows 8..15 hold 8 + PI(rho - 8).
+__device__ __forceinline__ int tok_pi(int rho) { return (rho & 1) ? 4 + ((rho >> 1) ^ 2) : (rho >> 1); }
+
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t movtrans(uint32_t x) {
+  uint32_t r;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+__device__ __forceinline__ void store_row8(uint16_t* dst, const float (&v)[8], float inv) {
+  uint4 w;
+  w.x = pack_bf16(v[0] * inv, v[1] * inv);
+  w.y = pack_bf16(v[2] * inv, v[3] * inv);
+  w.z = pack_bf16(v[4] * inv, v[5] * inv);
+  w.w = pack_bf16(v[6] * inv, v[7] * inv);
+  *reinterpret_cast<uint4*>(dst) = w;
+}
+
+__global__ void __launch_bounds__(kWarps * 32)
+    decode_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                       const KArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2;   // MMA groupID
+  const int qd = lane & 3;   // MMA thread-in-group
+
+  const int64_t unit = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
+  const int c = static_cast<int>(unit / BH);
+  if (c >= a.max_chunks) return;
+  const int bg = static_cast<int>(unit - static_cast<int64_t>(c) * BH);
+  const int b = bg / a.hkv;
+  const int g = bg - b * a.hkv;
+  const int G = a.G;
+
+  const int ctx = __ldg(a.seq_lens + b);
+  if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
+    if (c == 0) {
+      uint16_t* o = a.out + (static_cast<int64_t>(b) * a.hq + g * G) * kHeadDim;
+      for (int e = lane * 8; e < G * kHeadDim; e += 32 * 8) *reinterpret_cast<uint4*>(o + e) = make_uint4(0, 0, 0, 0);
+    }
+    return;
+  }
+  const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
+  const int n_chunks = (ntile_total + a.chunk_tiles - 1) / a.chunk_tiles;
+  if (c >= n_chunks) return;
+  const int t_begin = c * a.chunk_tiles;
+  const int nt = min(a.chunk_tiles, ntile_total - t_begin);
+
+  // block-table walk (a1): lane i holds the physical page of tile i of the unit
+  int my_pid = 0;
+  if (lane < nt) {
+    const int tok = (t_begin + lane) * kTileTokens;
+    my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + tok / a.page_size);
+  }
+
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
+  const uint32_t bar0 = smem_u32(&bars[warp][0]);
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const uint64_t policy = evict_first_policy();
+
+  // KV stream (a2): tile j of the unit -> stage j % kStages
+  auto issue = [&](int j) {
+    const int pid = __shfl_sync(kFull, my_pid, j);
+    if (lane == 0) {
+      const int s = j % kStages;
+      const int tok_in_page = ((t_begin + j) * kTileTokens) % a.page_size;
+      const uint32_t bar = bar0 + 8 * s;
+      const uint32_t dst = sbase + s * kStageBytes;
+      mbar_arrive_expect_tx(bar, kStageBytes);
+      tma_load_tile(dst, &tmk, tok_in_page, g, pid, bar, policy);
+      tma_load_tile(dst + kTileBytes, &tmv, tok_in_page, g, pid, bar, policy);
+    }
+  };
+  const int npro = nt < kStages ? nt : kStages;
+  for (int j = 0; j < npro; ++j) issue(j);
+
+  // Q fragment (B operand of S^T = K Q^T): head r of the group, dims of chunks
+  // qd + 4i in the same order as the K registers.  Heads r >= G are zero.
+  uint4 qf[4];
+  if (r < G) {
+    const uint16_t* qp = a.q + (static_cast<int64_t>(b) * a.hq + g * G + r) * kHeadDim;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qf[i] = __ldg(reinterpret_cast<const uint4*>(qp + 8 * (qd + 4 * i)));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) qf[i] = make_uint4(0, 0, 0, 0);
+  }
+
+  float o[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  const int tokA = tok_pi(r), tokB = 8 + tokA;              // S^T rows r, r+8
+  const int vt0 = tok_pi(2 * qd), vt1 = tok_pi(2 * qd + 1);  // P.V k-slots 2qd, 2qd+1 (+8)
+  const float sl2 = a.scale_log2;
+
+  for (int j = 0; j < nt; ++j) {
+    const int s = j % kStages;
+    mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
+    const uint32_t sk = sbase + s * kStageBytes;
+    const uint32_t sv = sk + kTileBytes;
+
+    // (a3) scores: S^T = K_tile . Q^T
+    uint4 ka[4], kb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      ka[i] = lds128(sk + swz(tokA, qd + 4 * i));
+      kb[i] = lds128(sk + swz(tokB, qd + 4 * i));
+    }
+    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int i = jj >> 1, w = 2 * (jj & 1);
+      mma_bf16(sc, word(ka[i], w), word(kb[i], w), word(ka[i], w + 1), word(kb[i], w + 1), word(qf[i], w),
+               word(qf[i], w + 1));
+    }
+    // V fragments: tokens vt0, vt1, vt0+8, vt1+8; chunks r and r+8
+    uint4 v00 = lds128(sv + swz(vt0, r)), v01 = lds128(sv + swz(vt0, r + 8));
+    uint4 v10 = lds128(sv + swz(vt1, r)), v11 = lds128(sv + swz(vt1, r + 8));
+    uint4 v20 = lds128(sv + swz(vt0 + 8, r)), v21 = lds128(sv + swz(vt0 + 8, r + 8));
+    uint4 v30 = lds128(sv + swz(vt1 + 8, r)), v31 = lds128(sv + swz(vt1 + 8, r + 8));
+
+    float x0 = sc[0] * sl2, x1 = sc[1] * sl2, x2 = sc[2] * sl2, x3 = sc[3] * sl2;
+    const int valid = ctx - (t_begin + j) * kTileTokens;  // >= 1
+    if (valid < kTileTokens) {                            // ragged last tile: mask scores, zero V
+      const uint4 z = make_uint4(0, 0, 0, 0);
+      if (tokA >= valid) x0 = x1 = -INFINITY;
+      if (tokB >= valid) x2 = x3 = -INFINITY;
+      if (vt0 >= valid) v00 = v01 = z;
+      if (vt1 >= valid) v10 = v11 = z;
+      if (vt0 + 8 >= valid) v20 = v21 = z;
+      if (vt1 + 8 >= valid) v30 = v31 = z;
+    }
+
+    // (a4) online softmax; token 0 of every tile is valid, so the tile max is finite
+    float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, off));
+      mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, off));
+    }
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    if (__any_sync(kFull, (mn0 > m0) || (mn1 > m1))) {
+      const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        o[i][0] *= al0;
+        o[i][2] *= al0;
+        o[i][1] *= al1;
+        o[i][3] *= al1;
+      }
+      l0 *= al0;
+      l1 *= al1;
+      m0 = mn0;
+      m1 = mn1;
+    }
+    const float p0 = ex2(x0 - m0), p1 = ex2(x1 - m1), p2 = ex2(x2 - m0), p3 = ex2(x3 - m1);
+    l0 += p0 + p2;
+    l1 += p1 + p3;
+    const uint32_t ht = pack_bf16(p0, p1), hb = pack_bf16(p2, p3);
+    const uint32_t lt = pack_bf16(p0 - bf_lo(ht), p1 - bf_hi(ht));
+    const uint32_t lb = pack_bf16(p2 - bf_lo(hb), p3 - bf_hi(hb));
+    const uint32_t bh0 = movtrans(ht), bh1 = movtrans(hb), bl0 = movtrans(lt), bl1 = movtrans(lb);
+
+    // (a5) O^T += V^T . P^T  (hi and lo parts of P)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t sel = (i & 1) ? 0x7632u : 0x5410u;
+      const int w = i >> 1;
+      const uint32_t a0 = prmt(word(v00, w), word(v10, w), sel);
+      const uint32_t a1 = prmt(word(v01, w), word(v11, w), sel);
+      const uint32_t a2 = prmt(word(v20, w), word(v30, w), sel);
+      const uint32_t a3 = prmt(word(v21, w), word(v31, w), sel);
+      mma_bf16(o[i], a0, a1, a2, a3, bh0, bh1);
+      mma_bf16(o[i], a0, a1, a2, a3, bl0, bl1);
+    }
+
+    __syncwarp();
+    if (j + kStages < nt) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(j + kStages);
+    }
+  }
+
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    l0 += __shfl_xor_sync(kFull, l0, off);
+    l1 += __shfl_xor_sync(kFull, l1, off);
+  }
+  const int h0 = 2 * qd, h1 = 2 * qd + 1;
+
+  if (n_chunks == 1) {  // whole context in one unit: write the output directly
+    uint16_t* ob = a.out + (static_cast<int64_t>(b) * a.hq + g * G) * kHeadDim;
+    float t[8];
+    if (h0 < G) {
+      const float inv = 1.f / l0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = o[i][0];
+      store_row8(ob + h0 * kHeadDim + 8 * r, t, inv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = o[i][2];
+      store_row8(ob + h0 * kHeadDim + 64 + 8 * r, t, inv);
+    }
+    if (h1 < G) {
+      const float inv = 1.f / l1;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = o[i][1];
+      store_row8(ob + h1 * kHeadDim + 8 * r, t, inv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) t[i] = o[i][3];
+      store_row8(ob + h1 * kHeadDim + 64 + 8 * r, t, inv);
+    }
+    return;
+  }
+
+  // (a6) partial: unnormalised acc + (m, l) in the exp2 domain
+  const int64_t slot = static_cast<int64_t>(bg) * a.max_chunks + c;
+  float* acc = a.ws_acc + slot * G * kHeadDim;
+  if (h0 < G) {
+    float4* p = reinterpret_cast<float4*>(acc + h0 * kHeadDim + 8 * r);
+    p[0] = make_float4(o[0][0], o[1][0], o[2][0], o[3][0]);
+    p[1] = make_float4(o[4][0], o[5][0], o[6][0], o[7][0]);
+    float4* p2 = reinterpret_cast<float4*>(acc + h0 * kHeadDim + 64 + 8 * r);
+    p2[0] = make_float4(o[0][2], o[1][2], o[2][2], o[3][2]);
+    p2[1] = make_float4(o[4][2], o[5][2], o[6][2], o[7][2]);
+    if (r == 0) a.ws_ml[slot * G + h0] = make_float2(m0, l0);
+  }
+  if (h1 < G) {
+    float4* p = reinterpret_cast<float4*>(acc + h1 * kHeadDim + 8 * r);
+    p[0] = make_float4(o[0][1], o[1][1], o[2][1], o[3][1]);
+    p[1] = make_float4(o[4][1], o[5][1], o[6][1], o[7][1]);
+    float4* p2 = reinterpret_cast<float4*>(acc + h1 * kHeadDim + 64 + 8 * r);
+    p2[0] = make_float4(o[0][3], o[1][3], o[2][3], o[3][3]);
+    p2[1] = make_float4(o[4][3], o[5][3], o[6][3], o[7][3]);
+    if (r == 0) a.ws_ml[slot * G + h1] = make_float2(m1, l1);
+  }
+  __threadfence();
+  __syncwarp();
+  int prev = 0;
+  if (lane == 0) prev = atomicAdd(a.ws_cnt + bg, 1);
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != n_chunks - 1) return;
+  __threadfence();
+
+  // (a7) combine, in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c
+  const int64_t slot0 = static_cast<int64_t>(bg) * a.max_chunks;
+  for (int h = 0; h < G; ++h) {
+    float M = -INFINITY;
+    for (int cc = 0; cc < n_chunks; ++cc) M = fmaxf(M, __ldcg(&a.ws_ml[(slot0 + cc) * G + h].x));
+    float L = 0.f;
+    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int cc = 0; cc < n_chunks; ++cc) {
+      const float2 ml = __ldcg(&a.ws_ml[(slot0 + cc) * G + h]);
+      const float w = ex2(ml.x - M);
+      L += ml.y * w;
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(a.ws_acc + ((slot0 + cc) * G + h) * kHeadDim) + lane);
+      s4.x += w * v.x;
+      s4.y += w * v.y;
+      s4.z += w * v.z;
+      s4.w += w * v.w;
+    }
+    const float inv = 1.f / L;
+    uint2 pk;
+    pk.x = pack_bf16(s4.x * inv, s4.y * inv);
+    pk.y = pack_bf16(s4.z * inv, s4.w * inv);
+    *reinterpret_cast<uint2*>(a.out + (static_cast<int64_t>(b) * a.hq + g * G + h) * kHeadDim + 4 * lane) = pk;
+  }
+  if (lane == 0) a.ws_cnt[bg] = 0;  // leave the workspace re-usable
+}
+
+}  // namespace
+
+WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks) {
+  const int64_t G = hkv > 0 ? hq / hkv : 0;
+  const int64_t units = static_cast<int64_t>(batch) * hkv * max_chunks;
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  WorkspaceLayout w;
+  w.cnt_off = 0;
+  w.ml_off = up(static_cast<size_t>(batch) * hkv * sizeof(int32_t));
+  const bool split = max_chunks > 1;
+  w.acc_off = w.ml_off + (split ? up(static_cast<size_t>(units * G) * sizeof(float2)) : 0);
+  w.total = w.acc_off + (split ? up(static_cast<size_t>(units * G * kHeadDim) * sizeof(float)) : 0);
+  if (w.total == 0) w.total = 256;
+  return w;
+}
+
+neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const CUtensorMap& tmv) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_kernel)");
+    configured = true;
+  }
+  const WorkspaceLayout w = workspace_layout(L.batch, L.hq, L.hkv, L.max_chunks);
+  uint8_t* ws = static_cast<uint8_t*>(L.workspace);
+  KArgs a;
+  a.q = static_cast<const uint16_t*>(L.q);
+  a.out = static_cast<uint16_t*>(L.out);
+  a.block_table = L.block_table;
+  a.seq_lens = L.seq_lens;
+  a.ws_cnt = reinterpret_cast<int32_t*>(ws + w.cnt_off);
+  a.ws_ml = reinterpret_cast<float2*>(ws + w.ml_off);
+  a.ws_acc = reinterpret_cast<float*>(ws + w.acc_off);
+  a.batch = L.batch;
+  a.hq = L.hq;
+  a.hkv = L.hkv;
+  a.G = L.hq / L.hkv;
+  a.page_size = L.page_size;
+  a.max_blocks = L.max_blocks;
+  a.chunk_tiles = L.chunk_tokens / kTileTokens;
+  a.max_chunks = L.max_chunks;
+  a.scale_log2 = L.scale * 1.4426950408889634f;
+  const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
+  const int64_t grid = (units + kWarps - 1) / kWarps;
+  decode_attn_kernel<<<static_cast<unsigned>(grid), kWarps * 32, kSmemBytes, L.stream>>>(tmk, tmv, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
+  return NEO_OK;
+}
+
+}  // namespace neo

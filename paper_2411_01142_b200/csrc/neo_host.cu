@@ -1,0 +1,486 @@
+// Host side of libneo: the C ABI of include/neo.h -- argument validation,
+// the two-pool page allocator (P:234-235 GPU-cache / CPU-cache; S:231-310
+// kv_pool semantics: all-or-nothing, conservation, residency), the TMA
+// tensor-map cache for the attention kernel, and swap orchestration
+// (gather kernel + cudaMemcpy2DAsync over PCIe).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "neo_internal.cuh"
+
+namespace neo {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string& msg) { g_err = msg; }
+
+neo_status fail(neo_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+neo_status cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return NEO_ERR_CUDA;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static bool debug_validate_enabled() {
+  const char* v = std::getenv("NEO_DEBUG_VALIDATE");
+  return v && v[0] == '1';
+}
+
+// ----------------------------------------------------------------- tensor maps
+namespace {
+
+struct TmKey {
+  const void* ptr;
+  int64_t page_stride, num_pages;
+  int32_t hkv, page_size;
+  bool operator==(const TmKey& o) const {
+    return ptr == o.ptr && page_stride == o.page_stride && num_pages == o.num_pages && hkv == o.hkv &&
+           page_size == o.page_size;
+  }
+};
+struct TmKeyHash {
+  size_t operator()(const TmKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    h ^= std::hash<int64_t>()(k.page_stride) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h ^= std::hash<int64_t>()(k.num_pages) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h ^= std::hash<int64_t>()((static_cast<int64_t>(k.hkv) << 32) | k.page_size) + (h << 6) + (h >> 2);
+    return h;
+  }
+};
+
+std::mutex g_tm_mu;
+std::unordered_map<TmKey, CUtensorMap, TmKeyHash> g_tm_cache;
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+neo_status get_encoder() {
+  if (g_encode) return NEO_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return fail(NEO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return NEO_OK;
+}
+
+// View of a layer's K (or V) pages as a 5-D tensor {64 el, 2 halves, P tokens,
+// Hkv heads, num_pages} with box {64, 2, 16, 1, 1}: one TMA load = one 16-token
+// tile (4 KiB) of one (page, kv-head), written to shared memory 128B-swizzled.
+neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,
+                      CUtensorMap* out) {
+  TmKey key{ptr, page_stride, num_pages, hkv, P};
+  std::lock_guard<std::mutex> lk(g_tm_mu);
+  auto it = g_tm_cache.find(key);
+  if (it != g_tm_cache.end()) {
+    *out = it->second;
+    return NEO_OK;
+  }
+  neo_status st = get_encoder();
+  if (st != NEO_OK) return st;
+  CUtensorMap tm;
+  std::memset(&tm, 0, sizeof tm);
+  cuuint64_t dims[5] = {64, 2, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(hkv),
+                        static_cast<cuuint64_t>(num_pages)};
+  cuuint64_t strides[4] = {128, 256, static_cast<cuuint64_t>(P) * 256, static_cast<cuuint64_t>(page_stride) * 2};
+  cuuint32_t box[5] = {64, 2, 16, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NEO_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  if (g_tm_cache.size() > 4096) g_tm_cache.clear();
+  g_tm_cache.emplace(key, tm);
+  *out = tm;
+  return NEO_OK;
+}
+
+int32_t default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
+  // Aim for ~8 waves of one-warp units over 148 SMs x 8 resident warps; the
+  // smallest power of two in [64, 512] that does not overshoot that.
+  const double target_units = 8.0 * 148 * 8;
+  const double want = static_cast<double>(batch) * hkv * std::max(max_seq_len, 1) / target_units;
+  int32_t c = 64;
+  while (c < want && c < kMaxChunkTokens) c *= 2;
+  return c;
+}
+
+neo_status check_chunk(int32_t C, int32_t P) {
+  if (C <= 0 || C % kTileTokens != 0 || C % P != 0 || C > kMaxChunkTokens)
+    return fail(NEO_ERR_UNSUPPORTED, "chunk_tokens must be a multiple of 16 and of page_size, <= 512 (got " +
+                                         std::to_string(C) + ")");
+  return NEO_OK;
+}
+
+}  // namespace
+
+// debug validation: copies device metadata back (synchronous; debug only)
+neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                               int32_t batch, int32_t page_size, int32_t max_seq_len, int64_t num_pages,
+                               cudaStream_t stream) {
+  std::vector<int32_t> sl(batch), bt(static_cast<size_t>(batch) * max_blocks);
+  cudaError_t e = cudaMemcpyAsync(sl.data(), seq_lens, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(bt.data(), block_table, sizeof(int32_t) * bt.size(), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "NEO_DEBUG_VALIDATE copy");
+  for (int32_t b = 0; b < batch; ++b) {
+    if (sl[b] < 0 || sl[b] > max_seq_len || static_cast<int64_t>(sl[b]) > static_cast<int64_t>(max_blocks) * page_size)
+      return fail(NEO_ERR_INVALID_ARG, "seq_lens[" + std::to_string(b) + "] = " + std::to_string(sl[b]) +
+                                           " outside [0, min(max_seq_len, max_blocks*P)]");
+    const int32_t np = (sl[b] + page_size - 1) / page_size;
+    for (int32_t j = 0; j < np; ++j) {
+      const int32_t id = bt[static_cast<size_t>(b) * max_blocks + j];
+      if (id < 0 || id >= num_pages)
+        return fail(NEO_ERR_INVALID_ARG, "block_table[" + std::to_string(b) + "][" + std::to_string(j) +
+                                             "] = " + std::to_string(id) + " outside [0, num_pages)");
+    }
+  }
+  return NEO_OK;
+}
+
+}  // namespace neo
+
+// ======================================================================= pool
+
+struct neo_kv_pool {
+  neo_kv_geometry geo;
+  uint8_t* gpu_base;
+  uint8_t* host_base;
+  int64_t page_elems;   // Hkv * P * D
+  size_t layer_bytes;   // page_elems * 2 (one layer, K or V, one page)
+  std::vector<int32_t> gpu_free;      // LIFO stack of free GPU page ids
+  std::vector<uint8_t> gpu_used;      // allocated flags
+  std::vector<uint8_t> host_used;
+  int64_t host_free;
+  std::mutex mu;
+};
+
+using neo::fail;
+
+static neo_status check_geo(const neo_kv_geometry* g) {
+  if (!g) return fail(NEO_ERR_INVALID_ARG, "geometry is NULL");
+  if (g->num_layers < 1 || g->num_kv_heads < 1 || g->num_gpu_pages < 0 || g->num_host_pages < 0)
+    return fail(NEO_ERR_INVALID_ARG, "geometry: layers/heads must be >= 1, page counts >= 0");
+  if (g->num_gpu_pages > INT32_MAX || g->num_host_pages > INT32_MAX)
+    return fail(NEO_ERR_INVALID_ARG, "geometry: page counts must fit int32 ids");
+  if (g->head_dim != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
+  if (g->page_size < 16 || g->page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
+  return NEO_OK;
+}
+
+extern "C" {
+
+NEO_API const char* neo_last_error(void) { return neo::g_err.c_str(); }
+NEO_API const char* neo_version(void) { return "neo-b200 0.1 (sm_100a)"; }
+
+NEO_API neo_status neo_kv_pool_bytes(const neo_kv_geometry* geo, size_t* gpu_bytes, size_t* host_bytes) {
+  neo_status st = check_geo(geo);
+  if (st != NEO_OK) return st;
+  const size_t page = static_cast<size_t>(geo->num_kv_heads) * geo->page_size * geo->head_dim * 2;
+  const size_t per_layer_pair = 2 * page;
+  if (gpu_bytes) *gpu_bytes = per_layer_pair * geo->num_layers * static_cast<size_t>(geo->num_gpu_pages);
+  if (host_bytes) *host_bytes = per_layer_pair * geo->num_layers * static_cast<size_t>(geo->num_host_pages);
+  return NEO_OK;
+}
+
+NEO_API neo_status neo_kv_pool_create(const neo_kv_geometry* geo, void* gpu_kv_base, size_t gpu_bytes,
+                                      void* host_kv_base, size_t host_bytes, neo_kv_pool** out) {
+  if (!out) return fail(NEO_ERR_INVALID_ARG, "out is NULL");
+  size_t need_gpu = 0, need_host = 0;
+  neo_status st = neo_kv_pool_bytes(geo, &need_gpu, &need_host);
+  if (st != NEO_OK) return st;
+  if (geo->num_gpu_pages > 0 && (!gpu_kv_base || !neo::aligned16(gpu_kv_base)))
+    return fail(NEO_ERR_INVALID_ARG, "gpu_kv_base must be a non-NULL 16-byte aligned device pointer");
+  if (geo->num_host_pages > 0 && (!host_kv_base || !neo::aligned16(host_kv_base)))
+    return fail(NEO_ERR_INVALID_ARG, "host_kv_base must be a non-NULL 16-byte aligned pinned pointer");
+  if (gpu_bytes < need_gpu) return fail(NEO_ERR_INVALID_ARG, "gpu_bytes smaller than neo_kv_pool_bytes()");
+  if (host_bytes < need_host) return fail(NEO_ERR_INVALID_ARG, "host_bytes smaller than neo_kv_pool_bytes()");
+  neo_kv_pool* p = new (std::nothrow) neo_kv_pool();
+  if (!p) return fail(NEO_ERR_INTERNAL, "out of host memory");
+  p->geo = *geo;
+  p->gpu_base = static_cast<uint8_t*>(gpu_kv_base);
+  p->host_base = static_cast<uint8_t*>(host_kv_base);
+  p->page_elems = static_cast<int64_t>(geo->num_kv_heads) * geo->page_size * geo->head_dim;
+  p->layer_bytes = static_cast<size_t>(p->page_elems) * 2;
+  try {
+    p->gpu_free.resize(geo->num_gpu_pages);
+    for (int64_t i = 0; i < geo->num_gpu_pages; ++i)
+      p->gpu_free[i] = static_cast<int32_t>(geo->num_gpu_pages - 1 - i);  // pop_back yields 0, 1, 2, ...
+    p->gpu_used.assign(geo->num_gpu_pages, 0);
+    p->host_used.assign(geo->num_host_pages, 0);
+  } catch (...) {
+    delete p;
+    return fail(NEO_ERR_INTERNAL, "out of host memory");
+  }
+  p->host_free = geo->num_host_pages;
+  *out = p;
+  return NEO_OK;
+}
+
+NEO_API void neo_kv_pool_destroy(neo_kv_pool* pool) { delete pool; }
+
+NEO_API neo_status neo_kv_alloc(neo_kv_pool* pool, int32_t where, int32_t n, int32_t* ids) {
+  if (!pool) return fail(NEO_ERR_INVALID_ARG, "pool is NULL");
+  if (where != NEO_GPU && where != NEO_HOST) return fail(NEO_ERR_INVALID_ARG, "where must be NEO_GPU or NEO_HOST");
+  if (n < 0) return fail(NEO_ERR_INVALID_ARG, "n_pages < 0");
+  if (n == 0) return NEO_OK;
+  if (!ids) return fail(NEO_ERR_INVALID_ARG, "page_ids_out is NULL");
+  std::lock_guard<std::mutex> lk(pool->mu);
+  if (where == NEO_GPU) {
+    if (static_cast<int64_t>(pool->gpu_free.size()) < n)
+      return fail(NEO_ERR_OUT_OF_PAGES, "GPU-cache has " + std::to_string(pool->gpu_free.size()) +
+                                            " free pages, need " + std::to_string(n));
+    for (int32_t i = 0; i < n; ++i) {
+      ids[i] = pool->gpu_free.back();
+      pool->gpu_free.pop_back();
+      pool->gpu_used[ids[i]] = 1;
+    }
+    return NEO_OK;
+  }
+  if (pool->host_free < n)
+    return fail(NEO_ERR_OUT_OF_PAGES, "CPU-cache has " + std::to_string(pool->host_free) + " free pages, need " +
+                                          std::to_string(n));
+  // first fit: one contiguous ascending run if possible, else the lowest free ids
+  const int64_t N = pool->geo.num_host_pages;
+  int64_t run = 0, start = -1;
+  for (int64_t i = 0; i < N; ++i) {
+    run = pool->host_used[i] ? 0 : run + 1;
+    if (run == n) {
+      start = i - n + 1;
+      break;
+    }
+  }
+  if (start >= 0) {
+    for (int32_t i = 0; i < n; ++i) ids[i] = static_cast<int32_t>(start + i);
+  } else {
+    int32_t k = 0;
+    for (int64_t i = 0; i < N && k < n; ++i)
+      if (!pool->host_used[i]) ids[k++] = static_cast<int32_t>(i);
+  }
+  for (int32_t i = 0; i < n; ++i) pool->host_used[ids[i]] = 1;
+  pool->host_free -= n;
+  return NEO_OK;
+}
+
+static neo_status check_ids(const std::vector<uint8_t>& used, int32_t n, const int32_t* ids, const char* what) {
+  std::vector<int32_t> seen;
+  seen.reserve(n);
+  for (int32_t i = 0; i < n; ++i) {
+    const int32_t id = ids[i];
+    if (id < 0 || id >= static_cast<int64_t>(used.size()) || !used[id])
+      return fail(NEO_ERR_INVALID_ARG, std::string(what) + " id " + std::to_string(id) + " is not allocated");
+    seen.push_back(id);
+  }
+  std::sort(seen.begin(), seen.end());
+  if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
+    return fail(NEO_ERR_INVALID_ARG, std::string(what) + " ids contain duplicates");
+  return NEO_OK;
+}
+
+NEO_API neo_status neo_kv_free(neo_kv_pool* pool, int32_t where, int32_t n, const int32_t* ids) {
+  if (!pool) return fail(NEO_ERR_INVALID_ARG, "pool is NULL");
+  if (where != NEO_GPU && where != NEO_HOST) return fail(NEO_ERR_INVALID_ARG, "where must be NEO_GPU or NEO_HOST");
+  if (n < 0) return fail(NEO_ERR_INVALID_ARG, "n_pages < 0");
+  if (n == 0) return NEO_OK;
+  if (!ids) return fail(NEO_ERR_INVALID_ARG, "page_ids is NULL");
+  std::lock_guard<std::mutex> lk(pool->mu);
+  std::vector<uint8_t>& used = where == NEO_GPU ? pool->gpu_used : pool->host_used;
+  neo_status st = check_ids(used, n, ids, where == NEO_GPU ? "GPU page" : "host page");
+  if (st != NEO_OK) return st;
+  for (int32_t i = 0; i < n; ++i) {
+    used[ids[i]] = 0;
+    if (where == NEO_GPU) pool->gpu_free.push_back(ids[i]);
+  }
+  if (where == NEO_HOST) pool->host_free += n;
+  return NEO_OK;
+}
+
+NEO_API neo_status neo_kv_free_count(const neo_kv_pool* pool, int32_t where, int64_t* n_free) {
+  if (!pool || !n_free) return fail(NEO_ERR_INVALID_ARG, "NULL argument");
+  if (where == NEO_GPU) *n_free = static_cast<int64_t>(pool->gpu_free.size());
+  else if (where == NEO_HOST) *n_free = pool->host_free;
+  else return fail(NEO_ERR_INVALID_ARG, "where must be NEO_GPU or NEO_HOST");
+  return NEO_OK;
+}
+
+NEO_API neo_status neo_kv_layer_view(const neo_kv_pool* pool, int32_t layer, void** k, void** v, int64_t* stride) {
+  if (!pool || !k || !v || !stride) return fail(NEO_ERR_INVALID_ARG, "NULL argument");
+  if (layer < 0 || layer >= pool->geo.num_layers) return fail(NEO_ERR_INVALID_ARG, "layer out of range");
+  const size_t kv_bytes = pool->layer_bytes * static_cast<size_t>(pool->geo.num_gpu_pages);
+  *k = pool->gpu_base + (static_cast<size_t>(layer) * 2 + 0) * kv_bytes;
+  *v = pool->gpu_base + (static_cast<size_t>(layer) * 2 + 1) * kv_bytes;
+  *stride = pool->page_elems;
+  return NEO_OK;
+}
+
+// ============================================================ decode attention
+
+NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
+  return neo::default_chunk(batch, hkv, max_seq_len);
+}
+
+static neo_status attn_shape(int32_t batch, int32_t hq, int32_t hkv, int32_t d, int32_t max_seq_len,
+                             int32_t* chunk_tokens, int32_t page_size) {
+  if (batch < 0 || hq <= 0 || hkv <= 0 || max_seq_len < 0)
+    return fail(NEO_ERR_INVALID_ARG, "batch >= 0, heads >= 1 and max_seq_len >= 0 required");
+  if (hq % hkv != 0) return fail(NEO_ERR_INVALID_ARG, "num_q_heads must be a multiple of num_kv_heads");
+  if (d != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
+  if (hq / hkv > neo::kMaxGroup) return fail(NEO_ERR_UNSUPPORTED, "GQA group size G = Hq/Hkv must be <= 8");
+  if (*chunk_tokens == 0) {
+    *chunk_tokens = neo::default_chunk(batch, hkv, max_seq_len);
+    if (page_size > 0 && *chunk_tokens % page_size) *chunk_tokens = page_size * ((*chunk_tokens + page_size - 1) / page_size);
+  }
+  return neo::check_chunk(*chunk_tokens, page_size > 0 ? page_size : 16);
+}
+
+NEO_API neo_status neo_decode_attn_workspace_bytes(int32_t batch, int32_t hq, int32_t hkv, int32_t d,
+                                                   int32_t max_seq_len, int32_t chunk_tokens, size_t* bytes) {
+  if (!bytes) return fail(NEO_ERR_INVALID_ARG, "bytes is NULL");
+  neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, 16);
+  if (st != NEO_OK) return st;
+  const int32_t max_chunks = std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
+  *bytes = neo::workspace_layout(batch, hq, hkv, max_chunks).total;
+  return NEO_OK;
+}
+
+NEO_API neo_status neo_decode_attn_workspace_init(void* ws, size_t bytes, void* stream) {
+  if (!ws || bytes == 0) return fail(NEO_ERR_INVALID_ARG, "workspace is NULL/empty");
+  cudaError_t e = cudaMemsetAsync(ws, 0, bytes, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? NEO_OK : neo::cuda_fail(e, "cudaMemsetAsync(workspace)");
+}
+
+NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+                                   int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
+                                   const int32_t* seq_lens, void* out, int32_t batch, int32_t hq, int32_t hkv,
+                                   int32_t d, int32_t page_size, int32_t max_seq_len, float scale,
+                                   int32_t chunk_tokens, void* workspace, size_t workspace_bytes, void* stream) {
+  if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
+  neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, page_size);
+  if (st != NEO_OK) return st;
+  if (batch == 0) return NEO_OK;
+  if (!q || !k_pages || !v_pages || !block_table || !seq_lens || !out || !workspace)
+    return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
+  if (!neo::aligned16(q) || !neo::aligned16(out) || !neo::aligned16(k_pages) || !neo::aligned16(v_pages) ||
+      !neo::aligned16(workspace))
+    return fail(NEO_ERR_INVALID_ARG, "q, out, k_pages, v_pages and workspace must be 16-byte aligned");
+  if (page_stride % 8 != 0 || page_stride < static_cast<int64_t>(hkv) * page_size * d)
+    return fail(NEO_ERR_INVALID_ARG, "page_stride must be a multiple of 8 elements and >= Hkv*P*D");
+  if (num_pages < 1 || num_pages > (int64_t(1) << 31)) return fail(NEO_ERR_INVALID_ARG, "num_pages out of range");
+  if (max_blocks < 1 || static_cast<int64_t>(max_seq_len) > static_cast<int64_t>(max_blocks) * page_size)
+    return fail(NEO_ERR_INVALID_ARG, "max_seq_len exceeds max_blocks * page_size");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(NEO_ERR_INVALID_ARG, "scale must be finite and > 0");
+  const int32_t max_chunks = std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
+  const neo::WorkspaceLayout wl = neo::workspace_layout(batch, hq, hkv, max_chunks);
+  if (workspace_bytes < wl.total)
+    return fail(NEO_ERR_INVALID_ARG, "workspace too small: need " + std::to_string(wl.total) + " bytes");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (neo::debug_validate_enabled()) {
+    st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_seq_len, num_pages, s);
+    if (st != NEO_OK) return st;
+  }
+  CUtensorMap tmk, tmv;
+  st = neo::tensor_map(k_pages, page_stride, num_pages, hkv, page_size, &tmk);
+  if (st != NEO_OK) return st;
+  st = neo::tensor_map(v_pages, page_stride, num_pages, hkv, page_size, &tmv);
+  if (st != NEO_OK) return st;
+  neo::AttnLaunch L{q, out, block_table, seq_lens, workspace, batch, hq, hkv, page_size, max_blocks,
+                    chunk_tokens, max_chunks, scale, s};
+  return neo::launch_decode_attn(L, tmk, tmv);
+}
+
+// ======================================================================= swap
+
+NEO_API neo_status neo_kv_swap_staging_bytes(const neo_kv_pool* pool, int32_t n, int32_t l0, int32_t l1,
+                                             size_t* bytes) {
+  if (!pool || !bytes) return fail(NEO_ERR_INVALID_ARG, "NULL argument");
+  if (n < 0 || l0 < 0 || l1 > pool->geo.num_layers || l0 >= l1)
+    return fail(NEO_ERR_INVALID_ARG, "bad page count or layer range");
+  *bytes = static_cast<size_t>(n) * (l1 - l0) * 2 * pool->layer_bytes;
+  return NEO_OK;
+}
+
+static neo_status swap_common(neo_kv_pool* pool, bool out_dir, int32_t n, const int32_t* gpu_ids,
+                              const int32_t* host_ids, int32_t l0, int32_t l1, void* staging, size_t staging_bytes,
+                              void* stream) {
+  if (!pool) return fail(NEO_ERR_INVALID_ARG, "pool is NULL");
+  if (n < 0) return fail(NEO_ERR_INVALID_ARG, "n_pages < 0");
+  if (l0 < 0 || l1 > pool->geo.num_layers || l0 >= l1) return fail(NEO_ERR_INVALID_ARG, "layer range out of bounds");
+  if (n == 0) return NEO_OK;
+  if (!gpu_ids || !host_ids || !staging) return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
+  if (!neo::aligned16(staging)) return fail(NEO_ERR_INVALID_ARG, "staging must be 16-byte aligned");
+  const size_t per_page = static_cast<size_t>(l1 - l0) * 2 * pool->layer_bytes;
+  if (staging_bytes < per_page) return fail(NEO_ERR_INVALID_ARG, "staging smaller than one page's layer range");
+  {
+    std::lock_guard<std::mutex> lk(pool->mu);
+    neo_status st = check_ids(pool->gpu_used, n, gpu_ids, "GPU page");
+    if (st != NEO_OK) return st;
+    st = check_ids(pool->host_used, n, host_ids, "host page");
+    if (st != NEO_OK) return st;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t host_page = static_cast<size_t>(pool->geo.num_layers) * 2 * pool->layer_bytes;
+  const size_t host_off = static_cast<size_t>(l0) * 2 * pool->layer_bytes;
+  const int64_t cap = std::min<int64_t>(staging_bytes / per_page, neo::kMaxSwapIdsPerLaunch);
+  uint8_t* stg = static_cast<uint8_t*>(staging);
+  const uint16_t* gpu16 = reinterpret_cast<const uint16_t*>(pool->gpu_base);
+  for (int32_t c0 = 0; c0 < n; c0 += static_cast<int32_t>(cap)) {
+    const int32_t cn = static_cast<int32_t>(std::min<int64_t>(cap, n - c0));
+    neo::SwapBatch ids;
+    for (int32_t i = 0; i < cn; ++i) ids.ids[i] = gpu_ids[c0 + i];
+    if (!out_dir) {  // host -> staging, per run of consecutive host ids
+      for (int32_t i = 0; i < cn;) {
+        int32_t j = i + 1;
+        while (j < cn && host_ids[c0 + j] == host_ids[c0 + j - 1] + 1) ++j;
+        cudaError_t e = cudaMemcpy2DAsync(stg + static_cast<size_t>(i) * per_page, per_page,
+                                          pool->host_base + static_cast<size_t>(host_ids[c0 + i]) * host_page + host_off,
+                                          host_page, per_page, j - i, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return neo::cuda_fail(e, "cudaMemcpy2DAsync(H2D swap-in)");
+        i = j;
+      }
+      neo_status st = neo::launch_scatter(reinterpret_cast<uint16_t*>(pool->gpu_base),
+                                          reinterpret_cast<const uint16_t*>(stg), ids, cn, pool->geo.num_gpu_pages,
+                                          pool->page_elems, l0, l1, s);
+      if (st != NEO_OK) return st;
+    } else {
+      neo_status st = neo::launch_gather(gpu16, reinterpret_cast<uint16_t*>(stg), ids, cn, pool->geo.num_gpu_pages,
+                                         pool->page_elems, l0, l1, s);
+      if (st != NEO_OK) return st;
+      for (int32_t i = 0; i < cn;) {
+        int32_t j = i + 1;
+        while (j < cn && host_ids[c0 + j] == host_ids[c0 + j - 1] + 1) ++j;
+        cudaError_t e = cudaMemcpy2DAsync(pool->host_base + static_cast<size_t>(host_ids[c0 + i]) * host_page + host_off,
+                                          host_page, stg + static_cast<size_t>(i) * per_page, per_page, per_page, j - i,
+                                          cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return neo::cuda_fail(e, "cudaMemcpy2DAsync(D2H swap-out)");
+        i = j;
+      }
+    }
+  }
+  return NEO_OK;
+}
+
+NEO_API neo_status neo_kv_swap_out(neo_kv_pool* pool, int32_t n, const int32_t* gpu_ids, const int32_t* host_ids,
+                                   int32_t l0, int32_t l1, void* staging, size_t staging_bytes, void* stream) {
+  return swap_common(pool, true, n, gpu_ids, host_ids, l0, l1, staging, staging_bytes, stream);
+}
+
+NEO_API neo_status neo_kv_swap_in(neo_kv_pool* pool, int32_t n, const int32_t* host_ids, const int32_t* gpu_ids,
+                                  int32_t l0, int32_t l1, void* staging, size_t staging_bytes, void* stream) {
+  return swap_common(pool, false, n, gpu_ids, host_ids, l0, l1, staging, staging_bytes, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// Internal declarations shared by the libneo translation units (host ABI,
+// attention kernel, swap kernels).  Not part of the public ABI (include/neo.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/neo.h"
+
+namespace neo {
+
+constexpr int kHeadDim = 128;
+constexpr int kTileTokens = 16;                       // tokens per MMA tile
+constexpr int kTileBytes = kTileTokens * kHeadDim * 2;  // 4096: one K (or V) tile
+constexpr int kMaxGroup = 8;                          // G <= 8 (MMA N = 8)
+constexpr int kMaxChunkTokens = 512;                  // <= 32 tiles per work unit
+
+// thread-local error text for neo_last_error()
+void set_error(const std::string& msg);
+neo_status fail(neo_status st, const std::string& msg);
+neo_status cuda_fail(cudaError_t e, const char* what);
+
+// ---- decode attention (neo_attn.cu)
+struct AttnLaunch {
+  const void* q;
+  void* out;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  void* workspace;
+  int32_t batch, hq, hkv, page_size, max_blocks, chunk_tokens, max_chunks;
+  float scale;
+  cudaStream_t stream;
+};
+// Byte layout of the workspace for a call shape.
+struct WorkspaceLayout {
+  size_t cnt_off, ml_off, acc_off, total;
+};
+WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks);
+neo_status launch_decode_attn(const AttnLaunch& a, const CUtensorMap& tmk, const CUtensorMap& tmv);
+// debug validation of device metadata (syncs the stream)
+neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                               int32_t batch, int32_t page_size, int32_t max_seq_len, int64_t num_pages,
+                               cudaStream_t stream);
+
+// ---- swap (neo_swap.cu)
+constexpr int kMaxSwapIdsPerLaunch = 960;  // page ids passed by value in the kernel params
+struct SwapBatch {
+  int32_t ids[kMaxSwapIdsPerLaunch];
+};
+// staging[i][l - l0][kv][...page_elems] <-> gpu[l][kv][ids[i]][...]
+neo_status launch_gather(const uint16_t* gpu_base, uint16_t* staging, const SwapBatch& ids, int32_t n,
+                         int64_t num_gpu_pages, int64_t page_elems, int32_t l0, int32_t l1, cudaStream_t s);
+neo_status launch_scatter(uint16_t* gpu_base, const uint16_t* staging, const SwapBatch& ids, int32_t n,
+                          int64_t num_gpu_pages, int64_t page_elems, int32_t l0, int32_t l1, cudaStream_t s);
+
+}  // namespace neo

@@ -1,0 +1,77 @@
+// Page gather / scatter for KV swap between the GPU-cache and the CPU-cache
+// (P:235 partial offloading, P:240 layer-wise swapping, P:285-288 swap steps).
+// The PCIe transfer (cudaMemcpy2DAsync from/to pinned host pages) is issued by
+// the host code in neo_host.cu; these kernels only pack the scattered GPU pages
+// of one request into a contiguous device staging buffer and unpack them back.
+// Pure bit copies: 16-byte vector loads/stores, one CTA per (page, layer, K|V)
+// block (Hkv*P*D*2 bytes, 32 KiB for LLaMa-3.1-8B), streaming cache hints.
+#include "neo_internal.cuh"
+
+namespace neo {
+namespace {
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_stream(uint4* p, const uint4& v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+struct CopyArgs {
+  const uint16_t* gpu_src;
+  uint16_t* gpu_dst;
+  const uint16_t* stg_src;
+  uint16_t* stg_dst;
+  int64_t num_gpu_pages, page_elems;
+  int32_t n, l0, nl;
+};
+
+// grid (n pages, nl layers * 2); staging block index ((i * nl) + (l - l0)) * 2 + kv
+template <bool kGather>
+__global__ void __launch_bounds__(256) swap_copy_kernel(const CopyArgs a, const SwapBatch ids) {
+  const int i = blockIdx.x;
+  const int lk = blockIdx.y;  // (l - l0) * 2 + kv
+  const int l = a.l0 + (lk >> 1), kv = lk & 1;
+  const int64_t gpu_block = (static_cast<int64_t>(l) * 2 + kv) * a.num_gpu_pages + ids.ids[i];
+  const int64_t stg_block = static_cast<int64_t>(i) * a.nl * 2 + lk;
+  const int64_t nvec = a.page_elems / 8;
+  if (kGather) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.gpu_src + gpu_block * a.page_elems);
+    uint4* dst = reinterpret_cast<uint4*>(a.stg_dst + stg_block * a.page_elems);
+    for (int64_t e = threadIdx.x; e < nvec; e += blockDim.x) st_stream(dst + e, ld_stream(src + e));
+  } else {
+    const uint4* src = reinterpret_cast<const uint4*>(a.stg_src + stg_block * a.page_elems);
+    uint4* dst = reinterpret_cast<uint4*>(a.gpu_dst + gpu_block * a.page_elems);
+    for (int64_t e = threadIdx.x; e < nvec; e += blockDim.x) st_stream(dst + e, ld_stream(src + e));
+  }
+}
+
+}  // namespace
+
+neo_status launch_gather(const uint16_t* gpu_base, uint16_t* staging, const SwapBatch& ids, int32_t n,
+                         int64_t num_gpu_pages, int64_t page_elems, int32_t l0, int32_t l1, cudaStream_t s) {
+  if (n <= 0) return NEO_OK;
+  CopyArgs a{gpu_base, nullptr, nullptr, staging, num_gpu_pages, page_elems, n, l0, l1 - l0};
+  dim3 grid(n, (l1 - l0) * 2);
+  swap_copy_kernel<true><<<grid, 256, 0, s>>>(a, ids);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? NEO_OK : cuda_fail(e, "gather kernel launch");
+}
+
+neo_status launch_scatter(uint16_t* gpu_base, const uint16_t* staging, const SwapBatch& ids, int32_t n,
+                          int64_t num_gpu_pages, int64_t page_elems, int32_t l0, int32_t l1, cudaStream_t s) {
+  if (n <= 0) return NEO_OK;
+  CopyArgs a{nullptr, gpu_base, staging, nullptr, num_gpu_pages, page_elems, n, l0, l1 - l0};
+  dim3 grid(n, (l1 - l0) * 2);
+  swap_copy_kernel<false><<<grid, 256, 0, s>>>(a, ids);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? NEO_OK : cuda_fail(e, "scatter kernel launch");
+}
+
+}  // namespace neo

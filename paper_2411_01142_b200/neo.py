@@ -1,0 +1,270 @@
+"""Thin Python binding of libneo (include/neo.h).  Argument marshalling only:
+every step of the hot path runs in the CUDA library.  torch supplies device
+memory, pinned host memory and streams -- plumbing, not compute.
+
+There is no fallback: if ``libneo.so`` is missing this module raises on first
+use, and every compute entry point requires CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libneo.so")
+
+NEO_OK, NEO_ERR_INVALID_ARG, NEO_ERR_OUT_OF_PAGES, NEO_ERR_UNSUPPORTED, NEO_ERR_CUDA, NEO_ERR_INTERNAL = range(6)
+NEO_GPU, NEO_HOST = 0, 1
+STATUS_NAMES = {0: "NEO_OK", 1: "NEO_ERR_INVALID_ARG", 2: "NEO_ERR_OUT_OF_PAGES", 3: "NEO_ERR_UNSUPPORTED",
+                4: "NEO_ERR_CUDA", 5: "NEO_ERR_INTERNAL"}
+
+EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_create", "neo_kv_pool_destroy",
+            "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
+            "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
+            "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes"]
+
+
+class NeoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Geometry(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("num_gpu_pages", ctypes.c_int64), ("num_host_pages", ctypes.c_int64)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2411_01142_b200.build` "
+                                  "(there is no CPU fallback)")
+            L = ctypes.CDLL(LIB_PATH)
+            P, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+            L.neo_last_error.restype = ctypes.c_char_p
+            L.neo_version.restype = ctypes.c_char_p
+            sig = {
+                "neo_kv_pool_bytes": [P, P, P],
+                "neo_kv_pool_create": [P, P, sz, P, sz, P],
+                "neo_kv_alloc": [P, i32, i32, P],
+                "neo_kv_free": [P, i32, i32, P],
+                "neo_kv_free_count": [P, i32, P],
+                "neo_kv_layer_view": [P, i32, P, P, P],
+                "neo_decode_attn": [P, P, P, i64, i64, P, i32, P, P, i32, i32, i32, i32, i32, i32,
+                                    ctypes.c_float, i32, P, sz, P],
+                "neo_decode_attn_workspace_bytes": [i32, i32, i32, i32, i32, i32, P],
+                "neo_decode_attn_workspace_init": [P, sz, P],
+                "neo_kv_swap_out": [P, i32, P, P, i32, i32, P, sz, P],
+                "neo_kv_swap_in": [P, i32, P, P, i32, i32, P, sz, P],
+                "neo_kv_swap_staging_bytes": [P, i32, i32, i32, P],
+            }
+            for name, args in sig.items():
+                f = getattr(L, name)
+                f.argtypes = args
+                f.restype = ctypes.c_int
+            L.neo_kv_pool_destroy.argtypes = [P]
+            L.neo_kv_pool_destroy.restype = None
+            L.neo_decode_attn_default_chunk.argtypes = [i32, i32, i32]
+            L.neo_decode_attn_default_chunk.restype = i32
+            _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != NEO_OK:
+        raise NeoError(status, lib().neo_last_error().decode())
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ids(ids) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(ids, dtype=np.int32).reshape(-1))
+
+
+# ------------------------------------------------------------------ attention
+
+
+def default_chunk(batch: int, num_kv_heads: int, max_seq_len: int) -> int:
+    return int(lib().neo_decode_attn_default_chunk(batch, num_kv_heads, max_seq_len))
+
+
+def workspace_bytes(batch: int, num_q_heads: int, num_kv_heads: int, max_seq_len: int,
+                    chunk_tokens: int = 0, head_dim: int = 128) -> int:
+    out = ctypes.c_size_t()
+    check(lib().neo_decode_attn_workspace_bytes(batch, num_q_heads, num_kv_heads, head_dim, max_seq_len,
+                                                chunk_tokens, ctypes.byref(out)))
+    return out.value
+
+
+def make_workspace(batch: int, num_q_heads: int, num_kv_heads: int, max_seq_len: int, chunk_tokens: int = 0,
+                   device=None, stream=None):
+    """Allocate (torch) and initialise a decode-attention workspace."""
+    import torch
+    n = workspace_bytes(batch, num_q_heads, num_kv_heads, max_seq_len, chunk_tokens)
+    ws = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+    check(lib().neo_decode_attn_workspace_init(ws.data_ptr(), n, _stream(stream)))
+    return ws
+
+
+def decode_attn(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, *, out=None, scale=None,
+                chunk_tokens: int = 0, workspace=None, stream=None, num_pages=None):
+    """Batched paged GQA decode attention: ``neo_decode_attn``.
+
+    q [B][Hq][D] bf16 cuda; k_pages/v_pages [num_pages][Hkv][P][D] bf16 cuda views
+    (page stride taken from ``stride(0)``; inner [Hkv][P][D] must be contiguous);
+    block_table [B][max_blocks] int32 cuda; seq_lens [B] int32 cuda."""
+    import torch
+    for name, t in (("q", q), ("k_pages", k_pages), ("v_pages", v_pages), ("block_table", block_table),
+                    ("seq_lens", seq_lens)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if q.dtype != torch.bfloat16 or k_pages.dtype != torch.bfloat16 or v_pages.dtype != torch.bfloat16:
+        raise ValueError("q, k_pages and v_pages must be bf16")
+    if block_table.dtype != torch.int32 or seq_lens.dtype != torch.int32:
+        raise ValueError("block_table and seq_lens must be int32")
+    if not q.is_contiguous() or not block_table.is_contiguous() or not seq_lens.is_contiguous():
+        raise ValueError("q, block_table and seq_lens must be contiguous")
+    B, hq, d = q.shape
+    npages, hkv, P, d2 = k_pages.shape
+    if tuple(v_pages.shape) != tuple(k_pages.shape) or v_pages.stride() != k_pages.stride():
+        raise ValueError("k_pages and v_pages must have the same shape and strides")
+    if k_pages.stride()[1:] != (P * d2, d2, 1):
+        raise ValueError("each page's [Hkv][P][D] block must be contiguous")
+    if out is None:
+        out = torch.empty_like(q)
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    if workspace is None:
+        workspace = make_workspace(B, hq, hkv, max_seq_len, chunk_tokens, device=q.device, stream=stream)
+    check(lib().neo_decode_attn(
+        q.data_ptr(), k_pages.data_ptr(), v_pages.data_ptr(), k_pages.stride(0),
+        int(num_pages if num_pages is not None else npages), block_table.data_ptr(), block_table.shape[1],
+        seq_lens.data_ptr(), out.data_ptr(), B, hq, hkv, d, P, int(max_seq_len), float(scale), int(chunk_tokens),
+        workspace.data_ptr(), workspace.numel(), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ KV pool
+
+
+class KVPool:
+    """GPU-cache + CPU-cache pool.  The device pool and the pinned
+    host pool are torch tensors owned by this object; the C handle owns only the
+    free lists."""
+
+    def __init__(self, num_layers: int, num_kv_heads: int, num_gpu_pages: int, num_host_pages: int = 0,
+                 page_size: int = 16, head_dim: int = 128, device=None, allocate: bool = True):
+        self.geo = Geometry(num_layers, num_kv_heads, head_dim, page_size, num_gpu_pages, num_host_pages)
+        gb, hb = ctypes.c_size_t(), ctypes.c_size_t()
+        check(lib().neo_kv_pool_bytes(ctypes.byref(self.geo), ctypes.byref(gb), ctypes.byref(hb)))
+        self.gpu_bytes, self.host_bytes = gb.value, hb.value
+        self.gpu = self.host = None
+        # allocate=False: accounting-only handle (allocator tests); sentinel bases
+        # that are never dereferenced because no swap/attention runs on it.
+        gptr, hptr = (1 << 40), ((1 << 41) if num_host_pages else None)
+        if allocate:
+            import torch
+            self.gpu = torch.empty(self.gpu_bytes // 2, dtype=torch.bfloat16, device=device or "cuda")
+            gptr = self.gpu.data_ptr()
+            if num_host_pages:
+                self.host = torch.empty(self.host_bytes // 2, dtype=torch.bfloat16, pin_memory=True)
+                hptr = self.host.data_ptr()
+        self._h = ctypes.c_void_p()
+        check(lib().neo_kv_pool_create(ctypes.byref(self.geo), gptr, self.gpu_bytes, hptr, self.host_bytes,
+                                       ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib().neo_kv_pool_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def alloc(self, where: int, n: int) -> np.ndarray:
+        ids = np.zeros(max(n, 1), dtype=np.int32)
+        check(lib().neo_kv_alloc(self._h, where, n, ids.ctypes.data))
+        return ids[:n].copy()
+
+    def free(self, where: int, ids) -> None:
+        a = _ids(ids)
+        check(lib().neo_kv_free(self._h, where, len(a), a.ctypes.data))
+
+    def free_count(self, where: int) -> int:
+        n = ctypes.c_int64()
+        check(lib().neo_kv_free_count(self._h, where, ctypes.byref(n)))
+        return n.value
+
+    def gpu_view(self):
+        """[L][2][num_gpu_pages][Hkv][P][D] view of the GPU-cache."""
+        g = self.geo
+        return self.gpu.view(g.num_layers, 2, g.num_gpu_pages, g.num_kv_heads, g.page_size, g.head_dim)
+
+    def host_view(self):
+        """[num_host_pages][L][2][Hkv][P][D] view of the CPU-cache."""
+        g = self.geo
+        return self.host.view(g.num_host_pages, g.num_layers, 2, g.num_kv_heads, g.page_size, g.head_dim)
+
+    def layer_view(self, layer: int):
+        """(k_pages, v_pages) [num_gpu_pages][Hkv][P][D] torch views via neo_kv_layer_view."""
+        import torch
+        k, v, stride = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+        check(lib().neo_kv_layer_view(self._h, layer, ctypes.byref(k), ctypes.byref(v), ctypes.byref(stride)))
+        g = self.geo
+        base = self.gpu.data_ptr()
+        ko = (k.value - base) // 2
+        vo = (v.value - base) // 2
+        shape = (g.num_gpu_pages, g.num_kv_heads, g.page_size, g.head_dim)
+        strides = (stride.value, g.page_size * g.head_dim, g.head_dim, 1)
+        return (torch.as_strided(self.gpu, shape, strides, ko), torch.as_strided(self.gpu, shape, strides, vo))
+
+    def staging_bytes(self, n: int, layer_begin: int = 0, layer_end: int | None = None) -> int:
+        le = self.geo.num_layers if layer_end is None else layer_end
+        out = ctypes.c_size_t()
+        check(lib().neo_kv_swap_staging_bytes(self._h, n, layer_begin, le, ctypes.byref(out)))
+        return out.value
+
+    def swap_out(self, gpu_ids, host_ids, staging, layer_begin: int = 0, layer_end: int | None = None,
+                 stream=None) -> None:
+        g, h = _ids(gpu_ids), _ids(host_ids)
+        if len(g) != len(h):
+            raise ValueError("gpu_ids and host_ids differ in length")
+        le = self.geo.num_layers if layer_end is None else layer_end
+        check(lib().neo_kv_swap_out(self._h, len(g), g.ctypes.data, h.ctypes.data, layer_begin, le,
+                                    _ptr(staging), staging.numel() * staging.element_size(), _stream(stream)))
+
+    def swap_in(self, host_ids, gpu_ids, staging, layer_begin: int = 0, layer_end: int | None = None,
+                stream=None) -> None:
+        g, h = _ids(gpu_ids), _ids(host_ids)
+        if len(g) != len(h):
+            raise ValueError("gpu_ids and host_ids differ in length")
+        le = self.geo.num_layers if layer_end is None else layer_end
+        check(lib().neo_kv_swap_in(self._h, len(g), h.ctypes.data, g.ctypes.data, layer_begin, le,
+                                   _ptr(staging), staging.numel() * staging.element_size(), _stream(stream)))

@@ -1,0 +1,225 @@
+"""C-ABI checks that need no GPU: every symbol include/neo.h declares is
+exported by libneo.so, argument validation returns the documented status
+without touching CUDA, and the two-pool page allocator keeps S:290-293's
+properties (conservation, atomicity, residency) under 10^5 random ops."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2411_01142_b200 import neo
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2411_01142_b200 import build
+    build.build()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "neo.h")).read()
+    return sorted(set(re.findall(r"NEO_API\s+[\w\s\*]+?\b(neo_\w+)\s*\(", src)))
+
+
+def test_every_declared_symbol_is_exported():
+    names = header_functions()
+    assert len(names) >= 16
+    L = neo.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    assert sorted(neo.EXPORTED) == names
+
+
+def test_version_and_error_text():
+    assert b"sm_100a" in neo.lib().neo_version()
+    with pytest.raises(neo.NeoError) as e:
+        neo.workspace_bytes(4, 30, 8, 100)                 # 30 % 8 != 0
+    assert e.value.status == neo.NEO_ERR_INVALID_ARG
+    assert "multiple" in str(e.value)
+
+
+def _attn(**kw):
+    args = dict(q=16, k=16, v=16, stride=2048 * 8, npages=10, bt=16, maxb=4, sl=16, out=16, B=2, hq=32, hkv=8,
+                d=128, P=16, msl=64, scale=0.088, C=0, ws=16, wsb=1 << 20, stream=0)
+    args.update(kw)
+    a = args
+    return neo.lib().neo_decode_attn(a["q"], a["k"], a["v"], a["stride"], a["npages"], a["bt"], a["maxb"], a["sl"],
+                                     a["out"], a["B"], a["hq"], a["hkv"], a["d"], a["P"], a["msl"],
+                                     ctypes.c_float(a["scale"]), a["C"], a["ws"], a["wsb"], a["stream"])
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(d=64), neo.NEO_ERR_UNSUPPORTED),
+    (dict(P=8), neo.NEO_ERR_UNSUPPORTED),
+    (dict(hq=30), neo.NEO_ERR_INVALID_ARG),
+    (dict(hq=128, hkv=8), neo.NEO_ERR_UNSUPPORTED),            # G = 16
+    (dict(q=0), neo.NEO_ERR_INVALID_ARG),
+    (dict(q=24), neo.NEO_ERR_INVALID_ARG),                     # misaligned
+    (dict(stride=2048 * 8 - 8), neo.NEO_ERR_INVALID_ARG),      # page stride < Hkv*P*D
+    (dict(msl=65), neo.NEO_ERR_INVALID_ARG),                   # > max_blocks * P
+    (dict(wsb=16), neo.NEO_ERR_INVALID_ARG),                   # workspace too small
+    (dict(C=24), neo.NEO_ERR_UNSUPPORTED),
+    (dict(C=1024), neo.NEO_ERR_UNSUPPORTED),
+    (dict(scale=0.0), neo.NEO_ERR_INVALID_ARG),
+    (dict(npages=0), neo.NEO_ERR_INVALID_ARG),
+])
+def test_decode_attn_validation(kw, status):
+    assert _attn(**kw) == status
+
+
+def test_decode_attn_batch_zero_is_noop():
+    assert _attn(B=0, q=0, out=0) == neo.NEO_OK
+
+
+def test_workspace_bytes_and_default_chunk():
+    assert neo.default_chunk(256, 8, 1126) == 256
+    assert neo.default_chunk(128, 8, 8192) == 512
+    assert neo.default_chunk(4, 32, 128) == 64
+    # single chunk: counters only; split: counters + (m, l) + fp32 partials
+    small = neo.workspace_bytes(4, 32, 32, 64, chunk_tokens=64)
+    assert small == 512
+    big = neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=256)
+    units = 256 * 8 * 5
+    assert big == 256 * 8 * 4 + units * 4 * 8 + units * 4 * 128 * 4
+
+
+def test_pool_bytes_and_layer_view():
+    pool = neo.KVPool(num_layers=3, num_kv_heads=8, num_gpu_pages=10, num_host_pages=4, allocate=False)
+    page = 8 * 16 * 128 * 2
+    assert pool.gpu_bytes == 3 * 2 * 10 * page
+    assert pool.host_bytes == 3 * 2 * 4 * page
+    pool.close()
+    # layer view pointer arithmetic on a fake (never dereferenced) base
+    geo = neo.Geometry(3, 8, 128, 16, 10, 0)
+    h = ctypes.c_void_p()
+    base = 1 << 32
+    neo.check(neo.lib().neo_kv_pool_create(ctypes.byref(geo), base, 3 * 2 * 10 * page, None, 0, ctypes.byref(h)))
+    k, v, s = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+    neo.check(neo.lib().neo_kv_layer_view(h, 2, ctypes.byref(k), ctypes.byref(v), ctypes.byref(s)))
+    assert k.value == base + 4 * 10 * page and v.value == base + 5 * 10 * page and s.value == 8 * 16 * 128
+    assert neo.lib().neo_kv_layer_view(h, 3, ctypes.byref(k), ctypes.byref(v), ctypes.byref(s)) == 1
+    neo.lib().neo_kv_pool_destroy(h)
+
+
+def test_pool_create_validation():
+    geo = neo.Geometry(1, 8, 128, 16, 10, 2)
+    h = ctypes.c_void_p()
+    L = neo.lib()
+    assert L.neo_kv_pool_create(ctypes.byref(geo), 1 << 32, 1, 1 << 33, 1 << 30, ctypes.byref(h)) == 1  # small
+    assert L.neo_kv_pool_create(ctypes.byref(geo), (1 << 32) + 8, 1 << 30, 1 << 33, 1 << 30,
+                                ctypes.byref(h)) == 1                                                   # misaligned
+    assert L.neo_kv_pool_create(ctypes.byref(geo), 1 << 32, 1 << 30, None, 1 << 30, ctypes.byref(h)) == 1
+    bad = neo.Geometry(1, 8, 96, 16, 10, 2)
+    assert L.neo_kv_pool_create(ctypes.byref(bad), 1 << 32, 1 << 30, 1 << 33, 1 << 30, ctypes.byref(h)) == 3
+
+
+def test_allocator_examples():
+    pool = neo.KVPool(1, 8, num_gpu_pages=10, num_host_pages=8, allocate=False)
+    a = pool.alloc(neo.NEO_GPU, 3)
+    assert pool.free_count(neo.NEO_GPU) == 7 and len(set(a)) == 3
+    with pytest.raises(neo.NeoError) as e:
+        pool.alloc(neo.NEO_GPU, 8)                         # free=7, need 8: state unchanged
+    assert e.value.status == neo.NEO_ERR_OUT_OF_PAGES and pool.free_count(neo.NEO_GPU) == 7
+    assert len(pool.alloc(neo.NEO_GPU, 0)) == 0
+    h = pool.alloc(neo.NEO_HOST, 5)
+    assert list(h) == [0, 1, 2, 3, 4]                      # one contiguous run
+    pool.free(neo.NEO_HOST, [1, 3])
+    h2 = pool.alloc(neo.NEO_HOST, 3)
+    assert list(h2) == [5, 6, 7]                           # first contiguous run of 3
+    h3 = pool.alloc(neo.NEO_HOST, 2)
+    assert sorted(h3) == [1, 3]                            # no run: lowest free ids
+    with pytest.raises(neo.NeoError):
+        pool.free(neo.NEO_GPU, [a[0], a[0]])               # duplicate: nothing freed
+    assert pool.free_count(neo.NEO_GPU) == 7
+    with pytest.raises(neo.NeoError):
+        pool.free(neo.NEO_GPU, [a[0], 9 if 9 not in a else 8])   # not allocated
+    assert pool.free_count(neo.NEO_GPU) == 7
+    pool.free(neo.NEO_GPU, a)
+    assert pool.free_count(neo.NEO_GPU) == 10
+
+
+def test_allocator_random_ops_conservation():
+    """10^5 random alloc/extend/migrate/release ops over two pools."""
+    rng = np.random.default_rng(0)
+    G, H = 300, 500
+    pool = neo.KVPool(1, 1, num_gpu_pages=G, num_host_pages=H, allocate=False)
+    reqs = {}                                   # id -> (where, list of pages)
+    owner = {neo.NEO_GPU: {}, neo.NEO_HOST: {}}  # page -> req
+    next_id = 0
+    for step in range(100000):
+        op = rng.integers(0, 4)
+        if op == 0 or not reqs:                 # allocate
+            where = int(rng.integers(0, 2))
+            n = int(rng.integers(0, 12))
+            before = pool.free_count(where)
+            try:
+                ids = pool.alloc(where, n)
+            except neo.NeoError as e:
+                assert e.status == neo.NEO_ERR_OUT_OF_PAGES and before < n
+                assert pool.free_count(where) == before
+                continue
+            for p in ids:
+                assert p not in owner[where]
+                owner[where][int(p)] = next_id
+            reqs[next_id] = (where, [int(p) for p in ids])
+            next_id += 1
+        else:
+            rid = list(reqs)[int(rng.integers(0, len(reqs)))]
+            where, pages = reqs[rid]
+            if op == 1:                         # extend by one page
+                try:
+                    p = int(pool.alloc(where, 1)[0])
+                except neo.NeoError:
+                    continue
+                owner[where][p] = rid
+                pages.append(p)
+            elif op == 2:                       # migrate to the other pool (all-or-nothing)
+                other = 1 - where
+                try:
+                    new = pool.alloc(other, len(pages))
+                except neo.NeoError:
+                    continue
+                pool.free(where, pages)
+                for p in pages:
+                    del owner[where][p]
+                for p in new:
+                    owner[other][int(p)] = rid
+                reqs[rid] = (other, [int(p) for p in new])
+            else:                               # release
+                pool.free(where, pages)
+                for p in pages:
+                    del owner[where][p]
+                del reqs[rid]
+        if step % 997 == 0:
+            assert pool.free_count(neo.NEO_GPU) + len(owner[neo.NEO_GPU]) == G
+            assert pool.free_count(neo.NEO_HOST) + len(owner[neo.NEO_HOST]) == H
+    assert pool.free_count(neo.NEO_GPU) + len(owner[neo.NEO_GPU]) == G
+    assert pool.free_count(neo.NEO_HOST) + len(owner[neo.NEO_HOST]) == H
+    # residency exclusivity: each request's pages are all in one pool
+    for rid, (where, pages) in reqs.items():
+        assert all(owner[where][p] == rid for p in pages)
+
+
+def test_swap_validation_without_gpu():
+    pool = neo.KVPool(4, 8, num_gpu_pages=10, num_host_pages=10, allocate=False)
+    g = pool.alloc(neo.NEO_GPU, 2)
+    h = pool.alloc(neo.NEO_HOST, 2)
+    L = neo.lib()
+    gi, hi = np.ascontiguousarray(g), np.ascontiguousarray(h)
+    per = pool.staging_bytes(1, 0, 4)
+    assert per == 4 * 2 * 8 * 16 * 128 * 2
+    # layer range out of bounds
+    assert L.neo_kv_swap_out(pool.handle, 2, gi.ctypes.data, hi.ctypes.data, 0, 5, 16, per, 0) == 1
+    # staging too small
+    assert L.neo_kv_swap_out(pool.handle, 2, gi.ctypes.data, hi.ctypes.data, 0, 4, 16, per - 16, 0) == 1
+    # unallocated host page
+    bad = np.array([h[0], 9], dtype=np.int32)
+    assert L.neo_kv_swap_out(pool.handle, 2, gi.ctypes.data, bad.ctypes.data, 0, 4, 16, per, 0) == 1
+    # duplicate gpu ids
+    dup = np.array([g[0], g[0]], dtype=np.int32)
+    assert L.neo_kv_swap_in(pool.handle, 2, hi.ctypes.data, dup.ctypes.data, 0, 4, 16, per, 0) == 1
+    assert L.neo_kv_swap_out(pool.handle, 0, None, None, 0, 4, None, 0, 0) == 0    # n = 0 no-op

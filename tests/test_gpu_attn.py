@@ -1,0 +1,216 @@
+"""GPU parity of neo_decode_attn against the fp64 oracle (SURVEY §8(c) items
+7-10 and 15's single-GPU part), through the C ABI.  Tolerance: the north
+star's |gpu - ref| <= 2e-3 + 1e-2 |ref| elementwise; bit-exact where the
+integer part (block table, masking, relocation) decides."""
+import math
+
+import numpy as np
+import pytest
+
+import neo_inputs as ni
+from harness import Case, within_tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2411_01142_b200 import build
+    build.build()
+
+
+def check_case(case, chunk=0, tag=""):
+    out = case.run(chunk_tokens=chunk)
+    got = case.out_f64(out)
+    worst = 0.0
+    for b in range(case.B):
+        ok, ratio = within_tol(got[b], case.oracle(b))
+        worst = max(worst, ratio)
+        assert ok, f"{tag} b={b} ctx={case.ctx[b]} err/tol={ratio:.3f}"
+    return out, worst
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 32), (32, 8), (64, 8), (16, 8), (8, 1)])
+@pytest.mark.parametrize("chunk", [0, 16, 64, 256, 512])
+def test_parity_ragged(hq, hkv, chunk):
+    ctx = [1, 15, 16, 17, 31, 32, 33, 127, 128, 129, 600, 1000]
+    case = Case(ctx, hq, hkv, seed=1 + hq + hkv + chunk)
+    check_case(case, chunk, f"G={hq // hkv} C={chunk}")
+
+
+@pytest.mark.parametrize("P,chunk", [(32, 64), (32, 0), (64, 128), (32, 512)])
+def test_parity_page_sizes(P, chunk):
+    case = Case([1, 31, 32, 33, 95, 513, 700], 32, 8, P=P, seed=7 + P)
+    check_case(case, chunk, f"P={P}")
+
+
+def test_parity_padded_page_stride():
+    # page-major style layout: pages 3x further apart than Hkv*P*D
+    case = Case([5, 40, 300], 32, 8, page_stride=3 * 8 * 16 * 128, seed=11)
+    check_case(case, 64)
+
+
+@pytest.mark.parametrize("variant", [ni.VARIANT_PEAKED, ni.VARIANT_SINK, ni.VARIANT_PEAKED | ni.VARIANT_SINK])
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (64, 8), (32, 32)])
+def test_parity_variants(variant, hq, hkv):
+    case = Case([1, 17, 250, 1100, 2049], hq, hkv, variant=variant, seed=21 + variant)
+    for chunk in (0, 64):
+        check_case(case, chunk, f"variant={variant}")
+
+
+def test_parity_random_configs():
+    """>= 500 random small configs (S:599 mirrored): ctx 1-600 incl. multiples of P
+    and P+-1, G in {1,2,4,8}, shuffled block tables, C in {16, 64, 256, 512}."""
+    rng = np.random.default_rng(599)
+    worst = 0.0
+    for trial in range(520):
+        G = int(rng.choice([1, 2, 4, 8]))
+        hkv = int(rng.choice([1, 2, 4, 8]))
+        B = int(rng.integers(1, 4))
+        P = int(rng.choice([16, 16, 32]))
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            ctx = rng.integers(1, 601, size=B)
+        else:
+            base = P * rng.integers(1, 600 // P + 1, size=B)
+            ctx = np.clip(base + (rng.integers(-1, 2, size=B) if kind == 1 else 0), 1, 600)
+        C = int(rng.choice([16, 64, 256, 512]))
+        if C % P:
+            C = P * max(1, C // P)
+        case = Case(ctx, hkv * G, hkv, P=P, seed=1000 + trial, variant=int(rng.choice([0, 0, 1, 2])))
+        _, r = check_case(case, C, f"trial {trial}")
+        worst = max(worst, r)
+    print(f"worst err/tol over random configs: {worst:.3f}")
+
+
+def test_single_token_bitwise_v():
+    case = Case([1, 1, 1], 32, 8, seed=5)
+    out = case.run()
+    got = case.out_f64(out)
+    for b in range(3):
+        for h in range(32):
+            assert np.array_equal(got[b, h], ni.bf16_bits_to_f64(case.v_req[b][0, h // 4]))
+
+
+def test_one_hot_dominant_bitwise():
+    """q = 1, k_j = 4 (s_j = 45.25), other k = 0: output is v_j bit for bit."""
+    import torch
+    from paper_2411_01142_b200 import neo
+    n, j = 16384, 9876
+    case = Case([n], 8, 1, seed=6)
+    k = case.k_dev.view(-1, 16, 128)             # [pages][P][D] (Hkv=1)
+    k.zero_()
+    table = case.table[0]
+    k[table[j // 16], j % 16] = 4.0
+    case.q_dev.fill_(1.0)
+    for chunk in (0, 64, 512):
+        out = case.run(chunk_tokens=chunk)
+        got = case.out_f64(out)
+        vj = ni.bf16_bits_to_f64(case.v_req[0][j, 0])
+        for h in range(8):
+            assert np.array_equal(got[0, h], vj), chunk
+
+
+def test_identical_keys_mean_of_v():
+    case = Case([3000], 32, 8, seed=8)
+    k = case.k_dev
+    kb = k[case.table[0, 0], :, 0:1, :].clone()          # token 0's K row for all heads
+    k.copy_(kb.unsqueeze(0).expand(k.shape[0], -1, 16, -1))
+    out = case.run()
+    got = case.out_f64(out)
+    vm = ni.bf16_bits_to_f64(case.v_req[0]).mean(axis=0)  # [Hkv][D]
+    for h in range(32):
+        ok, r = within_tol(got[0, h], vm[h // 4])
+        assert ok, r
+
+
+def test_relocation_and_poison_bitwise():
+    """Moving physical pages (same logical order) and NaN in every slot the kernel
+    must not read leave the output bitwise unchanged (items 9, 10)."""
+    ctx = [1, 17, 100, 257, 1000]
+    a = Case(ctx, 32, 8, seed=9, table_seed=1, tail="zero", fill_unused="zero", extra_pages=0)
+    b = Case(ctx, 32, 8, seed=9, table_seed=2, tail="nan", fill_unused="nan", extra_pages=40)
+    assert not np.array_equal(a.table, b.table)
+    for chunk in (0, 16, 64):
+        import torch
+        oa = a.run(chunk_tokens=chunk)
+        ob = b.run(chunk_tokens=chunk)
+        assert torch.isfinite(ob.float()).all()
+        assert torch.equal(oa.view(torch.int16), ob.view(torch.int16))
+
+
+def test_block_table_padding_ignored():
+    import torch
+    case = Case([20, 50], 32, 8, seed=12)
+    bt = torch.full((2, case.max_blocks + 5), 12345678, dtype=torch.int32, device="cuda")
+    bt[:, :case.max_blocks] = case.bt_dev
+    bt[0, 2:] = -1                                  # entries past ceil(ctx/P) are never read
+    base = case.run()
+    from paper_2411_01142_b200 import neo
+    out = neo.decode_attn(case.q_dev, case.k_dev, case.v_dev, bt, case.sl_dev, case.max_seq_len)
+    torch.cuda.synchronize()
+    assert torch.equal(base.view(torch.int16), out.view(torch.int16))
+
+
+def test_shared_pages_across_requests():
+    """The same physical pages in two rows (read-only sharing, reading c10)."""
+    import torch
+    case = Case([300, 300], 32, 8, seed=13)
+    bt = case.bt_dev.clone()
+    bt[1] = bt[0]
+    from paper_2411_01142_b200 import neo
+    q = case.q_dev.clone()
+    q[1] = q[0]
+    out = neo.decode_attn(q, case.k_dev, case.v_dev, bt, case.sl_dev, case.max_seq_len, chunk_tokens=64)
+    torch.cuda.synchronize()
+    assert torch.equal(out[0].view(torch.int16), out[1].view(torch.int16))
+
+
+def test_determinism_run_to_run():
+    import torch
+    case = Case(list(range(1, 2000, 97)), 64, 8, seed=14)
+    outs = [case.run(chunk_tokens=64).clone() for _ in range(3)]
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int16), outs[0].view(torch.int16))
+
+
+def test_empty_context_zero_row():
+    import torch
+    case = Case([0, 5, 0, 300], 32, 8, seed=15)
+    out = case.run(chunk_tokens=64)
+    got = case.out_f64(out)
+    assert (got[0] == 0).all() and (got[2] == 0).all()
+    for b in (1, 3):
+        assert within_tol(got[b], case.oracle(b))[0]
+
+
+def test_workspace_reuse_across_shapes():
+    """One workspace, many calls with different shapes: counters stay consistent."""
+    from paper_2411_01142_b200 import neo
+    ws = neo.make_workspace(64, 64, 8, 4096, chunk_tokens=16)
+    for seed, ctx in enumerate([[1000, 2000], [4096], [17, 33, 64], list(range(5, 900, 37))]):
+        case = Case(ctx, 32, 8, seed=40 + seed)
+        out = case.run(chunk_tokens=16, workspace=ws)
+        got = case.out_f64(out)
+        for b in range(case.B):
+            assert within_tol(got[b], case.oracle(b))[0]
+
+
+def test_debug_validate_rejects_bad_metadata(monkeypatch):
+    import torch
+    from paper_2411_01142_b200 import neo
+    monkeypatch.setenv("NEO_DEBUG_VALIDATE", "1")
+    case = Case([20, 50], 32, 8, seed=16)
+    case.run()                                         # valid metadata passes
+    bt = case.bt_dev.clone()
+    bt[1, 1] = case.npages + 5
+    with pytest.raises(neo.NeoError) as e:
+        neo.decode_attn(case.q_dev, case.k_dev, case.v_dev, bt, case.sl_dev, case.max_seq_len)
+    assert e.value.status == neo.NEO_ERR_INVALID_ARG
+    sl = case.sl_dev.clone()
+    sl[0] = case.max_seq_len + 1
+    with pytest.raises(neo.NeoError):
+        neo.decode_attn(case.q_dev, case.k_dev, case.v_dev, case.bt_dev, sl, case.max_seq_len)

@@ -1,0 +1,80 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (library-default chunk, device-generated inputs, scattered block
+tables): sampled requests of sampled layers are checked one by one against the
+fp64 oracle, and every output row is checked to be finite.  Head-sharded (c4)
+and request-sharded (c5) shards are checked the same way on their slice."""
+import math
+
+import numpy as np
+import pytest
+
+from harness import within_tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2411_01142_b200 import build
+    build.build()
+
+
+def run_and_sample(wl, layers, n_samples, rng, **kw):
+    import torch
+
+    import oracle
+    import neo_inputs as ni
+    from neo_inputs.gpu import GpuBatch
+    from paper_2411_01142_b200 import neo
+    gb = GpuBatch(wl, layers=max(layers) + 1, **kw)
+    worst = 0.0
+    for layer in layers:
+        k, v = gb.layer(layer)
+        out = neo.decode_attn(gb.q[layer], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len)
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+        picks = set(rng.choice(gb.B, size=min(n_samples, gb.B), replace=False).tolist())
+        picks |= {int(np.argmax(gb.ctx)), int(np.argmin(gb.ctx))}          # longest and shortest
+        for b in sorted(picks):
+            q, kb, vb = gb.oracle_inputs(b, layer)
+            ref = oracle.decode_attention(q, kb, vb, np.float32(1 / math.sqrt(128)))
+            got = ni.bf16_bits_to_f64(out[b].view(torch.int16).cpu().numpy().view(np.uint16))
+            ok, r = within_tol(got, ref)
+            worst = max(worst, r)
+            assert ok, f"{wl.name} layer {layer} request {b} ctx {gb.ctx[b]} err/tol {r:.3f}"
+    del gb
+    torch.cuda.empty_cache()
+    return worst
+
+
+@pytest.mark.parametrize("name,layers,n", [("c1", [0], 4), ("c2", [0, 31], 12), ("c2s", [5], 12),
+                                           ("c3", [0, 17], 8), ("c4", [0, 3], 10), ("c5", [0], 12)])
+def test_fullsize_sampled(name, layers, n):
+    from neo_inputs.workloads import WORKLOADS
+    rng = np.random.default_rng(hash(name) % 1000)
+    w = run_and_sample(WORKLOADS[name], layers, n, rng)
+    print(f"{name}: worst err/tol {w:.3f}")
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_fullsize_head_shard_c4(world):
+    from neo_inputs.workloads import WORKLOADS
+    from paper_2411_01142_b200.shard import head_shard
+    wl = WORKLOADS["c4"]
+    rng = np.random.default_rng(world)
+    for rank in (0, world - 1):
+        kvh, qh = head_shard(wl.hq, wl.hkv, rank, world)
+        run_and_sample(wl, [1], 6, rng, kv_heads=kvh, q_heads=qh)
+
+
+def test_fullsize_request_shard_c5():
+    from neo_inputs.workloads import WORKLOADS
+    from paper_2411_01142_b200.shard import lpt_assign
+    wl = WORKLOADS["c5"]
+    ctx = wl.contexts()
+    parts = lpt_assign(ctx[:512], 8)                        # f = 0.5, 8 ranks
+    rng = np.random.default_rng(5)
+    run_and_sample(wl, [0], 6, rng, ctx=ctx, req_ids=parts[3])

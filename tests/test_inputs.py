@@ -88,3 +88,30 @@ def test_block_tables_are_a_scattered_partition():
     assert used.max() < 64 and used.min() >= 0
     for i in range(len(ctx)):
         assert (table[i, need[i]:] == -1).all()
+
+
+def test_c_generator_matches_numpy():
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        hkv = int(rng.choice([1, 2, 8, 32]))
+        G = int(rng.choice([1, 4, 8]))
+        hq = hkv * G
+        b = int(rng.integers(0, 1024))
+        t0 = int(rng.integers(0, 50))
+        t1 = t0 + int(rng.integers(1, 40))
+        layer = int(rng.integers(0, 80))
+        variant = int(rng.integers(0, 4))
+        g0 = int(rng.integers(0, hkv))
+        heads = np.arange(g0, hkv)
+        for kind in (ni.KIND_K, ni.KIND_V):
+            a = ni.kv_bits(11, layer, kind, b, t0, t1, hkv, 128, heads=heads, variant=variant, hq_total=hq)
+            c = ni.kv_bits(11, layer, kind, b, t0, t1, hkv, 128, heads=heads, variant=variant, hq_total=hq,
+                           use_c=False)
+            assert np.array_equal(a, c)
+        if t0 == 0 or True:
+            a = ni.kv_bits(11, layer, ni.KIND_K, b, 0, 3, hkv, 128, variant=variant, hq_total=hq)
+            c = ni.kv_bits(11, layer, ni.KIND_K, b, 0, 3, hkv, 128, variant=variant, hq_total=hq, use_c=False)
+            assert np.array_equal(a, c)
+        qa = ni.q_bits(11, layer, [b, b + 1], hq, 128, heads=np.arange(G, hq), variant=variant)
+        qc = ni.q_bits(11, layer, [b, b + 1], hq, 128, heads=np.arange(G, hq), variant=variant, use_c=False)
+        assert np.array_equal(qa, qc)
