@@ -24,16 +24,21 @@
 // order (deterministic, no float atomics) and resets the counter.
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 #include "neo_internal.cuh"
 
 namespace neo {
 namespace {
 
-constexpr int kWarps = 4;
-constexpr int kStages = 4;
 constexpr int kStageBytes = 2 * kTileBytes;
-constexpr int kSmemBytes = kWarps * kStages * kStageBytes + 1024;
 constexpr unsigned kFull = 0xffffffffu;
+template <int W, int S>
+constexpr int smem_bytes() {
+  return W * S * kStageBytes + 1024;
+}
 
 struct KArgs {
   const uint16_t* q;
@@ -157,6 +162,7 @@ __device__ __forceinline__ void store_row8(uint16_t* dst, const float (&v)[8], f
   *reinterpret_cast<uint4*>(dst) = w;
 }
 
+template <int kWarps, int kStages>
 __global__ void __launch_bounds__(kWarps * 32)
     decode_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                        const KArgs a) {
@@ -422,28 +428,73 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 }  // namespace
 
-WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks) {
+size_t workspace_counter_cap(size_t ws_bytes) { return (ws_bytes / 64) & ~size_t(255); }
+
+static size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static void data_bytes(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t* ml, size_t* acc) {
   const int64_t G = hkv > 0 ? hq / hkv : 0;
   const int64_t units = static_cast<int64_t>(batch) * hkv * max_chunks;
-  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const bool split = max_chunks > 1;
+  *ml = split ? up256(static_cast<size_t>(units * G) * sizeof(float2)) : 0;
+  *acc = split ? up256(static_cast<size_t>(units * G * kHeadDim) * sizeof(float)) : 0;
+}
+
+WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t ws_bytes) {
+  size_t ml, acc;
+  data_bytes(batch, hq, hkv, max_chunks, &ml, &acc);
   WorkspaceLayout w;
   w.cnt_off = 0;
-  w.ml_off = up(static_cast<size_t>(batch) * hkv * sizeof(int32_t));
-  const bool split = max_chunks > 1;
-  w.acc_off = w.ml_off + (split ? up(static_cast<size_t>(units * G) * sizeof(float2)) : 0);
-  w.total = w.acc_off + (split ? up(static_cast<size_t>(units * G * kHeadDim) * sizeof(float)) : 0);
-  if (w.total == 0) w.total = 256;
+  w.cnt_cap = workspace_counter_cap(ws_bytes);
+  w.ml_off = w.cnt_cap;
+  w.acc_off = w.ml_off + ml;
+  w.total = w.acc_off + acc;
+  w.fits = w.total <= ws_bytes && static_cast<size_t>(batch) * hkv * sizeof(int32_t) <= w.cnt_cap;
   return w;
 }
 
-neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const CUtensorMap& tmv) {
+size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks) {
+  size_t ml, acc;
+  data_bytes(batch, hq, hkv, max_chunks, &ml, &acc);
+  const size_t need_cnt = up256(static_cast<size_t>(batch) * hkv * sizeof(int32_t));
+  size_t S = up256(ml + acc + need_cnt + 256);
+  while (!workspace_layout(batch, hq, hkv, max_chunks, S).fits) S = up256(S + std::max<size_t>(256, S / 128));
+  return S;
+}
+
+template <int W, int S>
+static neo_status launch_cfg(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t units,
+                             cudaStream_t stream) {
   static bool configured = false;
+  constexpr int smem = smem_bytes<W, S>();
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaError_t e =
+        cudaFuncSetAttribute(decode_attn_kernel<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_kernel)");
     configured = true;
   }
-  const WorkspaceLayout w = workspace_layout(L.batch, L.hq, L.hkv, L.max_chunks);
+  const int64_t grid = (units + W - 1) / W;
+  decode_attn_kernel<W, S><<<static_cast<unsigned>(grid), W * 32, smem, stream>>>(tmk, tmv, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
+  return NEO_OK;
+}
+
+// Kernel shape (warps per CTA, TMA stages per warp).  NEO_ATTN_CFG="W,S" selects
+// another compiled shape for tuning experiments.
+static int attn_cfg() {
+  static int cfg = [] {
+    const char* v = std::getenv("NEO_ATTN_CFG");
+    if (!v) return 44;
+    int w = 0, s = 0;
+    if (std::sscanf(v, "%d,%d", &w, &s) != 2) return 44;
+    return w * 10 + s;
+  }();
+  return cfg;
+}
+
+neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const CUtensorMap& tmv) {
+  const WorkspaceLayout w = workspace_layout(L.batch, L.hq, L.hkv, L.max_chunks, L.workspace_bytes);
   uint8_t* ws = static_cast<uint8_t*>(L.workspace);
   KArgs a;
   a.q = static_cast<const uint16_t*>(L.q);
@@ -463,11 +514,16 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.max_chunks = L.max_chunks;
   a.scale_log2 = L.scale * 1.4426950408889634f;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
-  const int64_t grid = (units + kWarps - 1) / kWarps;
-  decode_attn_kernel<<<static_cast<unsigned>(grid), kWarps * 32, kSmemBytes, L.stream>>>(tmk, tmv, a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
-  return NEO_OK;
+  switch (attn_cfg()) {
+    case 43: return launch_cfg<4, 3>(a, tmk, tmv, units, L.stream);
+    case 42: return launch_cfg<4, 2>(a, tmk, tmv, units, L.stream);
+    case 46: return launch_cfg<4, 6>(a, tmk, tmv, units, L.stream);
+    case 24: return launch_cfg<2, 4>(a, tmk, tmv, units, L.stream);
+    case 26: return launch_cfg<2, 6>(a, tmk, tmv, units, L.stream);
+    case 83: return launch_cfg<8, 3>(a, tmk, tmv, units, L.stream);
+    case 82: return launch_cfg<8, 2>(a, tmk, tmv, units, L.stream);
+    default: return launch_cfg<4, 4>(a, tmk, tmv, units, L.stream);
+  }
 }
 
 }  // namespace neo

@@ -353,7 +353,7 @@ NEO_API neo_status neo_decode_attn_workspace_bytes(int32_t batch, int32_t hq, in
   neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, 16);
   if (st != NEO_OK) return st;
   const int32_t max_chunks = std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
-  *bytes = neo::workspace_layout(batch, hq, hkv, max_chunks).total;
+  *bytes = neo::workspace_required(batch, hq, hkv, max_chunks);
   return NEO_OK;
 }
 
@@ -384,9 +384,9 @@ NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const voi
     return fail(NEO_ERR_INVALID_ARG, "max_seq_len exceeds max_blocks * page_size");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(NEO_ERR_INVALID_ARG, "scale must be finite and > 0");
   const int32_t max_chunks = std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
-  const neo::WorkspaceLayout wl = neo::workspace_layout(batch, hq, hkv, max_chunks);
-  if (workspace_bytes < wl.total)
-    return fail(NEO_ERR_INVALID_ARG, "workspace too small: need " + std::to_string(wl.total) + " bytes");
+  if (!neo::workspace_layout(batch, hq, hkv, max_chunks, workspace_bytes).fits)
+    return fail(NEO_ERR_INVALID_ARG, "workspace too small: need " +
+                                         std::to_string(neo::workspace_required(batch, hq, hkv, max_chunks)) + " bytes");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (neo::debug_validate_enabled()) {
     st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_seq_len, num_pages, s);
@@ -397,8 +397,8 @@ NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const voi
   if (st != NEO_OK) return st;
   st = neo::tensor_map(v_pages, page_stride, num_pages, hkv, page_size, &tmv);
   if (st != NEO_OK) return st;
-  neo::AttnLaunch L{q, out, block_table, seq_lens, workspace, batch, hq, hkv, page_size, max_blocks,
-                    chunk_tokens, max_chunks, scale, s};
+  neo::AttnLaunch L{q, out, block_table, seq_lens, workspace, workspace_bytes, batch, hq, hkv, page_size,
+                    max_blocks, chunk_tokens, max_chunks, scale, s};
   return neo::launch_decode_attn(L, tmk, tmv);
 }
 

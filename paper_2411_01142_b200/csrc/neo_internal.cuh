@@ -30,15 +30,22 @@ struct AttnLaunch {
   const int32_t* block_table;
   const int32_t* seq_lens;
   void* workspace;
+  size_t workspace_bytes;
   int32_t batch, hq, hkv, page_size, max_blocks, chunk_tokens, max_chunks;
   float scale;
   cudaStream_t stream;
 };
-// Byte layout of the workspace for a call shape.
+// Byte layout of a workspace of `ws_bytes` bytes for a call shape.  The
+// completion counters occupy [0, counter_cap(ws_bytes)) -- a region fixed by the
+// workspace size alone, so calls of different shapes sharing one workspace
+// never alias one call's counters with another call's partials.
 struct WorkspaceLayout {
-  size_t cnt_off, ml_off, acc_off, total;
+  size_t cnt_off, cnt_cap, ml_off, acc_off, total;
+  bool fits;
 };
-WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks);
+size_t workspace_counter_cap(size_t ws_bytes);
+size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks);
+WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t ws_bytes);
 neo_status launch_decode_attn(const AttnLaunch& a, const CUtensorMap& tmk, const CUtensorMap& tmv);
 // debug validation of device metadata (syncs the stream)
 neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
