@@ -35,10 +35,6 @@ namespace {
 
 constexpr int kStageBytes = 2 * kTileBytes;
 constexpr unsigned kFull = 0xffffffffu;
-template <int W, int S>
-constexpr int smem_bytes() {
-  return W * S * kStageBytes + 1024;
-}
 
 struct KArgs {
   const uint16_t* q;
@@ -49,6 +45,7 @@ struct KArgs {
   float2* ws_ml;
   int32_t* ws_cnt;
   int32_t batch, hq, hkv, G, page_size, max_blocks, chunk_tiles, max_chunks;
+  int32_t ctl_off;  // index (in ws_cnt) of the persistent kernel's claim/exit counters
   float scale_log2;
 };
 
@@ -162,235 +159,175 @@ __device__ __forceinline__ void store_row8(uint16_t* dst, const float (&v)[8], f
   *reinterpret_cast<uint4*>(dst) = w;
 }
 
-template <int kWarps, int kStages>
-__global__ void __launch_bounds__(kWarps * 32)
-    decode_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                       const KArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+// ------------------------------------------------------------------ tile math
 
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int r = lane >> 2;   // MMA groupID
-  const int qd = lane & 3;   // MMA thread-in-group
+struct Acc {
+  float o[8][4];  // O^T fragments: o[i][0|2] head 2qd, o[i][1|3] head 2qd+1; dims 8r+i | 64+8r+i
+  float m0, m1, l0, l1;
+};
 
-  const int64_t unit = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
-  const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
-  const int c = static_cast<int>(unit / BH);
-  if (c >= a.max_chunks) return;
-  const int bg = static_cast<int>(unit - static_cast<int64_t>(c) * BH);
-  const int b = bg / a.hkv;
-  const int g = bg - b * a.hkv;
-  const int G = a.G;
-
-  const int ctx = __ldg(a.seq_lens + b);
-  if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
-    if (c == 0) {
-      uint16_t* o = a.out + (static_cast<int64_t>(b) * a.hq + g * G) * kHeadDim;
-      for (int e = lane * 8; e < G * kHeadDim; e += 32 * 8) *reinterpret_cast<uint4*>(o + e) = make_uint4(0, 0, 0, 0);
-    }
-    return;
-  }
-  const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
-  const int n_chunks = (ntile_total + a.chunk_tiles - 1) / a.chunk_tiles;
-  if (c >= n_chunks) return;
-  const int t_begin = c * a.chunk_tiles;
-  const int nt = min(a.chunk_tiles, ntile_total - t_begin);
-
-  // block-table walk (a1): lane i holds the physical page of tile i of the unit
-  int my_pid = 0;
-  if (lane < nt) {
-    const int tok = (t_begin + lane) * kTileTokens;
-    my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + tok / a.page_size);
-  }
-
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
-  const uint32_t bar0 = smem_u32(&bars[warp][0]);
-  if (lane == 0) {
+__device__ __forceinline__ void acc_reset(Acc& s) {
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(bar0 + 8 * s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  const uint64_t policy = evict_first_policy();
+  for (int i = 0; i < 8; ++i) s.o[i][0] = s.o[i][1] = s.o[i][2] = s.o[i][3] = 0.f;
+  s.m0 = s.m1 = -INFINITY;
+  s.l0 = s.l1 = 0.f;
+}
 
-  // KV stream (a2): tile j of the unit -> stage j % kStages
-  auto issue = [&](int j) {
-    const int pid = __shfl_sync(kFull, my_pid, j);
-    if (lane == 0) {
-      const int s = j % kStages;
-      const int tok_in_page = ((t_begin + j) * kTileTokens) % a.page_size;
-      const uint32_t bar = bar0 + 8 * s;
-      const uint32_t dst = sbase + s * kStageBytes;
-      mbar_arrive_expect_tx(bar, kStageBytes);
-      tma_load_tile(dst, &tmk, tok_in_page, g, pid, bar, policy);
-      tma_load_tile(dst + kTileBytes, &tmv, tok_in_page, g, pid, bar, policy);
-    }
-  };
-  const int npro = nt < kStages ? nt : kStages;
-  for (int j = 0; j < npro; ++j) issue(j);
-
-  // Q fragment (B operand of S^T = K Q^T): head r of the group, dims of chunks
-  // qd + 4i in the same order as the K registers.  Heads r >= G are zero.
-  uint4 qf[4];
-  if (r < G) {
-    const uint16_t* qp = a.q + (static_cast<int64_t>(b) * a.hq + g * G + r) * kHeadDim;
+// Q fragment (B operand of S^T = K Q^T): head r of the group, dims of chunks
+// qd + 4i in the same order as the K registers.  Heads r >= G are zero.
+__device__ __forceinline__ void load_q(const KArgs& a, int b, int g, int r, int qd, uint4 (&qf)[4]) {
+  if (r < a.G) {
+    const uint16_t* qp = a.q + (static_cast<int64_t>(b) * a.hq + g * a.G + r) * kHeadDim;
 #pragma unroll
     for (int i = 0; i < 4; ++i) qf[i] = __ldg(reinterpret_cast<const uint4*>(qp + 8 * (qd + 4 * i)));
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i) qf[i] = make_uint4(0, 0, 0, 0);
   }
+}
 
-  float o[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
+// One 16-token tile (K at sk, V at sk + 4 KiB, 128B-swizzled) folded into the
+// running (O, m, l).  `valid` = tokens of the tile inside the context (>= 1).
+__device__ __forceinline__ void compute_tile(uint32_t sk, const uint4 (&qf)[4], int valid, float sl2, int r, int qd,
+                                             Acc& s) {
+  const uint32_t sv = sk + kTileBytes;
   const int tokA = tok_pi(r), tokB = 8 + tokA;              // S^T rows r, r+8
   const int vt0 = tok_pi(2 * qd), vt1 = tok_pi(2 * qd + 1);  // P.V k-slots 2qd, 2qd+1 (+8)
-  const float sl2 = a.scale_log2;
 
-  for (int j = 0; j < nt; ++j) {
-    const int s = j % kStages;
-    mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
-    const uint32_t sk = sbase + s * kStageBytes;
-    const uint32_t sv = sk + kTileBytes;
-
-    // (a3) scores: S^T = K_tile . Q^T
-    uint4 ka[4], kb[4];
+  // (a3) scores: S^T = K_tile . Q^T
+  uint4 ka[4], kb[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      ka[i] = lds128(sk + swz(tokA, qd + 4 * i));
-      kb[i] = lds128(sk + swz(tokB, qd + 4 * i));
-    }
-    float sc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < 4; ++i) {
+    ka[i] = lds128(sk + swz(tokA, qd + 4 * i));
+    kb[i] = lds128(sk + swz(tokB, qd + 4 * i));
+  }
+  float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      const int i = jj >> 1, w = 2 * (jj & 1);
-      mma_bf16(sc, word(ka[i], w), word(kb[i], w), word(ka[i], w + 1), word(kb[i], w + 1), word(qf[i], w),
-               word(qf[i], w + 1));
-    }
-    // V fragments: tokens vt0, vt1, vt0+8, vt1+8; chunks r and r+8
-    uint4 v00 = lds128(sv + swz(vt0, r)), v01 = lds128(sv + swz(vt0, r + 8));
-    uint4 v10 = lds128(sv + swz(vt1, r)), v11 = lds128(sv + swz(vt1, r + 8));
-    uint4 v20 = lds128(sv + swz(vt0 + 8, r)), v21 = lds128(sv + swz(vt0 + 8, r + 8));
-    uint4 v30 = lds128(sv + swz(vt1 + 8, r)), v31 = lds128(sv + swz(vt1 + 8, r + 8));
+  for (int jj = 0; jj < 8; ++jj) {
+    const int i = jj >> 1, w = 2 * (jj & 1);
+    mma_bf16(sc, word(ka[i], w), word(kb[i], w), word(ka[i], w + 1), word(kb[i], w + 1), word(qf[i], w),
+             word(qf[i], w + 1));
+  }
+  // V fragments: tokens vt0, vt1, vt0+8, vt1+8; chunks r and r+8
+  uint4 v00 = lds128(sv + swz(vt0, r)), v01 = lds128(sv + swz(vt0, r + 8));
+  uint4 v10 = lds128(sv + swz(vt1, r)), v11 = lds128(sv + swz(vt1, r + 8));
+  uint4 v20 = lds128(sv + swz(vt0 + 8, r)), v21 = lds128(sv + swz(vt0 + 8, r + 8));
+  uint4 v30 = lds128(sv + swz(vt1 + 8, r)), v31 = lds128(sv + swz(vt1 + 8, r + 8));
 
-    float x0 = sc[0] * sl2, x1 = sc[1] * sl2, x2 = sc[2] * sl2, x3 = sc[3] * sl2;
-    const int valid = ctx - (t_begin + j) * kTileTokens;  // >= 1
-    if (valid < kTileTokens) {                            // ragged last tile: mask scores, zero V
-      const uint4 z = make_uint4(0, 0, 0, 0);
-      if (tokA >= valid) x0 = x1 = -INFINITY;
-      if (tokB >= valid) x2 = x3 = -INFINITY;
-      if (vt0 >= valid) v00 = v01 = z;
-      if (vt1 >= valid) v10 = v11 = z;
-      if (vt0 + 8 >= valid) v20 = v21 = z;
-      if (vt1 + 8 >= valid) v30 = v31 = z;
-    }
-
-    // (a4) online softmax; token 0 of every tile is valid, so the tile max is finite
-    float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
-#pragma unroll
-    for (int off = 4; off < 32; off <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, off));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, off));
-    }
-    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
-    if (__any_sync(kFull, (mn0 > m0) || (mn1 > m1))) {
-      const float al0 = ex2(m0 - mn0), al1 = ex2(m1 - mn1);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        o[i][0] *= al0;
-        o[i][2] *= al0;
-        o[i][1] *= al1;
-        o[i][3] *= al1;
-      }
-      l0 *= al0;
-      l1 *= al1;
-      m0 = mn0;
-      m1 = mn1;
-    }
-    const float p0 = ex2(x0 - m0), p1 = ex2(x1 - m1), p2 = ex2(x2 - m0), p3 = ex2(x3 - m1);
-    l0 += p0 + p2;
-    l1 += p1 + p3;
-    const uint32_t ht = pack_bf16(p0, p1), hb = pack_bf16(p2, p3);
-    const uint32_t lt = pack_bf16(p0 - bf_lo(ht), p1 - bf_hi(ht));
-    const uint32_t lb = pack_bf16(p2 - bf_lo(hb), p3 - bf_hi(hb));
-    const uint32_t bh0 = movtrans(ht), bh1 = movtrans(hb), bl0 = movtrans(lt), bl1 = movtrans(lb);
-
-    // (a5) O^T += V^T . P^T  (hi and lo parts of P)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t sel = (i & 1) ? 0x7632u : 0x5410u;
-      const int w = i >> 1;
-      const uint32_t a0 = prmt(word(v00, w), word(v10, w), sel);
-      const uint32_t a1 = prmt(word(v01, w), word(v11, w), sel);
-      const uint32_t a2 = prmt(word(v20, w), word(v30, w), sel);
-      const uint32_t a3 = prmt(word(v21, w), word(v31, w), sel);
-      mma_bf16(o[i], a0, a1, a2, a3, bh0, bh1);
-      mma_bf16(o[i], a0, a1, a2, a3, bl0, bl1);
-    }
-
-    __syncwarp();
-    if (j + kStages < nt) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(j + kStages);
-    }
+  float x0 = sc[0] * sl2, x1 = sc[1] * sl2, x2 = sc[2] * sl2, x3 = sc[3] * sl2;
+  if (valid < kTileTokens) {  // ragged last tile: mask scores, zero V (NaN-safe)
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    if (tokA >= valid) x0 = x1 = -INFINITY;
+    if (tokB >= valid) x2 = x3 = -INFINITY;
+    if (vt0 >= valid) v00 = v01 = z;
+    if (vt1 >= valid) v10 = v11 = z;
+    if (vt0 + 8 >= valid) v20 = v21 = z;
+    if (vt1 + 8 >= valid) v30 = v31 = z;
   }
 
+  // (a4) online softmax; token 0 of every tile is valid, so the tile max is finite
+  float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
 #pragma unroll
   for (int off = 4; off < 32; off <<= 1) {
-    l0 += __shfl_xor_sync(kFull, l0, off);
-    l1 += __shfl_xor_sync(kFull, l1, off);
+    mx0 = fmaxf(mx0, __shfl_xor_sync(kFull, mx0, off));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(kFull, mx1, off));
+  }
+  const float mn0 = fmaxf(s.m0, mx0), mn1 = fmaxf(s.m1, mx1);
+  if (__any_sync(kFull, (mn0 > s.m0) || (mn1 > s.m1))) {
+    const float al0 = ex2(s.m0 - mn0), al1 = ex2(s.m1 - mn1);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s.o[i][0] *= al0;
+      s.o[i][2] *= al0;
+      s.o[i][1] *= al1;
+      s.o[i][3] *= al1;
+    }
+    s.l0 *= al0;
+    s.l1 *= al1;
+    s.m0 = mn0;
+    s.m1 = mn1;
+  }
+  const float p0 = ex2(x0 - s.m0), p1 = ex2(x1 - s.m1), p2 = ex2(x2 - s.m0), p3 = ex2(x3 - s.m1);
+  s.l0 += p0 + p2;
+  s.l1 += p1 + p3;
+  const uint32_t ht = pack_bf16(p0, p1), hb = pack_bf16(p2, p3);
+  const uint32_t lt = pack_bf16(p0 - bf_lo(ht), p1 - bf_hi(ht));
+  const uint32_t lb = pack_bf16(p2 - bf_lo(hb), p3 - bf_hi(hb));
+  const uint32_t bh0 = movtrans(ht), bh1 = movtrans(hb), bl0 = movtrans(lt), bl1 = movtrans(lb);
+
+  // (a5) O^T += V^T . P^T  (hi and lo parts of P)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t sel = (i & 1) ? 0x7632u : 0x5410u;
+    const int w = i >> 1;
+    const uint32_t a0 = prmt(word(v00, w), word(v10, w), sel);
+    const uint32_t a1 = prmt(word(v01, w), word(v11, w), sel);
+    const uint32_t a2 = prmt(word(v20, w), word(v30, w), sel);
+    const uint32_t a3 = prmt(word(v21, w), word(v31, w), sel);
+    mma_bf16(s.o[i], a0, a1, a2, a3, bh0, bh1);
+    mma_bf16(s.o[i], a0, a1, a2, a3, bl0, bl1);
+  }
+}
+
+__device__ __forceinline__ void write_zero_row(const KArgs& a, int b, int g, int lane) {
+  uint16_t* o = a.out + (static_cast<int64_t>(b) * a.hq + g * a.G) * kHeadDim;
+  for (int e = lane * 8; e < a.G * kHeadDim; e += 32 * 8) *reinterpret_cast<uint4*>(o + e) = make_uint4(0, 0, 0, 0);
+}
+
+// End of a unit: single-chunk units write the output (a6 bypass); others write
+// the partial and the last-arriving warp of (b, g) runs the combine (a7).
+__device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g, int c, int n_chunks, int lane,
+                                            int r, int qd) {
+  const int G = a.G;
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    s.l0 += __shfl_xor_sync(kFull, s.l0, off);
+    s.l1 += __shfl_xor_sync(kFull, s.l1, off);
   }
   const int h0 = 2 * qd, h1 = 2 * qd + 1;
-
-  if (n_chunks == 1) {  // whole context in one unit: write the output directly
+  if (n_chunks == 1) {
     uint16_t* ob = a.out + (static_cast<int64_t>(b) * a.hq + g * G) * kHeadDim;
     float t[8];
     if (h0 < G) {
-      const float inv = 1.f / l0;
+      const float inv = 1.f / s.l0;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) t[i] = o[i][0];
+      for (int i = 0; i < 8; ++i) t[i] = s.o[i][0];
       store_row8(ob + h0 * kHeadDim + 8 * r, t, inv);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) t[i] = o[i][2];
+      for (int i = 0; i < 8; ++i) t[i] = s.o[i][2];
       store_row8(ob + h0 * kHeadDim + 64 + 8 * r, t, inv);
     }
     if (h1 < G) {
-      const float inv = 1.f / l1;
+      const float inv = 1.f / s.l1;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) t[i] = o[i][1];
+      for (int i = 0; i < 8; ++i) t[i] = s.o[i][1];
       store_row8(ob + h1 * kHeadDim + 8 * r, t, inv);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) t[i] = o[i][3];
+      for (int i = 0; i < 8; ++i) t[i] = s.o[i][3];
       store_row8(ob + h1 * kHeadDim + 64 + 8 * r, t, inv);
     }
     return;
   }
-
-  // (a6) partial: unnormalised acc + (m, l) in the exp2 domain
+  const int bg = b * a.hkv + g;
   const int64_t slot = static_cast<int64_t>(bg) * a.max_chunks + c;
   float* acc = a.ws_acc + slot * G * kHeadDim;
   if (h0 < G) {
     float4* p = reinterpret_cast<float4*>(acc + h0 * kHeadDim + 8 * r);
-    p[0] = make_float4(o[0][0], o[1][0], o[2][0], o[3][0]);
-    p[1] = make_float4(o[4][0], o[5][0], o[6][0], o[7][0]);
+    p[0] = make_float4(s.o[0][0], s.o[1][0], s.o[2][0], s.o[3][0]);
+    p[1] = make_float4(s.o[4][0], s.o[5][0], s.o[6][0], s.o[7][0]);
     float4* p2 = reinterpret_cast<float4*>(acc + h0 * kHeadDim + 64 + 8 * r);
-    p2[0] = make_float4(o[0][2], o[1][2], o[2][2], o[3][2]);
-    p2[1] = make_float4(o[4][2], o[5][2], o[6][2], o[7][2]);
-    if (r == 0) a.ws_ml[slot * G + h0] = make_float2(m0, l0);
+    p2[0] = make_float4(s.o[0][2], s.o[1][2], s.o[2][2], s.o[3][2]);
+    p2[1] = make_float4(s.o[4][2], s.o[5][2], s.o[6][2], s.o[7][2]);
+    if (r == 0) a.ws_ml[slot * G + h0] = make_float2(s.m0, s.l0);
   }
   if (h1 < G) {
     float4* p = reinterpret_cast<float4*>(acc + h1 * kHeadDim + 8 * r);
-    p[0] = make_float4(o[0][1], o[1][1], o[2][1], o[3][1]);
-    p[1] = make_float4(o[4][1], o[5][1], o[6][1], o[7][1]);
+    p[0] = make_float4(s.o[0][1], s.o[1][1], s.o[2][1], s.o[3][1]);
+    p[1] = make_float4(s.o[4][1], s.o[5][1], s.o[6][1], s.o[7][1]);
     float4* p2 = reinterpret_cast<float4*>(acc + h1 * kHeadDim + 64 + 8 * r);
-    p2[0] = make_float4(o[0][3], o[1][3], o[2][3], o[3][3]);
-    p2[1] = make_float4(o[4][3], o[5][3], o[6][3], o[7][3]);
-    if (r == 0) a.ws_ml[slot * G + h1] = make_float2(m1, l1);
+    p2[0] = make_float4(s.o[0][3], s.o[1][3], s.o[2][3], s.o[3][3]);
+    p2[1] = make_float4(s.o[4][3], s.o[5][3], s.o[6][3], s.o[7][3]);
+    if (r == 0) a.ws_ml[slot * G + h1] = make_float2(s.m1, s.l1);
   }
   __threadfence();
   __syncwarp();
@@ -399,8 +336,7 @@ __global__ void __launch_bounds__(kWarps * 32)
   prev = __shfl_sync(kFull, prev, 0);
   if (prev != n_chunks - 1) return;
   __threadfence();
-
-  // (a7) combine, in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c
+  // combine in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c
   const int64_t slot0 = static_cast<int64_t>(bg) * a.max_chunks;
   for (int h = 0; h < G; ++h) {
     float M = -INFINITY;
@@ -426,6 +362,299 @@ __global__ void __launch_bounds__(kWarps * 32)
   if (lane == 0) a.ws_cnt[bg] = 0;  // leave the workspace re-usable
 }
 
+__device__ __forceinline__ void init_ring(uint32_t bar0, int stages, int lane) {
+  if (lane == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(bar0 + 8 * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+// Issue the TMA loads of one tile into a stage (one elected lane).
+__device__ __forceinline__ void issue_tile(const CUtensorMap* tmk, const CUtensorMap* tmv, uint32_t dst, uint32_t bar,
+                                           int tok_in_page, int g, int pid, uint64_t policy) {
+  mbar_arrive_expect_tx(bar, kStageBytes);
+  tma_load_tile(dst, tmk, tok_in_page, g, pid, bar, policy);
+  tma_load_tile(dst + kTileBytes, tmv, tok_in_page, g, pid, bar, policy);
+}
+
+// ------------------------------------------------- kernel 1: one unit per warp
+
+template <int kWarps, int kStages>
+__global__ void __launch_bounds__(kWarps * 32)
+    decode_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                       const KArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2;   // MMA groupID
+  const int qd = lane & 3;   // MMA thread-in-group
+
+  const int64_t unit = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
+  const int c = static_cast<int>(unit / BH);
+  if (c >= a.max_chunks) return;
+  const int bg = static_cast<int>(unit - static_cast<int64_t>(c) * BH);
+  const int b = bg / a.hkv;
+  const int g = bg - b * a.hkv;
+
+  const int ctx = __ldg(a.seq_lens + b);
+  if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
+    if (c == 0) write_zero_row(a, b, g, lane);
+    return;
+  }
+  const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
+  const int n_chunks = (ntile_total + a.chunk_tiles - 1) / a.chunk_tiles;
+  if (c >= n_chunks) return;
+  const int t_begin = c * a.chunk_tiles;
+  const int nt = min(a.chunk_tiles, ntile_total - t_begin);
+
+  // block-table walk (a1): lane i holds the physical page of tile i of the unit
+  int my_pid = 0;
+  if (lane < nt) {
+    const int tok = (t_begin + lane) * kTileTokens;
+    my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + tok / a.page_size);
+  }
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
+  const uint32_t bar0 = smem_u32(&bars[warp][0]);
+  init_ring(bar0, kStages, lane);
+  const uint64_t policy = evict_first_policy();
+
+  // KV stream (a2): tile j of the unit -> stage j % kStages
+  auto issue = [&](int j) {
+    const int pid = __shfl_sync(kFull, my_pid, j);
+    if (lane == 0) {
+      const int s = j % kStages;
+      issue_tile(&tmk, &tmv, sbase + s * kStageBytes, bar0 + 8 * s, ((t_begin + j) * kTileTokens) % a.page_size, g,
+                 pid, policy);
+    }
+  };
+  const int npro = nt < kStages ? nt : kStages;
+  for (int j = 0; j < npro; ++j) issue(j);
+
+  uint4 qf[4];
+  load_q(a, b, g, r, qd, qf);
+  Acc acc;
+  acc_reset(acc);
+  for (int j = 0; j < nt; ++j) {
+    const int s = j % kStages;
+    mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
+    compute_tile(sbase + s * kStageBytes, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
+    __syncwarp();
+    if (j + kStages < nt) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(j + kStages);
+    }
+  }
+  finish_unit(a, acc, b, g, c, n_chunks, lane, r, qd);
+}
+
+// ------------------------------------------- kernel 2: persistent streaming warps
+//
+// Grid = #SMs x CTAs/SM.  Every CTA first builds the compact work list in shared
+// memory from seq_lens: phase A = all FULL chunks (C tokens) of every request,
+// phase B = the ragged last chunks (LPT-ish: the small units run last).  Unit u
+// -> (request b by binary search over the phase's prefix sums, kv-head g, chunk
+// c).  Each warp then streams tiles continuously across units: its first unit is
+// static (global warp id), later ones are claimed with one atomicAdd each,
+// claimed two units ahead; the issue side runs up to kStages tiles (and at most
+// one unit) ahead of the consume side, prefetching the next unit's page ids and
+// q fragment into registers, so no unit boundary drains the TMA ring.  Which warp
+// computes a unit never changes its result (partials merge in chunk order).
+
+struct Unit {
+  int b, g, c, t_begin, nt, ctx, n_chunks;
+};
+
+__device__ __forceinline__ Unit decode_unit(int u, const int* sl, const int* prefA, const int* prefB, int B,
+                                            int hkv, int UA, int chunk_tiles) {
+  Unit x;
+  const bool phaseB = u >= UA;
+  const int uu = phaseB ? u - UA : u;
+  const int k = uu / hkv;
+  x.g = uu - k * hkv;
+  const int* pref = phaseB ? prefB : prefA;
+  int lo = 0, hi = B;  // pref[lo] <= k < pref[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pref[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  x.b = lo;
+  x.ctx = sl[lo];
+  const int ntt = (x.ctx + kTileTokens - 1) / kTileTokens;
+  x.n_chunks = (ntt + chunk_tiles - 1) / chunk_tiles;
+  x.c = phaseB ? x.ctx / (chunk_tiles * kTileTokens) : k - prefA[lo];
+  x.t_begin = x.c * chunk_tiles;
+  x.nt = min(chunk_tiles, ntt - x.t_begin);
+  return x;
+}
+
+__device__ __forceinline__ int load_pids(const KArgs& a, const Unit& x, int lane) {
+  int pid = 0;
+  if (lane < x.nt) {
+    const int tok = (x.t_begin + lane) * kTileTokens;
+    pid = __ldg(a.block_table + static_cast<int64_t>(x.b) * a.max_blocks + tok / a.page_size);
+  }
+  return pid;
+}
+
+__device__ __forceinline__ void warp_scan_inplace(int* arr, int n, int lane) {
+  // arr[1..n] hold counts; afterwards arr[i] = sum of counts[1..i], arr[0] = 0
+  int carry = 0;
+  for (int base = 0; base < n; base += 32) {
+    int v = (base + lane < n) ? arr[base + lane + 1] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(kFull, v, off);
+      if (lane >= off) v += t;
+    }
+    if (base + lane < n) arr[base + lane + 1] = v + carry;
+    carry += __shfl_sync(kFull, v, 31);
+  }
+  if (lane == 0) arr[0] = 0;
+}
+
+template <int kWarps, int kStages>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    decode_attn_persistent(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                           const KArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[kWarps][kStages];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2;
+  const int qd = lane & 3;
+  const int B = a.batch;
+  const int hkv = a.hkv;
+  const int C = a.chunk_tiles * kTileTokens;
+
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  int* sl = reinterpret_cast<int*>(base + kWarps * kStages * kStageBytes);
+  int* prefA = sl + B;
+  int* prefB = prefA + B + 1;
+
+  // (a0) plan: per-request chunk counts and prefix sums, in shared memory
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const int x = __ldg(a.seq_lens + b);
+    sl[b] = x;
+    prefA[b + 1] = x > 0 ? x / C : 0;
+    prefB[b + 1] = (x > 0 && x % C) ? 1 : 0;
+    if (x <= 0 && (b % gridDim.x) == blockIdx.x) {  // reading c4: zero rows
+      uint4* o = reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(b) * a.hq * kHeadDim);
+      for (int e = 0; e < a.hq * kHeadDim / 8; ++e) o[e] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) warp_scan_inplace(prefA, B, lane);
+  if (warp == 1 % kWarps) warp_scan_inplace(prefB, B, lane);
+  __syncthreads();
+  const int UA = prefA[B] * hkv;
+  const int U = UA + prefB[B] * hkv;
+  const int NW = gridDim.x * kWarps;
+  const int gw = blockIdx.x * kWarps + warp;
+  int* claim_ctr = a.ws_cnt + a.ctl_off;
+  int* exit_ctr = claim_ctr + 1;
+
+  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
+  const uint32_t bar0 = smem_u32(&bars[warp][0]);
+  init_ring(bar0, kStages, lane);
+  const uint64_t policy = evict_first_policy();
+
+  if (gw < U) {
+    // issue side
+    int iu = gw;
+    Unit mi = decode_unit(iu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
+    int pid_i = load_pids(a, mi, lane);
+    int ij = 0;
+    int cl = 0;
+    if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
+    int nu = __shfl_sync(kFull, cl, 0);
+    int pid_n = 0;
+    if (nu < U) {
+      pid_n = load_pids(a, decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles), lane);
+      if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
+    }
+    bool issue_end = false;
+    bool ahead = false;  // issue side already on the unit after the consumer's
+    uint4 qn[4];
+    // consume side
+    Unit mc = mi;
+    uint4 qf[4];
+    load_q(a, mc.b, mc.g, r, qd, qf);
+    int cj = 0;
+    Acc acc;
+    acc_reset(acc);
+    uint32_t n_issued = 0, n_cons = 0;
+
+    for (;;) {
+      // ---- issue as far as the ring (and the one-unit look-ahead) allows
+      for (;;) {
+        if (ij < mi.nt) {
+          if (n_issued - n_cons >= static_cast<uint32_t>(kStages)) break;
+          const int pid = __shfl_sync(kFull, pid_i, ij);
+          if (lane == 0) {
+            const int s = n_issued % kStages;
+            if (n_issued >= static_cast<uint32_t>(kStages)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_tile(&tmk, &tmv, sbase + s * kStageBytes, bar0 + 8 * s,
+                       ((mi.t_begin + ij) * kTileTokens) % a.page_size, mi.g, pid, policy);
+          }
+          ++ij;
+          ++n_issued;
+          continue;
+        }
+        if (issue_end || ahead) break;
+        // advance the issue side to the next claimed unit
+        iu = nu;
+        if (iu >= U) {
+          issue_end = true;
+          break;
+        }
+        mi = decode_unit(iu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
+        pid_i = pid_n;
+        load_q(a, mi.b, mi.g, r, qd, qn);
+        ij = 0;
+        ahead = true;
+        nu = __shfl_sync(kFull, cl, 0);
+        if (nu < U) {
+          pid_n = load_pids(a, decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles), lane);
+          if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
+        }
+      }
+      // ---- consume one tile
+      const int s = n_cons % kStages;
+      mbar_wait(bar0 + 8 * s, (n_cons / kStages) & 1);
+      compute_tile(sbase + s * kStageBytes, qf, mc.ctx - (mc.t_begin + cj) * kTileTokens, a.scale_log2, r, qd, acc);
+      __syncwarp();
+      ++n_cons;
+      if (++cj == mc.nt) {
+        finish_unit(a, acc, mc.b, mc.g, mc.c, mc.n_chunks, lane, r, qd);
+        if (!ahead) break;  // the issue side has run out of units
+        mc = mi;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qf[i] = qn[i];
+        ahead = false;
+        cj = 0;
+        acc_reset(acc);
+      }
+    }
+  }
+  // last warp out resets the claim counter for the next launch
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) {
+    const int prev = atomicAdd(exit_ctr, 1);
+    if (prev == NW - 1) {
+      *claim_ctr = 0;
+      *exit_ctr = 0;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace
 
 size_t workspace_counter_cap(size_t ws_bytes) { return (ws_bytes / 64) & ~size_t(255); }
@@ -449,24 +678,24 @@ WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t
   w.ml_off = w.cnt_cap;
   w.acc_off = w.ml_off + ml;
   w.total = w.acc_off + acc;
-  w.fits = w.total <= ws_bytes && static_cast<size_t>(batch) * hkv * sizeof(int32_t) <= w.cnt_cap;
+  w.fits = w.total <= ws_bytes && (static_cast<size_t>(batch) * hkv + 2) * sizeof(int32_t) <= w.cnt_cap;
   return w;
 }
 
 size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks) {
   size_t ml, acc;
   data_bytes(batch, hq, hkv, max_chunks, &ml, &acc);
-  const size_t need_cnt = up256(static_cast<size_t>(batch) * hkv * sizeof(int32_t));
+  const size_t need_cnt = up256((static_cast<size_t>(batch) * hkv + 2) * sizeof(int32_t));
   size_t S = up256(ml + acc + need_cnt + 256);
   while (!workspace_layout(batch, hq, hkv, max_chunks, S).fits) S = up256(S + std::max<size_t>(256, S / 128));
   return S;
 }
 
 template <int W, int S>
-static neo_status launch_cfg(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t units,
-                             cudaStream_t stream) {
+static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t units,
+                              cudaStream_t stream) {
   static bool configured = false;
-  constexpr int smem = smem_bytes<W, S>();
+  constexpr int smem = W * S * kStageBytes + 1024;
   if (!configured) {
     cudaError_t e =
         cudaFuncSetAttribute(decode_attn_kernel<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -480,15 +709,50 @@ static neo_status launch_cfg(const KArgs& a, const CUtensorMap& tmk, const CUten
   return NEO_OK;
 }
 
-// Kernel shape (warps per CTA, TMA stages per warp).  NEO_ATTN_CFG="W,S" selects
-// another compiled shape for tuning experiments.
+constexpr int kMaxSmem = 227 * 1024;
+
+template <int W, int S>
+constexpr int persistent_smem(int batch) {
+  return W * S * kStageBytes + 1024 + 4 * (3 * batch + 2);
+}
+
+// Launch the persistent kernel if its shared memory fits; returns false otherwise.
+template <int W, int S>
+static bool launch_persistent(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, cudaStream_t stream,
+                              neo_status* st) {
+  const int smem = persistent_smem<W, S>(a.batch);
+  if (smem > kMaxSmem) return false;
+  static int configured_smem = 0;
+  if (configured_smem < smem) {
+    cudaError_t e =
+        cudaFuncSetAttribute(decode_attn_persistent<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+    if (e != cudaSuccess) {
+      *st = cuda_fail(e, "cudaFuncSetAttribute(decode_attn_persistent)");
+      return true;
+    }
+    configured_smem = kMaxSmem;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_attn_persistent<W, S>, W * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  decode_attn_persistent<W, S><<<sms * per_sm, W * 32, smem, stream>>>(tmk, tmv, a);
+  cudaError_t e = cudaGetLastError();
+  *st = e == cudaSuccess ? NEO_OK : cuda_fail(e, "decode_attn_persistent launch");
+  return true;
+}
+
+// Kernel variant.  NEO_ATTN_CFG selects another compiled shape for tuning:
+// "pW,S" = persistent kernel with W warps x S stages, "uW,S" = one unit per warp.
 static int attn_cfg() {
   static int cfg = [] {
     const char* v = std::getenv("NEO_ATTN_CFG");
-    if (!v) return 44;
+    if (!v) return 0;
     int w = 0, s = 0;
-    if (std::sscanf(v, "%d,%d", &w, &s) != 2) return 44;
-    return w * 10 + s;
+    char kind = 'p';
+    if (std::sscanf(v, "%c%d,%d", &kind, &w, &s) != 3) return 0;
+    return (kind == 'u' ? 1000 : 0) + w * 10 + s;
   }();
   return cfg;
 }
@@ -512,18 +776,24 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.max_blocks = L.max_blocks;
   a.chunk_tiles = L.chunk_tokens / kTileTokens;
   a.max_chunks = L.max_chunks;
+  a.ctl_off = static_cast<int32_t>(w.cnt_cap / sizeof(int32_t)) - 2;
   a.scale_log2 = L.scale * 1.4426950408889634f;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
+  neo_status st = NEO_OK;
   switch (attn_cfg()) {
-    case 43: return launch_cfg<4, 3>(a, tmk, tmv, units, L.stream);
-    case 42: return launch_cfg<4, 2>(a, tmk, tmv, units, L.stream);
-    case 46: return launch_cfg<4, 6>(a, tmk, tmv, units, L.stream);
-    case 24: return launch_cfg<2, 4>(a, tmk, tmv, units, L.stream);
-    case 26: return launch_cfg<2, 6>(a, tmk, tmv, units, L.stream);
-    case 83: return launch_cfg<8, 3>(a, tmk, tmv, units, L.stream);
-    case 82: return launch_cfg<8, 2>(a, tmk, tmv, units, L.stream);
-    default: return launch_cfg<4, 4>(a, tmk, tmv, units, L.stream);
+    case 1044: return launch_unit<4, 4>(a, tmk, tmv, units, L.stream);
+    case 1043: return launch_unit<4, 3>(a, tmk, tmv, units, L.stream);
+    case 1042: return launch_unit<4, 2>(a, tmk, tmv, units, L.stream);
+    case 1083: return launch_unit<8, 3>(a, tmk, tmv, units, L.stream);
+    case 43: if (launch_persistent<4, 3>(a, tmk, tmv, L.stream, &st)) return st; break;
+    case 42: if (launch_persistent<4, 2>(a, tmk, tmv, L.stream, &st)) return st; break;
+    case 46: if (launch_persistent<4, 6>(a, tmk, tmv, L.stream, &st)) return st; break;
+    case 64: if (launch_persistent<6, 4>(a, tmk, tmv, L.stream, &st)) return st; break;
+    case 82: if (launch_persistent<8, 2>(a, tmk, tmv, L.stream, &st)) return st; break;
+    case 122: if (launch_persistent<12, 2>(a, tmk, tmv, L.stream, &st)) return st; break;
+    default: if (launch_persistent<8, 3>(a, tmk, tmv, L.stream, &st)) return st; break;
   }
+  return launch_unit<4, 2>(a, tmk, tmv, units, L.stream);  // batch too large for the shared-memory plan
 }
 
 }  // namespace neo
