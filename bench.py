@@ -187,7 +187,16 @@ def run_neo(args):
             step()
         torch.cuda.synchronize()
 
+    # Small configs (c1: 8 MB of KV) would be served from the 126 MB L2 across
+    # steps: flush it with a 512 MB write before every step, outside the timed
+    # attention window.  Big configs cycle >= 4 GB of distinct KV per step.
+    flush = None
+    if gb.layers * gb.kv_bytes_per_call() < 1e9:
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
     for _ in range(args.warmup):
+        if flush is not None:
+            flush.zero_()
         step() if graph is None else graph.replay()
     torch.cuda.synchronize()
     if world > 1:
@@ -196,23 +205,22 @@ def run_neo(args):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     per = [[torch.cuda.Event(enable_timing=True) for _ in range(L)] for _ in range(args.steps)]
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev0.record(stream)
     for s in range(args.steps):
+        if flush is not None:
+            flush.zero_()
         starts[s].record(stream)
         if graph is None:
             step(per[s])
         else:
             graph.replay()
             per[s][-1].record(stream)
-    ev1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    t_ms = ev0.elapsed_time(ev1)
-    # per-launch durations of the attention kernel (back-to-back launches on one stream)
+    # device time of the attention launches: per step, from the step's start event
+    # to its last launch's end event (launches are back to back on one stream)
+    t_ms = sum(starts[s].elapsed_time(per[s][-1]) for s in range(args.steps))
     launch_ms = []
     for s in range(args.steps):
         if graph is None:
@@ -254,6 +262,10 @@ def run_neo(args):
     if not args.no_e2e:
         e2e = run_e2e(args, gb, L, chunk, ws, stream, world, dist)
 
+    swap = None
+    if wl.swap_requests and not args.no_swap:
+        swap = run_swap(args, gb, L, step, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(gb, target_s=10.0)
@@ -285,8 +297,9 @@ def run_neo(args):
                 "seq_len_max": int(gb.ctx.max()),
                 "layers_per_step": L, "distinct_layer_pools": gb.layers,
                 "chunk_tokens": chunk, "parallelism": par,
-                "l2": f"inputs {gb.layers * gb.kv_bytes_per_call() / 1e9:.1f} GB of KV cycled per step >> 126 MB L2; "
-                      "no flush" if gb.layers * gb.kv_bytes_per_call() > 1e9 else "L2 not flushed (small config)",
+                "l2": (f"inputs {gb.layers * gb.kv_bytes_per_call() / 1e9:.1f} GB of distinct KV cycled per step "
+                       ">> 126 MB L2; no flush") if flush is None else
+                      "L2 flushed (512 MB write) before every step, outside the timed attention window",
                 "cuda_graph": bool(graph is not None),
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -296,12 +309,82 @@ def run_neo(args):
             "gpu_launches": L * args.steps,
             "clocks": clk,
             "e2e": e2e,
+            "swap": swap,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_swap(args, gb, L, step, stream):
+    """c3's a8 row: swap the last `swap_requests` requests (LIFO victims)
+    out to pinned host through neo_kv_swap_out on a side stream (gather kernel +
+    cudaMemcpy2DAsync over PCIe), alone and concurrently with attention steps;
+    compare with a plain pinned D2H memcpy of the same bytes; swap back in."""
+    import torch
+
+    from paper_2411_01142_b200 import NEO_GPU, NEO_HOST, neo
+    wl = gb.wl
+    victims = np.arange(gb.B - wl.swap_requests, gb.B)
+    need = (gb.ctx + gb.P - 1) // gb.P
+    gpu_ids = np.concatenate([gb.table[b, :need[b]] for b in victims]).astype(np.int32)
+    n = len(gpu_ids)
+    pool = neo.KVPool(gb.layers, gb.hkv, gb.num_pages, num_host_pages=n, page_size=gb.P, gpu_buffer=gb.pool)
+    pool.alloc(NEO_GPU, gb.num_pages)                # every page of the batch is in use
+    host_ids = pool.alloc(NEO_HOST, n)
+    nbytes = pool.staging_bytes(n)
+    staging = torch.empty(min(nbytes, 1 << 30), dtype=torch.uint8, device="cuda")
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
+
+    def timed(fn, s):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        fn()
+        e1.record(s)
+        return e0, e1
+
+    pool.swap_out(gpu_ids[:8], host_ids[:8], staging, stream=side)        # warm-up
+    torch.cuda.synchronize()
+    a, b = timed(lambda: pool.swap_out(gpu_ids, host_ids, staging, stream=side), side)
+    torch.cuda.synchronize()
+    t_out = a.elapsed_time(b) / 1e3
+    # plain pinned D2H memcpy of the same number of bytes (PCIe ceiling for this path)
+    dev = gb.pool.view(-1)[: nbytes // 2]
+    hostv = pool.host.view(-1)[: nbytes // 2]
+    a, b = timed(lambda: hostv.copy_(dev, non_blocking=True), side)
+    torch.cuda.synchronize()
+    t_d2h = a.elapsed_time(b) / 1e3
+    # swap-in back to the same pages (H2D + scatter)
+    a, b = timed(lambda: pool.swap_in(host_ids, gpu_ids, staging, stream=side), side)
+    torch.cuda.synchronize()
+    t_in = a.elapsed_time(b) / 1e3
+    a, b = timed(lambda: dev.copy_(hostv, non_blocking=True), side)
+    torch.cuda.synchronize()
+    t_h2d = a.elapsed_time(b) / 1e3
+    # attention while a swap-out runs on the side stream
+    steps = max(2, min(args.steps, 5))
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sa, sb = timed(lambda: pool.swap_out(gpu_ids, host_ids, staging, stream=side), side)
+    s0.record(stream)
+    for _ in range(steps):
+        step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    t_att = s0.elapsed_time(s1) / 1e3
+    pool.swap_in(host_ids, gpu_ids, staging, stream=side)              # restore
+    torch.cuda.synchronize()
+    pool.close()
+    return {"requests": int(wl.swap_requests), "pages": int(n), "layers": int(gb.layers), "bytes": int(nbytes),
+            "swap_out_gbs": round(nbytes / t_out / 1e9, 2), "swap_in_gbs": round(nbytes / t_in / 1e9, 2),
+            "pcie_d2h_memcpy_gbs": round(nbytes / t_d2h / 1e9, 2),
+            "pcie_h2d_memcpy_gbs": round(nbytes / t_h2d / 1e9, 2),
+            "swap_out_frac_of_memcpy": round(t_d2h / t_out, 4),
+            "attention_gbs_during_swap": round(gb.kv_bytes_per_call() * L * steps / t_att / 1e9, 2),
+            "attention_steps_during_swap": steps, "staging_bytes": int(staging.numel()),
+            "swap_outlasted_attention": bool(sa.elapsed_time(s1) < sa.elapsed_time(sb))}
 
 
 def run_e2e(args, gb, L, chunk, ws, stream, world, dist):

@@ -720,18 +720,23 @@ constexpr int persistent_smem(int batch) {
 template <int W, int S>
 static bool launch_persistent(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, cudaStream_t stream,
                               neo_status* st) {
-  const int smem = persistent_smem<W, S>(a.batch);
-  if (smem > kMaxSmem) return false;
-  static int configured_smem = 0;
-  if (configured_smem < smem) {
-    cudaError_t e =
-        cudaFuncSetAttribute(decode_attn_persistent<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, decode_attn_persistent<W, S>);
+    if (e != cudaSuccess) {
+      *st = cuda_fail(e, "cudaFuncGetAttributes(decode_attn_persistent)");
+      return true;
+    }
+    max_dyn = kMaxSmem - static_cast<int>(fa.sharedSizeBytes);
+    e = cudaFuncSetAttribute(decode_attn_persistent<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
     if (e != cudaSuccess) {
       *st = cuda_fail(e, "cudaFuncSetAttribute(decode_attn_persistent)");
       return true;
     }
-    configured_smem = kMaxSmem;
   }
+  const int smem = persistent_smem<W, S>(a.batch);
+  if (smem > max_dyn) return false;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

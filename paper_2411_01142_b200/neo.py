@@ -173,7 +173,10 @@ class KVPool:
     free lists."""
 
     def __init__(self, num_layers: int, num_kv_heads: int, num_gpu_pages: int, num_host_pages: int = 0,
-                 page_size: int = 16, head_dim: int = 128, device=None, allocate: bool = True):
+                 page_size: int = 16, head_dim: int = 128, device=None, allocate: bool = True,
+                 gpu_buffer=None, host_buffer=None):
+        """gpu_buffer/host_buffer: optional caller-owned tensors (bf16, at least
+        gpu_bytes/host_bytes, host one pinned) to wrap instead of allocating."""
         self.geo = Geometry(num_layers, num_kv_heads, head_dim, page_size, num_gpu_pages, num_host_pages)
         gb, hb = ctypes.c_size_t(), ctypes.c_size_t()
         check(lib().neo_kv_pool_bytes(ctypes.byref(self.geo), ctypes.byref(gb), ctypes.byref(hb)))
@@ -184,10 +187,20 @@ class KVPool:
         gptr, hptr = (1 << 40), ((1 << 41) if num_host_pages else None)
         if allocate:
             import torch
-            self.gpu = torch.empty(self.gpu_bytes // 2, dtype=torch.bfloat16, device=device or "cuda")
+            if gpu_buffer is not None:
+                if gpu_buffer.numel() * gpu_buffer.element_size() < self.gpu_bytes or not gpu_buffer.is_cuda:
+                    raise ValueError("gpu_buffer too small or not on CUDA")
+                self.gpu = gpu_buffer.reshape(-1).view(torch.bfloat16)[: self.gpu_bytes // 2]
+            else:
+                self.gpu = torch.empty(self.gpu_bytes // 2, dtype=torch.bfloat16, device=device or "cuda")
             gptr = self.gpu.data_ptr()
             if num_host_pages:
-                self.host = torch.empty(self.host_bytes // 2, dtype=torch.bfloat16, pin_memory=True)
+                if host_buffer is not None:
+                    if host_buffer.numel() * host_buffer.element_size() < self.host_bytes or not host_buffer.is_pinned():
+                        raise ValueError("host_buffer too small or not pinned")
+                    self.host = host_buffer.reshape(-1).view(torch.bfloat16)[: self.host_bytes // 2]
+                else:
+                    self.host = torch.empty(self.host_bytes // 2, dtype=torch.bfloat16, pin_memory=True)
                 hptr = self.host.data_ptr()
         self._h = ctypes.c_void_p()
         check(lib().neo_kv_pool_create(ctypes.byref(self.geo), gptr, self.gpu_bytes, hptr, self.host_bytes,
