@@ -336,27 +336,59 @@ __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g
   prev = __shfl_sync(kFull, prev, 0);
   if (prev != n_chunks - 1) return;
   __threadfence();
-  // combine in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c
+  // combine in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c.
+  // Latency-parallel: pass 1 spreads the (chunk, head) statistics over the lanes
+  // (G divides 32, so lane L only ever sees head L % G); pass 2 walks the chunks in
+  // order with independent loads, four chunks per batch, all heads at once.
   const int64_t slot0 = static_cast<int64_t>(bg) * a.max_chunks;
-  for (int h = 0; h < G; ++h) {
-    float M = -INFINITY;
-    for (int cc = 0; cc < n_chunks; ++cc) M = fmaxf(M, __ldcg(&a.ws_ml[(slot0 + cc) * G + h].x));
-    float L = 0.f;
-    float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int cc = 0; cc < n_chunks; ++cc) {
-      const float2 ml = __ldcg(&a.ws_ml[(slot0 + cc) * G + h]);
-      const float w = ex2(ml.x - M);
-      L += ml.y * w;
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(a.ws_acc + ((slot0 + cc) * G + h) * kHeadDim) + lane);
-      s4.x += w * v.x;
-      s4.y += w * v.y;
-      s4.z += w * v.z;
-      s4.w += w * v.w;
+  const float2* ml = a.ws_ml + slot0 * G;
+  const int ne = n_chunks * G;
+  float mloc = -INFINITY;
+  for (int e = lane; e < ne; e += 32) mloc = fmaxf(mloc, __ldcg(&ml[e].x));
+  for (int off = G; off < 32; off <<= 1) mloc = fmaxf(mloc, __shfl_xor_sync(kFull, mloc, off));
+  float lloc = 0.f;
+  for (int e = lane; e < ne; e += 32) {
+    const float2 v = __ldcg(&ml[e]);
+    lloc += v.y * ex2(v.x - mloc);
+  }
+  for (int off = G; off < 32; off <<= 1) lloc += __shfl_xor_sync(kFull, lloc, off);
+  // lane h (< G) now holds M_h in mloc and L_h in lloc
+  float Mh[kMaxGroup], inv[kMaxGroup];
+  float4 s4[kMaxGroup];
+#pragma unroll
+  for (int h = 0; h < kMaxGroup; ++h) {
+    Mh[h] = __shfl_sync(kFull, mloc, h < G ? h : 0);
+    inv[h] = 1.f / __shfl_sync(kFull, lloc, h < G ? h : 0);
+    s4[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float* accb = a.ws_acc + slot0 * G * kHeadDim + 4 * lane;
+  for (int c0 = 0; c0 < n_chunks; c0 += 4) {
+#pragma unroll
+    for (int h = 0; h < kMaxGroup; ++h) {
+      if (h >= G) break;
+      float4 v[4];
+      float w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int cc = c0 + k < n_chunks ? c0 + k : n_chunks - 1;
+        v[k] = __ldcg(reinterpret_cast<const float4*>(accb + (static_cast<int64_t>(cc) * G + h) * kHeadDim));
+        w[k] = c0 + k < n_chunks ? ex2(__ldcg(&ml[cc * G + h].x) - Mh[h]) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        s4[h].x += w[k] * v[k].x;
+        s4[h].y += w[k] * v[k].y;
+        s4[h].z += w[k] * v[k].z;
+        s4[h].w += w[k] * v[k].w;
+      }
     }
-    const float inv = 1.f / L;
+  }
+#pragma unroll
+  for (int h = 0; h < kMaxGroup; ++h) {
+    if (h >= G) break;
     uint2 pk;
-    pk.x = pack_bf16(s4.x * inv, s4.y * inv);
-    pk.y = pack_bf16(s4.z * inv, s4.w * inv);
+    pk.x = pack_bf16(s4[h].x * inv[h], s4[h].y * inv[h]);
+    pk.y = pack_bf16(s4[h].z * inv[h], s4[h].w * inv[h]);
     *reinterpret_cast<uint2*>(a.out + (static_cast<int64_t>(b) * a.hq + g * G + h) * kHeadDim + 4 * lane) = pk;
   }
   if (lane == 0) a.ws_cnt[bg] = 0;  // leave the workspace re-usable
