@@ -606,13 +606,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
     int nu = __shfl_sync(kFull, cl, 0);
     int pid_n = 0;
+    uint4 qn[4], qb[4];  // q of the issue side's unit (when ahead) and of the next claimed unit
     if (nu < U) {
-      pid_n = load_pids(a, decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles), lane);
+      const Unit x = decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
+      pid_n = load_pids(a, x, lane);
+      load_q(a, x.b, x.g, r, qd, qb);
       if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
     }
     bool issue_end = false;
     bool ahead = false;  // issue side already on the unit after the consumer's
-    uint4 qn[4];
     // consume side
     Unit mc = mi;
     uint4 qf[4];
@@ -647,12 +649,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         mi = decode_unit(iu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
         pid_i = pid_n;
-        load_q(a, mi.b, mi.g, r, qd, qn);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) qn[i] = qb[i];
         ij = 0;
         ahead = true;
         nu = __shfl_sync(kFull, cl, 0);
         if (nu < U) {
-          pid_n = load_pids(a, decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles), lane);
+          const Unit x = decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
+          pid_n = load_pids(a, x, lane);
+          load_q(a, x.b, x.g, r, qd, qb);
           if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
         }
       }
@@ -822,6 +827,11 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
     case 1043: return launch_unit<4, 3>(a, tmk, tmv, units, L.stream);
     case 1042: return launch_unit<4, 2>(a, tmk, tmv, units, L.stream);
     case 1083: return launch_unit<8, 3>(a, tmk, tmv, units, L.stream);
+    case 1023: return launch_unit<2, 3>(a, tmk, tmv, units, L.stream);
+    case 1024: return launch_unit<2, 4>(a, tmk, tmv, units, L.stream);
+    case 1033: return launch_unit<3, 3>(a, tmk, tmv, units, L.stream);
+    case 1062: return launch_unit<6, 2>(a, tmk, tmv, units, L.stream);
+    case 1082: return launch_unit<8, 2>(a, tmk, tmv, units, L.stream);
     case 43: if (launch_persistent<4, 3>(a, tmk, tmv, L.stream, &st)) return st; break;
     case 42: if (launch_persistent<4, 2>(a, tmk, tmv, L.stream, &st)) return st; break;
     case 46: if (launch_persistent<4, 6>(a, tmk, tmv, L.stream, &st)) return st; break;
