@@ -45,7 +45,6 @@ struct KArgs {
   float2* ws_ml;
   int32_t* ws_cnt;
   int32_t batch, hq, hkv, G, page_size, max_blocks, chunk_tiles, max_chunks;
-  int32_t ctl_off;  // index (in ws_cnt) of the persistent kernel's claim/exit counters
   float scale_log2;
 };
 
@@ -484,214 +483,6 @@ __global__ void __launch_bounds__(kWarps * 32)
   finish_unit(a, acc, b, g, c, n_chunks, lane, r, qd);
 }
 
-// ------------------------------------------- kernel 2: persistent streaming warps
-//
-// Grid = #SMs x CTAs/SM.  Every CTA first builds the compact work list in shared
-// memory from seq_lens: phase A = all FULL chunks (C tokens) of every request,
-// phase B = the ragged last chunks (LPT-ish: the small units run last).  Unit u
-// -> (request b by binary search over the phase's prefix sums, kv-head g, chunk
-// c).  Each warp then streams tiles continuously across units: its first unit is
-// static (global warp id), later ones are claimed with one atomicAdd each,
-// claimed two units ahead; the issue side runs up to kStages tiles (and at most
-// one unit) ahead of the consume side, prefetching the next unit's page ids and
-// q fragment into registers, so no unit boundary drains the TMA ring.  Which warp
-// computes a unit never changes its result (partials merge in chunk order).
-
-struct Unit {
-  int b, g, c, t_begin, nt, ctx, n_chunks;
-};
-
-__device__ __forceinline__ Unit decode_unit(int u, const int* sl, const int* prefA, const int* prefB, int B,
-                                            int hkv, int UA, int chunk_tiles) {
-  Unit x;
-  const bool phaseB = u >= UA;
-  const int uu = phaseB ? u - UA : u;
-  const int k = uu / hkv;
-  x.g = uu - k * hkv;
-  const int* pref = phaseB ? prefB : prefA;
-  int lo = 0, hi = B;  // pref[lo] <= k < pref[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (pref[mid] <= k) lo = mid;
-    else hi = mid;
-  }
-  x.b = lo;
-  x.ctx = sl[lo];
-  const int ntt = (x.ctx + kTileTokens - 1) / kTileTokens;
-  x.n_chunks = (ntt + chunk_tiles - 1) / chunk_tiles;
-  x.c = phaseB ? x.ctx / (chunk_tiles * kTileTokens) : k - prefA[lo];
-  x.t_begin = x.c * chunk_tiles;
-  x.nt = min(chunk_tiles, ntt - x.t_begin);
-  return x;
-}
-
-__device__ __forceinline__ int load_pids(const KArgs& a, const Unit& x, int lane) {
-  int pid = 0;
-  if (lane < x.nt) {
-    const int tok = (x.t_begin + lane) * kTileTokens;
-    pid = __ldg(a.block_table + static_cast<int64_t>(x.b) * a.max_blocks + tok / a.page_size);
-  }
-  return pid;
-}
-
-__device__ __forceinline__ void warp_scan_inplace(int* arr, int n, int lane) {
-  // arr[1..n] hold counts; afterwards arr[i] = sum of counts[1..i], arr[0] = 0
-  int carry = 0;
-  for (int base = 0; base < n; base += 32) {
-    int v = (base + lane < n) ? arr[base + lane + 1] : 0;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int t = __shfl_up_sync(kFull, v, off);
-      if (lane >= off) v += t;
-    }
-    if (base + lane < n) arr[base + lane + 1] = v + carry;
-    carry += __shfl_sync(kFull, v, 31);
-  }
-  if (lane == 0) arr[0] = 0;
-}
-
-template <int kWarps, int kStages>
-__global__ void __launch_bounds__(kWarps * 32, 1)
-    decode_attn_persistent(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
-                           const KArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[kWarps][kStages];
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int r = lane >> 2;
-  const int qd = lane & 3;
-  const int B = a.batch;
-  const int hkv = a.hkv;
-  const int C = a.chunk_tiles * kTileTokens;
-
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  int* sl = reinterpret_cast<int*>(base + kWarps * kStages * kStageBytes);
-  int* prefA = sl + B;
-  int* prefB = prefA + B + 1;
-
-  // (a0) plan: per-request chunk counts and prefix sums, in shared memory
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    const int x = __ldg(a.seq_lens + b);
-    sl[b] = x;
-    prefA[b + 1] = x > 0 ? x / C : 0;
-    prefB[b + 1] = (x > 0 && x % C) ? 1 : 0;
-    if (x <= 0 && (b % gridDim.x) == blockIdx.x) {  // reading c4: zero rows
-      uint4* o = reinterpret_cast<uint4*>(a.out + static_cast<int64_t>(b) * a.hq * kHeadDim);
-      for (int e = 0; e < a.hq * kHeadDim / 8; ++e) o[e] = make_uint4(0, 0, 0, 0);
-    }
-  }
-  __syncthreads();
-  if (warp == 0) warp_scan_inplace(prefA, B, lane);
-  if (warp == 1 % kWarps) warp_scan_inplace(prefB, B, lane);
-  __syncthreads();
-  const int UA = prefA[B] * hkv;
-  const int U = UA + prefB[B] * hkv;
-  const int NW = gridDim.x * kWarps;
-  const int gw = blockIdx.x * kWarps + warp;
-  int* claim_ctr = a.ws_cnt + a.ctl_off;
-  int* exit_ctr = claim_ctr + 1;
-
-  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
-  const uint32_t bar0 = smem_u32(&bars[warp][0]);
-  init_ring(bar0, kStages, lane);
-  const uint64_t policy = evict_first_policy();
-
-  if (gw < U) {
-    // issue side
-    int iu = gw;
-    Unit mi = decode_unit(iu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
-    int pid_i = load_pids(a, mi, lane);
-    int ij = 0;
-    int cl = 0;
-    if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
-    int nu = __shfl_sync(kFull, cl, 0);
-    int pid_n = 0;
-    uint4 qn[4], qb[4];  // q of the issue side's unit (when ahead) and of the next claimed unit
-    if (nu < U) {
-      const Unit x = decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
-      pid_n = load_pids(a, x, lane);
-      load_q(a, x.b, x.g, r, qd, qb);
-      if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
-    }
-    bool issue_end = false;
-    bool ahead = false;  // issue side already on the unit after the consumer's
-    // consume side
-    Unit mc = mi;
-    uint4 qf[4];
-    load_q(a, mc.b, mc.g, r, qd, qf);
-    int cj = 0;
-    Acc acc;
-    acc_reset(acc);
-    uint32_t n_issued = 0, n_cons = 0;
-
-    for (;;) {
-      // ---- issue as far as the ring (and the one-unit look-ahead) allows
-      for (;;) {
-        if (ij < mi.nt) {
-          if (n_issued - n_cons >= static_cast<uint32_t>(kStages)) break;
-          const int pid = __shfl_sync(kFull, pid_i, ij);
-          if (lane == 0) {
-            const int s = n_issued % kStages;
-            if (n_issued >= static_cast<uint32_t>(kStages)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_tile(&tmk, &tmv, sbase + s * kStageBytes, bar0 + 8 * s,
-                       ((mi.t_begin + ij) * kTileTokens) % a.page_size, mi.g, pid, policy);
-          }
-          ++ij;
-          ++n_issued;
-          continue;
-        }
-        if (issue_end || ahead) break;
-        // advance the issue side to the next claimed unit
-        iu = nu;
-        if (iu >= U) {
-          issue_end = true;
-          break;
-        }
-        mi = decode_unit(iu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
-        pid_i = pid_n;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) qn[i] = qb[i];
-        ij = 0;
-        ahead = true;
-        nu = __shfl_sync(kFull, cl, 0);
-        if (nu < U) {
-          const Unit x = decode_unit(nu, sl, prefA, prefB, B, hkv, UA, a.chunk_tiles);
-          pid_n = load_pids(a, x, lane);
-          load_q(a, x.b, x.g, r, qd, qb);
-          if (lane == 0) cl = NW + atomicAdd(claim_ctr, 1);
-        }
-      }
-      // ---- consume one tile
-      const int s = n_cons % kStages;
-      mbar_wait(bar0 + 8 * s, (n_cons / kStages) & 1);
-      compute_tile(sbase + s * kStageBytes, qf, mc.ctx - (mc.t_begin + cj) * kTileTokens, a.scale_log2, r, qd, acc);
-      __syncwarp();
-      ++n_cons;
-      if (++cj == mc.nt) {
-        finish_unit(a, acc, mc.b, mc.g, mc.c, mc.n_chunks, lane, r, qd);
-        if (!ahead) break;  // the issue side has run out of units
-        mc = mi;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) qf[i] = qn[i];
-        ahead = false;
-        cj = 0;
-        acc_reset(acc);
-      }
-    }
-  }
-  // last warp out resets the claim counter for the next launch
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) {
-    const int prev = atomicAdd(exit_ctr, 1);
-    if (prev == NW - 1) {
-      *claim_ctr = 0;
-      *exit_ctr = 0;
-      __threadfence();
-    }
-  }
-}
-
 }  // namespace
 
 size_t workspace_counter_cap(size_t ws_bytes) { return (ws_bytes / 64) & ~size_t(255); }
@@ -715,14 +506,14 @@ WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t
   w.ml_off = w.cnt_cap;
   w.acc_off = w.ml_off + ml;
   w.total = w.acc_off + acc;
-  w.fits = w.total <= ws_bytes && (static_cast<size_t>(batch) * hkv + 2) * sizeof(int32_t) <= w.cnt_cap;
+  w.fits = w.total <= ws_bytes && static_cast<size_t>(batch) * hkv * sizeof(int32_t) <= w.cnt_cap;
   return w;
 }
 
 size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks) {
   size_t ml, acc;
   data_bytes(batch, hq, hkv, max_chunks, &ml, &acc);
-  const size_t need_cnt = up256((static_cast<size_t>(batch) * hkv + 2) * sizeof(int32_t));
+  const size_t need_cnt = up256(static_cast<size_t>(batch) * hkv * sizeof(int32_t));
   size_t S = up256(ml + acc + need_cnt + 256);
   while (!workspace_layout(batch, hq, hkv, max_chunks, S).fits) S = up256(S + std::max<size_t>(256, S / 128));
   return S;
@@ -746,55 +537,17 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
   return NEO_OK;
 }
 
-constexpr int kMaxSmem = 227 * 1024;
-
-template <int W, int S>
-constexpr int persistent_smem(int batch) {
-  return W * S * kStageBytes + 1024 + 4 * (3 * batch + 2);
-}
-
-// Launch the persistent kernel if its shared memory fits; returns false otherwise.
-template <int W, int S>
-static bool launch_persistent(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, cudaStream_t stream,
-                              neo_status* st) {
-  static int max_dyn = -1;
-  if (max_dyn < 0) {
-    cudaFuncAttributes fa{};
-    cudaError_t e = cudaFuncGetAttributes(&fa, decode_attn_persistent<W, S>);
-    if (e != cudaSuccess) {
-      *st = cuda_fail(e, "cudaFuncGetAttributes(decode_attn_persistent)");
-      return true;
-    }
-    max_dyn = kMaxSmem - static_cast<int>(fa.sharedSizeBytes);
-    e = cudaFuncSetAttribute(decode_attn_persistent<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
-    if (e != cudaSuccess) {
-      *st = cuda_fail(e, "cudaFuncSetAttribute(decode_attn_persistent)");
-      return true;
-    }
-  }
-  const int smem = persistent_smem<W, S>(a.batch);
-  if (smem > max_dyn) return false;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, decode_attn_persistent<W, S>, W * 32, smem);
-  if (per_sm < 1) per_sm = 1;
-  decode_attn_persistent<W, S><<<sms * per_sm, W * 32, smem, stream>>>(tmk, tmv, a);
-  cudaError_t e = cudaGetLastError();
-  *st = e == cudaSuccess ? NEO_OK : cuda_fail(e, "decode_attn_persistent launch");
-  return true;
-}
-
-// Kernel variant.  NEO_ATTN_CFG selects another compiled shape for tuning:
-// "pW,S" = persistent kernel with W warps x S stages, "uW,S" = one unit per warp.
+// Kernel shape: kWarps independent warps per CTA x kStages TMA stages per warp.
+// (4, 2) -> 65 KiB of stages per CTA, 3 CTAs (12 warps, 24 tiles in flight) per
+// SM; it measured best or within 1% of best on c2-c5 (profiles/r01_sweep.md).
+// NEO_ATTN_CFG="uW,S" selects another compiled shape for tuning experiments.
 static int attn_cfg() {
   static int cfg = [] {
     const char* v = std::getenv("NEO_ATTN_CFG");
-    if (!v) return 0;
+    if (!v) return 42;
     int w = 0, s = 0;
-    char kind = 'p';
-    if (std::sscanf(v, "%c%d,%d", &kind, &w, &s) != 3) return 0;
-    return (kind == 'u' ? 1000 : 0) + w * 10 + s;
+    if (std::sscanf(v, "u%d,%d", &w, &s) != 2) return 42;
+    return w * 10 + s;
   }();
   return cfg;
 }
@@ -818,29 +571,17 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.max_blocks = L.max_blocks;
   a.chunk_tiles = L.chunk_tokens / kTileTokens;
   a.max_chunks = L.max_chunks;
-  a.ctl_off = static_cast<int32_t>(w.cnt_cap / sizeof(int32_t)) - 2;
   a.scale_log2 = L.scale * 1.4426950408889634f;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
-  neo_status st = NEO_OK;
   switch (attn_cfg()) {
-    case 1044: return launch_unit<4, 4>(a, tmk, tmv, units, L.stream);
-    case 1043: return launch_unit<4, 3>(a, tmk, tmv, units, L.stream);
-    case 1042: return launch_unit<4, 2>(a, tmk, tmv, units, L.stream);
-    case 1083: return launch_unit<8, 3>(a, tmk, tmv, units, L.stream);
-    case 1023: return launch_unit<2, 3>(a, tmk, tmv, units, L.stream);
-    case 1024: return launch_unit<2, 4>(a, tmk, tmv, units, L.stream);
-    case 1033: return launch_unit<3, 3>(a, tmk, tmv, units, L.stream);
-    case 1062: return launch_unit<6, 2>(a, tmk, tmv, units, L.stream);
-    case 1082: return launch_unit<8, 2>(a, tmk, tmv, units, L.stream);
-    case 43: if (launch_persistent<4, 3>(a, tmk, tmv, L.stream, &st)) return st; break;
-    case 42: if (launch_persistent<4, 2>(a, tmk, tmv, L.stream, &st)) return st; break;
-    case 46: if (launch_persistent<4, 6>(a, tmk, tmv, L.stream, &st)) return st; break;
-    case 64: if (launch_persistent<6, 4>(a, tmk, tmv, L.stream, &st)) return st; break;
-    case 82: if (launch_persistent<8, 2>(a, tmk, tmv, L.stream, &st)) return st; break;
-    case 122: if (launch_persistent<12, 2>(a, tmk, tmv, L.stream, &st)) return st; break;
-    default: if (launch_persistent<8, 3>(a, tmk, tmv, L.stream, &st)) return st; break;
+    case 44: return launch_unit<4, 4>(a, tmk, tmv, units, L.stream);
+    case 43: return launch_unit<4, 3>(a, tmk, tmv, units, L.stream);
+    case 23: return launch_unit<2, 3>(a, tmk, tmv, units, L.stream);
+    case 33: return launch_unit<3, 3>(a, tmk, tmv, units, L.stream);
+    case 62: return launch_unit<6, 2>(a, tmk, tmv, units, L.stream);
+    case 82: return launch_unit<8, 2>(a, tmk, tmv, units, L.stream);
+    default: return launch_unit<4, 2>(a, tmk, tmv, units, L.stream);
   }
-  return launch_unit<4, 2>(a, tmk, tmv, units, L.stream);  // batch too large for the shared-memory plan
 }
 
 }  // namespace neo

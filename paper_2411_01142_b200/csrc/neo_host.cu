@@ -109,9 +109,11 @@ neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, i
 }
 
 int32_t default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
-  // Aim for ~8 waves of one-warp units over 148 SMs x 8 resident warps; the
-  // smallest power of two in [64, 512] that does not overshoot that.
-  const double target_units = 8.0 * 148 * 8;
+  // Aim for ~3 waves of one-warp units over 148 SMs x 12 resident warps (the
+  // (4 warps, 2 stages) kernel at 3 CTAs/SM): the smallest power of two in
+  // [64, 512] that does not overshoot that.  Longer chunks mean fewer pipeline
+  // ramps and partials; c2-c5 measured best at C = 384-512.
+  const double target_units = 3.0 * 148 * 12;
   const double want = static_cast<double>(batch) * hkv * std::max(max_seq_len, 1) / target_units;
   int32_t c = 64;
   while (c < want && c < kMaxChunkTokens) c *= 2;

@@ -76,7 +76,8 @@ def test_decode_attn_batch_zero_is_noop():
 
 
 def test_workspace_bytes_and_default_chunk():
-    assert neo.default_chunk(256, 8, 1126) == 256
+    assert neo.default_chunk(256, 8, 1126) == 512
+    assert neo.default_chunk(512, 1, 2252) == 256
     assert neo.default_chunk(128, 8, 8192) == 512
     assert neo.default_chunk(4, 32, 128) == 64
     # single chunk: counters only; split: counters + (m, l) + fp32 partials.  The
