@@ -423,6 +423,13 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int r = lane >> 2;   // MMA groupID
   const int qd = lane & 3;   // MMA thread-in-group
 
+  // Programmatic dependent launch: let the next kernel in the stream get its CTAs
+  // resident as soon as every CTA of this grid has started, and wait for the
+  // previous kernel (which may have produced q, the KV pages, the block table or
+  // seq_lens) to complete before touching any input.  No-ops without PDL.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
   const int64_t unit = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
   const int c = static_cast<int>(unit / BH);
@@ -431,6 +438,21 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int b = bg / a.hkv;
   const int g = bg - b * a.hkv;
 
+  if (lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+  }
+  // Issue the block-table walk (a1) and the q loads speculatively, in parallel
+  // with the seq_lens load: lane i reads the page of tile i of the chunk (index
+  // clamped into the table; entries past the context are loaded but never used).
+  const int t_begin = c * a.chunk_tiles;
+  int my_pid = 0;
+  if (lane < a.chunk_tiles) {
+    const int pg = min((t_begin + lane) * kTileTokens / a.page_size, a.max_blocks - 1);
+    my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + pg);
+  }
+  uint4 qf[4];
+  load_q(a, b, g, r, qd, qf);
   const int ctx = __ldg(a.seq_lens + b);
   if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
     if (c == 0) write_zero_row(a, b, g, lane);
@@ -439,15 +461,8 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
   const int n_chunks = (ntile_total + a.chunk_tiles - 1) / a.chunk_tiles;
   if (c >= n_chunks) return;
-  const int t_begin = c * a.chunk_tiles;
   const int nt = min(a.chunk_tiles, ntile_total - t_begin);
 
-  // block-table walk (a1): lane i holds the physical page of tile i of the unit
-  int my_pid = 0;
-  if (lane < nt) {
-    const int tok = (t_begin + lane) * kTileTokens;
-    my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + tok / a.page_size);
-  }
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
   const uint32_t bar0 = smem_u32(&bars[warp][0]);
@@ -466,8 +481,6 @@ __global__ void __launch_bounds__(kWarps * 32)
   const int npro = nt < kStages ? nt : kStages;
   for (int j = 0; j < npro; ++j) issue(j);
 
-  uint4 qf[4];
-  load_q(a, b, g, r, qd, qf);
   Acc acc;
   acc_reset(acc);
   for (int j = 0; j < nt; ++j) {
@@ -519,6 +532,15 @@ size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_ch
   return S;
 }
 
+// NEO_PDL=0 disables programmatic dependent launch (default on).
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("NEO_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
 template <int W, int S>
 static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t units,
                               cudaStream_t stream) {
@@ -531,7 +553,17 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
     configured = true;
   }
   const int64_t grid = (units + W - 1) / W;
-  decode_attn_kernel<W, S><<<static_cast<unsigned>(grid), W * 32, smem, stream>>>(tmk, tmv, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S>, tmk, tmv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
   return NEO_OK;
