@@ -186,7 +186,11 @@ NEO_API neo_status neo_decode_attn_workspace_init(void* workspace, size_t worksp
  * GPU pages: record an event on `stream` and free them after it completes.  The
  * caller orders the call after the kernels that wrote those pages.
  * Swap-in is the mirror image (host -> staging -> scatter into gpu_page_ids,
- * which may differ from the ids the request had before). */
+ * which may differ from the ids the request had before).
+ * Zero-copy variant: staging == NULL makes the kernel read/write
+ * the pinned host pages directly through their device-mapped (UVA) address --
+ * no staging buffer and no copy engine; NEO_ERR_UNSUPPORTED if the CPU-cache is
+ * not device-mapped. */
 NEO_API neo_status neo_kv_swap_out(neo_kv_pool* pool, int32_t n_pages, const int32_t* gpu_page_ids,
                                    const int32_t* host_page_ids, int32_t layer_begin, int32_t layer_end,
                                    void* staging, size_t staging_bytes, void* stream);

@@ -607,6 +607,9 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
   switch (attn_cfg()) {
     case 44: return launch_unit<4, 4>(a, tmk, tmv, units, L.stream);
+    case 28: return launch_unit<2, 8>(a, tmk, tmv, units, L.stream);
+    case 46: return launch_unit<4, 6>(a, tmk, tmv, units, L.stream);
+    case 48: return launch_unit<4, 8>(a, tmk, tmv, units, L.stream);
     case 43: return launch_unit<4, 3>(a, tmk, tmv, units, L.stream);
     case 23: return launch_unit<2, 3>(a, tmk, tmv, units, L.stream);
     case 33: return launch_unit<3, 3>(a, tmk, tmv, units, L.stream);

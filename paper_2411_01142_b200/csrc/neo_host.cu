@@ -422,10 +422,21 @@ static neo_status swap_common(neo_kv_pool* pool, bool out_dir, int32_t n, const 
   if (n < 0) return fail(NEO_ERR_INVALID_ARG, "n_pages < 0");
   if (l0 < 0 || l1 > pool->geo.num_layers || l0 >= l1) return fail(NEO_ERR_INVALID_ARG, "layer range out of bounds");
   if (n == 0) return NEO_OK;
-  if (!gpu_ids || !host_ids || !staging) return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
-  if (!neo::aligned16(staging)) return fail(NEO_ERR_INVALID_ARG, "staging must be 16-byte aligned");
+  if (!gpu_ids || !host_ids) return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
+  if (staging && !neo::aligned16(staging)) return fail(NEO_ERR_INVALID_ARG, "staging must be 16-byte aligned");
   const size_t per_page = static_cast<size_t>(l1 - l0) * 2 * pool->layer_bytes;
-  if (staging_bytes < per_page) return fail(NEO_ERR_INVALID_ARG, "staging smaller than one page's layer range");
+  if (staging && staging_bytes < per_page)
+    return fail(NEO_ERR_INVALID_ARG, "staging smaller than one page's layer range");
+  uint16_t* host_dev = nullptr;
+  if (!staging) {  // zero-copy: the CPU-cache must be device-mapped (UVA pinned memory)
+    void* dp = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&dp, pool->host_base, 0);
+    if (e != cudaSuccess || !dp) {
+      cudaGetLastError();
+      return fail(NEO_ERR_UNSUPPORTED, "zero-copy swap needs device-mapped pinned host memory");
+    }
+    host_dev = static_cast<uint16_t*>(dp);
+  }
   {
     std::lock_guard<std::mutex> lk(pool->mu);
     neo_status st = check_ids(pool->gpu_used, n, gpu_ids, "GPU page");
@@ -434,6 +445,20 @@ static neo_status swap_common(neo_kv_pool* pool, bool out_dir, int32_t n, const 
     if (st != NEO_OK) return st;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!staging) {
+    for (int32_t c0 = 0; c0 < n; c0 += neo::kMaxZeroCopyPairs) {
+      const int32_t cn = std::min<int32_t>(neo::kMaxZeroCopyPairs, n - c0);
+      neo::SwapPairs ids;
+      for (int32_t i = 0; i < cn; ++i) {
+        ids.gpu[i] = gpu_ids[c0 + i];
+        ids.host[i] = host_ids[c0 + i];
+      }
+      neo_status st = neo::launch_zero_copy(out_dir, reinterpret_cast<uint16_t*>(pool->gpu_base), host_dev, ids, cn,
+                                            pool->geo.num_gpu_pages, pool->page_elems, pool->geo.num_layers, l0, l1, s);
+      if (st != NEO_OK) return st;
+    }
+    return NEO_OK;
+  }
   const size_t host_page = static_cast<size_t>(pool->geo.num_layers) * 2 * pool->layer_bytes;
   const size_t host_off = static_cast<size_t>(l0) * 2 * pool->layer_bytes;
   const int64_t cap = std::min<int64_t>(staging_bytes / per_page, neo::kMaxSwapIdsPerLaunch);

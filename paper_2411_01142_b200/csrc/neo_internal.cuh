@@ -60,6 +60,16 @@ struct SwapBatch {
 // staging[i][l - l0][kv][...page_elems] <-> gpu[l][kv][ids[i]][...]
 neo_status launch_gather(const uint16_t* gpu_base, uint16_t* staging, const SwapBatch& ids, int32_t n,
                          int64_t num_gpu_pages, int64_t page_elems, int32_t l0, int32_t l1, cudaStream_t s);
+// Zero-copy variant: the kernel reads/writes the pinned host pages directly
+// through their device-mapped (UVA) address -- no staging buffer, no copy engine.
+constexpr int kMaxZeroCopyPairs = 480;
+struct SwapPairs {
+  int32_t gpu[kMaxZeroCopyPairs];
+  int32_t host[kMaxZeroCopyPairs];
+};
+neo_status launch_zero_copy(bool to_host, uint16_t* gpu_base, uint16_t* host_dev, const SwapPairs& ids, int32_t n,
+                            int64_t num_gpu_pages, int64_t page_elems, int32_t num_layers, int32_t l0, int32_t l1,
+                            cudaStream_t s);
 neo_status launch_scatter(uint16_t* gpu_base, const uint16_t* staging, const SwapBatch& ids, int32_t n,
                           int64_t num_gpu_pages, int64_t page_elems, int32_t l0, int32_t l1, cudaStream_t s);
 

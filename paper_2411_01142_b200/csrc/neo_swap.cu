@@ -52,7 +52,45 @@ __global__ void __launch_bounds__(256) swap_copy_kernel(const CopyArgs a, const 
   }
 }
 
+struct ZcArgs {
+  uint16_t* gpu;
+  uint16_t* host;
+  int64_t num_gpu_pages, page_elems;
+  int32_t num_layers, l0;
+};
+
+// grid (n pages, nl layers * 2): one (page, layer, K|V) block per CTA, moved
+// between GPU-cache page gpu[i] and CPU-cache page host[i] over PCIe by SM
+// loads/stores on the host page's mapped address.
+template <bool kToHost>
+__global__ void __launch_bounds__(256) zero_copy_kernel(const ZcArgs a, const SwapPairs ids) {
+  const int i = blockIdx.x;
+  const int l = a.l0 + (blockIdx.y >> 1), kv = blockIdx.y & 1;
+  uint16_t* g = a.gpu + ((static_cast<int64_t>(l) * 2 + kv) * a.num_gpu_pages + ids.gpu[i]) * a.page_elems;
+  uint16_t* h = a.host + ((static_cast<int64_t>(ids.host[i]) * a.num_layers + l) * 2 + kv) * a.page_elems;
+  const int64_t nvec = a.page_elems / 8;
+  if (kToHost) {
+    for (int64_t e = threadIdx.x; e < nvec; e += blockDim.x)
+      st_stream(reinterpret_cast<uint4*>(h) + e, ld_stream(reinterpret_cast<const uint4*>(g) + e));
+  } else {
+    for (int64_t e = threadIdx.x; e < nvec; e += blockDim.x)
+      st_stream(reinterpret_cast<uint4*>(g) + e, ld_stream(reinterpret_cast<const uint4*>(h) + e));
+  }
+}
+
 }  // namespace
+
+neo_status launch_zero_copy(bool to_host, uint16_t* gpu_base, uint16_t* host_dev, const SwapPairs& ids, int32_t n,
+                            int64_t num_gpu_pages, int64_t page_elems, int32_t num_layers, int32_t l0, int32_t l1,
+                            cudaStream_t s) {
+  if (n <= 0) return NEO_OK;
+  ZcArgs a{gpu_base, host_dev, num_gpu_pages, page_elems, num_layers, l0};
+  dim3 grid(n, (l1 - l0) * 2);
+  if (to_host) zero_copy_kernel<true><<<grid, 256, 0, s>>>(a, ids);
+  else zero_copy_kernel<false><<<grid, 256, 0, s>>>(a, ids);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? NEO_OK : cuda_fail(e, "zero-copy swap kernel launch");
+}
 
 neo_status launch_gather(const uint16_t* gpu_base, uint16_t* staging, const SwapBatch& ids, int32_t n,
                          int64_t num_gpu_pages, int64_t page_elems, int32_t l0, int32_t l1, cudaStream_t s) {

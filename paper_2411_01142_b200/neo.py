@@ -266,12 +266,14 @@ class KVPool:
 
     def swap_out(self, gpu_ids, host_ids, staging, layer_begin: int = 0, layer_end: int | None = None,
                  stream=None) -> None:
+        """neo_kv_swap_out; staging=None selects the zero-copy path."""
         g, h = _ids(gpu_ids), _ids(host_ids)
         if len(g) != len(h):
             raise ValueError("gpu_ids and host_ids differ in length")
         le = self.geo.num_layers if layer_end is None else layer_end
+        nbytes = 0 if staging is None else staging.numel() * staging.element_size()
         check(lib().neo_kv_swap_out(self._h, len(g), g.ctypes.data, h.ctypes.data, layer_begin, le,
-                                    _ptr(staging), staging.numel() * staging.element_size(), _stream(stream)))
+                                    _ptr(staging), nbytes, _stream(stream)))
 
     def swap_in(self, host_ids, gpu_ids, staging, layer_begin: int = 0, layer_end: int | None = None,
                 stream=None) -> None:
@@ -279,5 +281,6 @@ class KVPool:
         if len(g) != len(h):
             raise ValueError("gpu_ids and host_ids differ in length")
         le = self.geo.num_layers if layer_end is None else layer_end
+        nbytes = 0 if staging is None else staging.numel() * staging.element_size()
         check(lib().neo_kv_swap_in(self._h, len(g), h.ctypes.data, g.ctypes.data, layer_begin, le,
-                                   _ptr(staging), staging.numel() * staging.element_size(), _stream(stream)))
+                                   _ptr(staging), nbytes, _stream(stream)))

@@ -43,7 +43,7 @@ def host_np(pool):
 
 
 @pytest.mark.parametrize("l0,l1", [(0, 4), (1, 3), (3, 4)])
-@pytest.mark.parametrize("staging_pages", [100, 3, 1])
+@pytest.mark.parametrize("staging_pages", [100, 3, 1, 0])
 def test_swap_out_matches_gather_definition(l0, l1, staging_pages):
     import torch
     from paper_2411_01142_b200 import NEO_GPU, NEO_HOST
@@ -51,7 +51,8 @@ def test_swap_out_matches_gather_definition(l0, l1, staging_pages):
     gids = pool.alloc(NEO_GPU, 40)
     sel = gids[[5, 17, 2, 33, 8, 9, 10, 11, 39]]
     hids = pool.alloc(NEO_HOST, 12)[[0, 1, 2, 7, 8, 9, 10, 4, 5]]      # several contiguous runs
-    staging = torch.empty(pool.staging_bytes(staging_pages, l0, l1), dtype=torch.uint8, device="cuda")
+    staging = (torch.empty(pool.staging_bytes(staging_pages, l0, l1), dtype=torch.uint8, device="cuda")
+               if staging_pages else None)                    # 0: zero-copy path
     before = gpu_np(pool)
     pool.swap_out(sel, hids, staging, l0, l1)
     torch.cuda.synchronize()
@@ -65,13 +66,14 @@ def test_swap_out_matches_gather_definition(l0, l1, staging_pages):
     assert np.array_equal(gpu_np(pool), before)          # swap-out does not modify the GPU-cache
 
 
-def test_swap_in_roundtrip_to_new_ids():
+@pytest.mark.parametrize("zero_copy", [False, True])
+def test_swap_in_roundtrip_to_new_ids(zero_copy):
     import torch
     from paper_2411_01142_b200 import NEO_GPU, NEO_HOST
     pool = make_pool()
     old = pool.alloc(NEO_GPU, 10)
     hids = pool.alloc(NEO_HOST, 10)
-    staging = torch.empty(pool.staging_bytes(4), dtype=torch.uint8, device="cuda")
+    staging = None if zero_copy else torch.empty(pool.staging_bytes(4), dtype=torch.uint8, device="cuda")
     before = gpu_np(pool)
     pool.swap_out(old, hids, staging)
     ev = torch.cuda.Event()
