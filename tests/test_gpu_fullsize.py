@@ -78,3 +78,55 @@ def test_fullsize_request_shard_c5():
     parts = lpt_assign(ctx[:512], 8)                        # f = 0.5, 8 ranks
     rng = np.random.default_rng(5)
     run_and_sample(wl, [0], 6, rng, ctx=ctx, req_ids=parts[3])
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_head_shards_reassemble_bitwise(world):
+    """KV-head shards (each rank's own heads, own pool),
+    reassembled along heads, equal the unsharded output bit for bit at the same C."""
+    import torch
+
+    from neo_inputs.gpu import GpuBatch
+    from neo_inputs.workloads import WORKLOADS
+    from paper_2411_01142_b200 import neo
+    from paper_2411_01142_b200.shard import head_shard
+    wl = WORKLOADS["c4"]
+    ctx = wl.contexts()[:96]
+    C = 256
+    full = GpuBatch(wl, ctx=ctx, layers=1)
+    k, v = full.layer(0)
+    ref = neo.decode_attn(full.q[0], k, v, full.block_table, full.seq_lens, full.max_seq_len, chunk_tokens=C)
+    torch.cuda.synchronize()
+    parts = []
+    for rank in range(world):
+        kvh, qh = head_shard(wl.hq, wl.hkv, rank, world)
+        sh = GpuBatch(wl, ctx=ctx, layers=1, kv_heads=kvh, q_heads=qh)
+        k, v = sh.layer(0)
+        parts.append(neo.decode_attn(sh.q[0], k, v, sh.block_table, sh.seq_lens, sh.max_seq_len, chunk_tokens=C))
+    torch.cuda.synchronize()
+    got = torch.cat(parts, dim=1)
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+
+
+def test_request_shards_reassemble_bitwise():
+    """Request (LPT) shards in their own pools and batches equal the unsharded
+    output bit for bit: a request's result depends only on its inputs and C."""
+    import torch
+
+    from neo_inputs.gpu import GpuBatch
+    from neo_inputs.workloads import WORKLOADS
+    from paper_2411_01142_b200 import neo
+    from paper_2411_01142_b200.shard import lpt_assign
+    wl = WORKLOADS["c5"]
+    ctx = wl.contexts()[:200]
+    C = 128
+    full = GpuBatch(wl, ctx=ctx, layers=1)
+    k, v = full.layer(0)
+    ref = neo.decode_attn(full.q[0], k, v, full.block_table, full.seq_lens, full.max_seq_len, chunk_tokens=C)
+    torch.cuda.synchronize()
+    for ids in lpt_assign(ctx, 4):
+        sh = GpuBatch(wl, ctx=ctx, layers=1, req_ids=ids)
+        k, v = sh.layer(0)
+        out = neo.decode_attn(sh.q[0], k, v, sh.block_table, sh.seq_lens, sh.max_seq_len, chunk_tokens=C)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), ref[torch.from_numpy(ids).cuda()].view(torch.int16))
