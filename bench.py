@@ -271,6 +271,10 @@ def run_neo(args):
     if wl.name == "c4" and world > 1:
         reassembly = run_reassembly(args, gb, L, step, stream, world, dist)
 
+    cpu_share = None
+    if wl.name == "c5" and args.fraction < 1.0 and rank == 0:
+        cpu_share = run_cpu_share(args, wl, ctx_all, int(round(args.fraction * len(ctx_all))), t_max / (L * args.steps))
+
     swap = None
     if wl.swap_requests and not args.no_swap:
         swap = run_swap(args, gb, L, step, stream)
@@ -320,12 +324,75 @@ def run_neo(args):
             "e2e": e2e,
             "swap": swap,
             "reassembly": reassembly,
+            "cpu_share": cpu_share,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_cpu_share(args, wl, ctx_all, n_gpu, t_ga):
+    """NEXT-2 in NEO's asymmetric setting (c5, f < 1): the CPU-resident requests
+    [n_gpu, 1024) are swapped out to the pinned CPU-cache with the product's own
+    neo_kv_swap_out, then their decode attention runs on the host cores with
+    neo_cpu_decode_attn (T_ca), next to the GPU's per-layer time T_ga.
+    Also times the per-layer TrQKV / TrO transfers of those requests."""
+    import torch
+
+    from neo_inputs.gpu import GpuBatch
+    from paper_2411_01142_b200 import NEO_GPU, NEO_HOST, neo
+    ids = np.arange(n_gpu, len(ctx_all))
+    if len(ids) == 0:
+        return None
+    cb = GpuBatch(wl, ctx=ctx_all, req_ids=ids, layers=1)
+    pool = neo.KVPool(1, cb.hkv, cb.num_pages, num_host_pages=cb.num_pages, page_size=cb.P, gpu_buffer=cb.pool)
+    gids = pool.alloc(NEO_GPU, cb.num_pages)
+    hids = pool.alloc(NEO_HOST, cb.num_pages)
+    assert np.array_equal(gids, np.arange(cb.num_pages)) and np.array_equal(hids, np.arange(cb.num_pages))
+    staging = torch.empty(min(pool.staging_bytes(cb.num_pages), 1 << 30), dtype=torch.uint8, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pool.swap_out(gids, hids, staging)                     # host page id == GPU page id
+    e1.record()
+    torch.cuda.synchronize()
+    swap_ms = e0.elapsed_time(e1)
+    q_host = cb.q[0].cpu()
+    nth = ncores()
+    out = pool.cpu_decode_attn(0, q_host, cb.table, cb.ctx, num_threads=nth)   # warm-up
+    reps, t = 0, 0.0
+    while reps < 3 or (t < 5.0 and reps < 50):
+        t0 = time.time()
+        pool.cpu_decode_attn(0, q_host, cb.table, cb.ctx, out=out, num_threads=nth)
+        t += time.time() - t0
+        reps += 1
+    t_ca = t / reps
+    kvb = cb.kv_bytes_per_call()
+    # TrQKV (q, k, v of the new token of every CPU-request, device -> host) and
+    # TrO (attention output, host -> device), per layer, pinned memory
+    nq = len(ids) * wl.hq * 128 * 2
+    nkv = len(ids) * wl.hkv * 128 * 2 * 2
+    dev = torch.empty(nq + nkv, dtype=torch.uint8, device="cuda")
+    hst = torch.empty(nq + nkv, dtype=torch.uint8).pin_memory()
+    e0.record()
+    hst.copy_(dev, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    tr_qkv = e0.elapsed_time(e1)
+    e0.record()
+    dev[:nq].copy_(hst[:nq], non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    tr_o = e0.elapsed_time(e1)
+    res = {"requests": int(len(ids)), "kv_bytes": int(kvb), "threads": nth, "cpu": cpu_model(),
+           "t_ca_ms": round(t_ca * 1e3, 3), "cpu_attention_gbs": round(kvb / t_ca / 1e9, 3),
+           "t_ga_ms_gpu_share": round(t_ga * 1e3, 4), "swap_out_ms": round(swap_ms, 3),
+           "trqkv_bytes": int(nq + nkv), "trqkv_ms": round(tr_qkv, 4), "tro_bytes": int(nq), "tro_ms": round(tr_o, 4)}
+    pool.close()
+    del cb
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_reassembly(args, gb, L, step, stream, world, dist):

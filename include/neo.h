@@ -198,6 +198,26 @@ NEO_API neo_status neo_kv_swap_in(neo_kv_pool* pool, int32_t n_pages, const int3
                                   const int32_t* gpu_page_ids, int32_t layer_begin, int32_t layer_end,
                                   void* staging, size_t staging_bytes, void* stream);
 
+/* ------------------------------------------------------ CPU attention (NEXT-2)
+ * Decode attention of CPU-requests over the CPU-cache -- NEO's PACPU:
+ * the same result as neo_decode_attn (same definition, DESIGN c1-c4), computed
+ * by host threads over the pinned host pages of layer `layer`:
+ *   K_b[t] = host[host_block_table[b][t / P]][layer][0][g][t % P][:]  (V: [1]).
+ * Partition: the (request, kv-head, page) blocks are dealt to the
+ * threads in equal contiguous ranges; each thread's run of one (request,
+ * kv-head) yields a partial (m, l, acc) and the partials of a request are merged
+ * in block order.  AVX-512 within a core when the CPU has it.
+ *   q, out           HOST [batch][num_q_heads][D] bf16.
+ *   host_block_table HOST [batch][max_blocks] int32 CPU-cache page ids.
+ *   seq_lens         HOST [batch] int32.
+ *   num_threads      0 = all hardware threads.
+ * Synchronous (returns when out is written).  Results are deterministic for a
+ * fixed (inputs, num_threads); different thread counts round differently. */
+NEO_API neo_status neo_cpu_decode_attn(const neo_kv_pool* pool, int32_t layer, const void* q,
+                                       const int32_t* host_block_table, int32_t max_blocks, const int32_t* seq_lens,
+                                       void* out, int32_t batch, int32_t num_q_heads, float scale,
+                                       int32_t num_threads);
+
 /* Staging bytes that let a swap of n_pages over the layer range run in one chunk. */
 NEO_API neo_status neo_kv_swap_staging_bytes(const neo_kv_pool* pool, int32_t n_pages, int32_t layer_begin,
                                              int32_t layer_end, size_t* bytes);

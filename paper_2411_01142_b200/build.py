@@ -43,7 +43,7 @@ def _nvcc(out: str, srcs: list[str], extra: list[str], verbose: bool) -> None:
 
 
 def build(force: bool = False, verbose: bool = False) -> list[str]:
-    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
+    srcs = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")) + glob.glob(os.path.join(PKG, "csrc", "*.cpp")))
     deps = srcs + glob.glob(os.path.join(PKG, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "neo.h")]
     built = []
     if force or _stale(LIBNEO, deps):

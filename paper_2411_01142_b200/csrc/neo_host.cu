@@ -173,6 +173,11 @@ struct neo_kv_pool {
 
 using neo::fail;
 
+namespace neo {
+const neo_kv_geometry* pool_geometry(const neo_kv_pool* p) { return &p->geo; }
+const uint8_t* pool_host_base(const neo_kv_pool* p) { return p->host_base; }
+}  // namespace neo
+
 static neo_status check_geo(const neo_kv_geometry* g) {
   if (!g) return fail(NEO_ERR_INVALID_ARG, "geometry is NULL");
   if (g->num_layers < 1 || g->num_kv_heads < 1 || g->num_gpu_pages < 0 || g->num_host_pages < 0)

@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "NEO_OK", 1: "NEO_ERR_INVALID_ARG", 2: "NEO_ERR_OUT_OF_PAGES"
 EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_create", "neo_kv_pool_destroy",
             "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
             "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
-            "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes"]
+            "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn"]
 
 
 class NeoError(RuntimeError):
@@ -68,6 +68,7 @@ def lib() -> ctypes.CDLL:
                 "neo_kv_swap_out": [P, i32, P, P, i32, i32, P, sz, P],
                 "neo_kv_swap_in": [P, i32, P, P, i32, i32, P, sz, P],
                 "neo_kv_swap_staging_bytes": [P, i32, i32, i32, P],
+                "neo_cpu_decode_attn": [P, i32, P, P, i32, P, P, i32, i32, ctypes.c_float, i32],
             }
             for name, args in sig.items():
                 f = getattr(L, name)
@@ -95,6 +96,15 @@ def _stream(stream) -> int:
     if stream is None:
         stream = torch.cuda.current_stream()
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _host_u16(t) -> np.ndarray:
+    if isinstance(t, np.ndarray):
+        return np.ascontiguousarray(t, dtype=np.uint16)
+    import torch
+    if t.is_cuda:
+        raise ValueError("CPU attention takes host tensors")
+    return np.ascontiguousarray(t.contiguous().view(torch.int16).numpy().view(np.uint16))
 
 
 def _ids(ids) -> np.ndarray:
@@ -174,7 +184,7 @@ class KVPool:
 
     def __init__(self, num_layers: int, num_kv_heads: int, num_gpu_pages: int, num_host_pages: int = 0,
                  page_size: int = 16, head_dim: int = 128, device=None, allocate: bool = True,
-                 gpu_buffer=None, host_buffer=None):
+                 gpu_buffer=None, host_buffer=None, host_array=None):
         """gpu_buffer/host_buffer: optional caller-owned tensors (bf16, at least
         gpu_bytes/host_bytes, host one pinned) to wrap instead of allocating."""
         self.geo = Geometry(num_layers, num_kv_heads, head_dim, page_size, num_gpu_pages, num_host_pages)
@@ -185,6 +195,13 @@ class KVPool:
         # allocate=False: accounting-only handle (allocator tests); sentinel bases
         # that are never dereferenced because no swap/attention runs on it.
         gptr, hptr = (1 << 40), ((1 << 41) if num_host_pages else None)
+        self.host_array = None
+        if not allocate and host_array is not None:
+            # CPU-only pool (CPU attention tests): a numpy uint16 CPU-cache
+            if host_array.dtype != np.uint16 or host_array.nbytes < self.host_bytes:
+                raise ValueError("host_array must be uint16 and hold host_bytes")
+            self.host_array = host_array
+            hptr = host_array.ctypes.data
         if allocate:
             import torch
             if gpu_buffer is not None:
@@ -257,6 +274,20 @@ class KVPool:
         shape = (g.num_gpu_pages, g.num_kv_heads, g.page_size, g.head_dim)
         strides = (stride.value, g.page_size * g.head_dim, g.head_dim, 1)
         return (torch.as_strided(self.gpu, shape, strides, ko), torch.as_strided(self.gpu, shape, strides, vo))
+
+    def cpu_decode_attn(self, layer: int, q, host_block_table, seq_lens, out=None, scale=None,
+                        num_threads: int = 0):
+        """neo_cpu_decode_attn (NEXT-2): host q [B][Hq][D] bf16 bits
+        (numpy uint16 or a CPU torch bf16 tensor), host table/seq_lens -> out."""
+        qa = _host_u16(q)
+        B, hq, d = qa.shape
+        tab = np.ascontiguousarray(np.asarray(host_block_table, dtype=np.int32))
+        sl = np.ascontiguousarray(np.asarray(seq_lens, dtype=np.int32))
+        o = np.empty_like(qa) if out is None else out
+        check(lib().neo_cpu_decode_attn(self._h, layer, qa.ctypes.data, tab.ctypes.data, tab.shape[1], sl.ctypes.data,
+                                        o.ctypes.data, B, hq, float(scale if scale is not None else 1 / math.sqrt(d)),
+                                        num_threads))
+        return o
 
     def staging_bytes(self, n: int, layer_begin: int = 0, layer_end: int | None = None) -> int:
         le = self.geo.num_layers if layer_end is None else layer_end
