@@ -185,33 +185,48 @@ __device__ __forceinline__ void load_q(const KArgs& a, int b, int g, int r, int 
   }
 }
 
-// One 16-token tile (K at sk, V at sk + 4 KiB, 128B-swizzled) folded into the
-// running (O, m, l).  `valid` = tokens of the tile inside the context (>= 1).
-__device__ __forceinline__ void compute_tile(uint32_t sk, const uint4 (&qf)[4], int valid, float sl2, int r, int qd,
-                                             Acc& s) {
+// Fragments of one 16-token tile, read from the 128B-swizzled stage: K rows
+// tokA/tokB (chunks qd + 4i) and V tokens vt0, vt1, vt0+8, vt1+8 (chunks r, r+8).
+struct Frags {
+  uint4 ka[4], kb[4];
+  uint4 v00, v01, v10, v11, v20, v21, v30, v31;
+};
+
+__device__ __forceinline__ void load_frags(uint32_t sk, int r, int qd, Frags& f) {
   const uint32_t sv = sk + kTileBytes;
+  const int tokA = tok_pi(r), tokB = 8 + tokA;
+  const int vt0 = tok_pi(2 * qd), vt1 = tok_pi(2 * qd + 1);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f.ka[i] = lds128(sk + swz(tokA, qd + 4 * i));
+    f.kb[i] = lds128(sk + swz(tokB, qd + 4 * i));
+  }
+  f.v00 = lds128(sv + swz(vt0, r));
+  f.v01 = lds128(sv + swz(vt0, r + 8));
+  f.v10 = lds128(sv + swz(vt1, r));
+  f.v11 = lds128(sv + swz(vt1, r + 8));
+  f.v20 = lds128(sv + swz(vt0 + 8, r));
+  f.v21 = lds128(sv + swz(vt0 + 8, r + 8));
+  f.v30 = lds128(sv + swz(vt1 + 8, r));
+  f.v31 = lds128(sv + swz(vt1 + 8, r + 8));
+}
+
+// Fold one tile (already in registers) into the running (O, m, l).  `valid` =
+// tokens of the tile inside the context (>= 1).
+__device__ __forceinline__ void compute_tile(Frags& f, const uint4 (&qf)[4], int valid, float sl2, int r, int qd,
+                                             Acc& s) {
   const int tokA = tok_pi(r), tokB = 8 + tokA;              // S^T rows r, r+8
   const int vt0 = tok_pi(2 * qd), vt1 = tok_pi(2 * qd + 1);  // P.V k-slots 2qd, 2qd+1 (+8)
 
   // (a3) scores: S^T = K_tile . Q^T
-  uint4 ka[4], kb[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    ka[i] = lds128(sk + swz(tokA, qd + 4 * i));
-    kb[i] = lds128(sk + swz(tokB, qd + 4 * i));
-  }
   float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     const int i = jj >> 1, w = 2 * (jj & 1);
-    mma_bf16(sc, word(ka[i], w), word(kb[i], w), word(ka[i], w + 1), word(kb[i], w + 1), word(qf[i], w),
+    mma_bf16(sc, word(f.ka[i], w), word(f.kb[i], w), word(f.ka[i], w + 1), word(f.kb[i], w + 1), word(qf[i], w),
              word(qf[i], w + 1));
   }
-  // V fragments: tokens vt0, vt1, vt0+8, vt1+8; chunks r and r+8
-  uint4 v00 = lds128(sv + swz(vt0, r)), v01 = lds128(sv + swz(vt0, r + 8));
-  uint4 v10 = lds128(sv + swz(vt1, r)), v11 = lds128(sv + swz(vt1, r + 8));
-  uint4 v20 = lds128(sv + swz(vt0 + 8, r)), v21 = lds128(sv + swz(vt0 + 8, r + 8));
-  uint4 v30 = lds128(sv + swz(vt1 + 8, r)), v31 = lds128(sv + swz(vt1 + 8, r + 8));
+  uint4 v00 = f.v00, v01 = f.v01, v10 = f.v10, v11 = f.v11, v20 = f.v20, v21 = f.v21, v30 = f.v30, v31 = f.v31;
 
   float x0 = sc[0] * sl2, x1 = sc[1] * sl2, x2 = sc[2] * sl2, x3 = sc[3] * sl2;
   if (valid < kTileTokens) {  // ragged last tile: mask scores, zero V (NaN-safe)
@@ -411,8 +426,19 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* tmk, const CUtenso
 
 // ------------------------------------------------- kernel 1: one unit per warp
 
+// kStreamOnly = roofline probe (NEO_ATTN_CFG="s4,2"): identical grid, page walk
+// and TMA ring, but no math and no output -- the memory-system ceiling of this
+// exact access pattern.  Never selected by default.
+// CTAs per SM that the stage ring allows; passed to __launch_bounds__ so the
+// register budget never becomes the occupancy limit.
 template <int kWarps, int kStages>
-__global__ void __launch_bounds__(kWarps * 32)
+constexpr int ctas_per_sm() {
+  return (220 * 1024) / (kWarps * kStages * kStageBytes + 1024) < 1 ? 1
+                                                                      : (220 * 1024) / (kWarps * kStages * kStageBytes + 1024);
+}
+
+template <int kWarps, int kStages, bool kStreamOnly = false>
+__global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
     decode_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                        const KArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -486,14 +512,18 @@ __global__ void __launch_bounds__(kWarps * 32)
   for (int j = 0; j < nt; ++j) {
     const int s = j % kStages;
     mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
-    compute_tile(sbase + s * kStageBytes, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
+    // read the tile into registers, hand the stage back to TMA, then do the math:
+    // the next load is in flight while this tile is being computed
+    Frags f;
+    if (!kStreamOnly) load_frags(sbase + s * kStageBytes, r, qd, f);
     __syncwarp();
     if (j + kStages < nt) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(j + kStages);
     }
+    if (!kStreamOnly) compute_tile(f, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
   }
-  finish_unit(a, acc, b, g, c, n_chunks, lane, r, qd);
+  if (!kStreamOnly) finish_unit(a, acc, b, g, c, n_chunks, lane, r, qd);
 }
 
 }  // namespace
@@ -541,14 +571,14 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int W, int S>
+template <int W, int S, bool kStreamOnly = false>
 static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t units,
                               cudaStream_t stream) {
   static bool configured = false;
   constexpr int smem = W * S * kStageBytes + 1024;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(decode_attn_kernel<W, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(decode_attn_kernel<W, S, kStreamOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_kernel)");
     configured = true;
   }
@@ -563,7 +593,7 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S>, tmk, tmv, a);
+  cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S, kStreamOnly>, tmk, tmv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
   return NEO_OK;
@@ -572,14 +602,16 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
 // Kernel shape: kWarps independent warps per CTA x kStages TMA stages per warp.
 // (4, 2) -> 65 KiB of stages per CTA, 3 CTAs (12 warps, 24 tiles in flight) per
 // SM; it measured best or within 1% of best on c2-c5 (profiles/r01_sweep.md).
-// NEO_ATTN_CFG="uW,S" selects another compiled shape for tuning experiments.
+// NEO_ATTN_CFG="uW,S" selects another compiled shape for tuning experiments;
+// "sW,S" the stream-only roofline probe.
 static int attn_cfg() {
   static int cfg = [] {
     const char* v = std::getenv("NEO_ATTN_CFG");
     if (!v) return 42;
     int w = 0, s = 0;
-    if (std::sscanf(v, "u%d,%d", &w, &s) != 2) return 42;
-    return w * 10 + s;
+    char kind = 'u';
+    if (std::sscanf(v, "%c%d,%d", &kind, &w, &s) != 3) return 42;
+    return (kind == 's' ? 1000 : 0) + w * 10 + s;
   }();
   return cfg;
 }
@@ -606,6 +638,9 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.scale_log2 = L.scale * 1.4426950408889634f;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
   switch (attn_cfg()) {
+    case 1042: return launch_unit<4, 2, true>(a, tmk, tmv, units, L.stream);
+    case 1043: return launch_unit<4, 3, true>(a, tmk, tmv, units, L.stream);
+    case 1044: return launch_unit<4, 4, true>(a, tmk, tmv, units, L.stream);
     case 44: return launch_unit<4, 4>(a, tmk, tmv, units, L.stream);
     case 28: return launch_unit<2, 8>(a, tmk, tmv, units, L.stream);
     case 46: return launch_unit<4, 6>(a, tmk, tmv, units, L.stream);
