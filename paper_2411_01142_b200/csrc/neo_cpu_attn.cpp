@@ -215,8 +215,12 @@ NEO_BF16_TARGET inline __m512 exp2_vec(__m512 y) {
   return _mm512_scalef_ps(p, n);
 }
 
+// kG = compile-time group size (0 = runtime jb.G): fixed G lets the head loops
+// unroll so the per-head score / softmax dependency chains interleave.
+template <int kG>
 NEO_BF16_TARGET void task_avx512bf16(const Job& jb, int b, int g, int j0, int j1, Partial& out) {
-  const int G = jb.G, P = jb.P, ctx = jb.seq_lens[b];
+  const int G = kG > 0 ? kG : jb.G;
+  const int P = jb.P, ctx = jb.seq_lens[b];
   const float l2e = 1.4426950408889634f;
   const __m512 sl2 = _mm512_set1_ps(jb.scale * l2e);
   const uint16_t* qb = jb.q + (static_cast<int64_t>(b) * jb.hq + g * G) * kD;
@@ -230,6 +234,7 @@ NEO_BF16_TARGET void task_avx512bf16(const Job& jb, int b, int g, int j0, int j1
     for (int d = 0; d < kD; d += 16) _mm512_storeu_ps(&out.acc[h][d], _mm512_setzero_ps());
   }
   alignas(64) float pw[kMaxG][16];
+  float alpha[kMaxG];  // per-head rescale factor of the running state for this tile
   for (int j = j0; j < j1; ++j) {
     const int32_t pg = jb.table[static_cast<int64_t>(b) * jb.max_blocks + j];
     const uint16_t* Kp = page_kv(jb, pg, 0, g);
@@ -240,8 +245,9 @@ NEO_BF16_TARGET void task_avx512bf16(const Job& jb, int b, int g, int j0, int j1
       const uint16_t* K = Kp + t0 * kD;
       const uint16_t* V = Vp + t0 * kD;
       const __mmask16 valid = static_cast<__mmask16>((1u << nt) - 1u);
-      // (a3) scores for all heads of the group; rows past the context are
-      // loaded as zeros (masked loads), so no garbage/NaN enters the tile
+      // (a3) scores of all heads; rows past the context load as zeros
+      __m512 sc[kMaxG];
+#pragma GCC unroll 8
       for (int h = 0; h < G; ++h) {
         __m512 acc[16];
 #pragma GCC unroll 16
@@ -253,30 +259,28 @@ NEO_BF16_TARGET void task_avx512bf16(const Job& jb, int b, int g, int j0, int j1
             a = _mm512_dpbf16_ps(a, (__m512bh)_mm512_maskz_loadu_epi16(mt, K + t * kD + 32 * c), (__m512bh)qv[h][c]);
           acc[t] = a;
         }
-        __m512 sc = _mm512_mul_ps(hsum16x16(acc), sl2);                    // log2 domain
-        sc = _mm512_mask_mov_ps(_mm512_set1_ps(-INFINITY), valid, sc);
-        const float mx = _mm512_reduce_max_ps(sc);
-        const float mn = std::max(m2[h], mx);
-        if (mn > m2[h]) {  // rescale the running state
-          const float al = std::exp2(m2[h] - mn);
-          const __m512 va = _mm512_set1_ps(al);
-          for (int d = 0; d < kD; d += 16)
-            _mm512_storeu_ps(&out.acc[h][d], _mm512_mul_ps(_mm512_loadu_ps(&out.acc[h][d]), va));
-          l[h] *= al;
-          m2[h] = mn;
-        }
-        const __m512 p = _mm512_maskz_mov_ps(valid, exp2_vec(_mm512_sub_ps(sc, _mm512_set1_ps(mn))));
-        l[h] += _mm512_reduce_add_ps(p);
+        sc[h] = _mm512_mask_mov_ps(_mm512_set1_ps(-INFINITY), valid, _mm512_mul_ps(hsum16x16(acc), sl2));
+      }
+      // (a4) online softmax, branch-free rescale of the running state
+#pragma GCC unroll 8
+      for (int h = 0; h < G; ++h) {
+        const float mn = std::max(m2[h], _mm512_reduce_max_ps(sc[h]));
+        alpha[h] = _mm512_cvtss_f32(exp2_vec(_mm512_set1_ps(m2[h] - mn)));   // 0 when m2 = -inf
+        const __m512 p = _mm512_maskz_mov_ps(valid, exp2_vec(_mm512_sub_ps(sc[h], _mm512_set1_ps(mn))));
+        l[h] = l[h] * alpha[h] + _mm512_reduce_add_ps(p);
+        m2[h] = mn;
         _mm512_store_ps(pw[h], p);
       }
       // (a5) P.V: two heads at a time with their accumulators in registers
+#pragma GCC unroll 4
       for (int h = 0; h < G; h += 2) {
         const bool two = h + 1 < G;
+        const __m512 al0 = _mm512_set1_ps(alpha[h]), al1 = _mm512_set1_ps(two ? alpha[h + 1] : 0.f);
         __m512 a0[8], a1[8];
 #pragma GCC unroll 8
         for (int c = 0; c < 8; ++c) {
-          a0[c] = _mm512_loadu_ps(&out.acc[h][16 * c]);
-          a1[c] = two ? _mm512_loadu_ps(&out.acc[h + 1][16 * c]) : _mm512_setzero_ps();
+          a0[c] = _mm512_mul_ps(_mm512_loadu_ps(&out.acc[h][16 * c]), al0);
+          a1[c] = two ? _mm512_mul_ps(_mm512_loadu_ps(&out.acc[h + 1][16 * c]), al1) : _mm512_setzero_ps();
         }
         for (int t = 0; t < nt; ++t) {
           const __m512 p0 = _mm512_set1_ps(pw[h][t]);
@@ -300,6 +304,16 @@ NEO_BF16_TARGET void task_avx512bf16(const Job& jb, int b, int g, int j0, int j1
   for (int h = 0; h < G; ++h) {
     out.m[h] = m2[h] / l2e;
     out.l[h] = l[h];
+  }
+}
+
+NEO_BF16_TARGET void task_avx512bf16_dispatch(const Job& jb, int b, int g, int j0, int j1, Partial& out) {
+  switch (jb.G) {
+    case 1: return task_avx512bf16<1>(jb, b, g, j0, j1, out);
+    case 2: return task_avx512bf16<2>(jb, b, g, j0, j1, out);
+    case 4: return task_avx512bf16<4>(jb, b, g, j0, j1, out);
+    case 8: return task_avx512bf16<8>(jb, b, g, j0, j1, out);
+    default: return task_avx512bf16<0>(jb, b, g, j0, j1, out);
   }
 }
 
@@ -382,7 +396,7 @@ extern "C" NEO_API neo_status neo_cpu_decode_attn(const neo_kv_pool* pool, int32
     parts[t].resize(segs[t].size());
     for (size_t i = 0; i < segs[t].size(); ++i) {
       const Segment& sg = segs[t][i];
-      if (path == 2) task_avx512bf16(jb, sg.b, sg.g, sg.j0, sg.j1, parts[t][i]);
+      if (path == 2) task_avx512bf16_dispatch(jb, sg.b, sg.g, sg.j0, sg.j1, parts[t][i]);
       else if (path == 1) task_avx512(jb, sg.b, sg.g, sg.j0, sg.j1, parts[t][i]);
       else task_generic(jb, sg.b, sg.g, sg.j0, sg.j1, parts[t][i]);
     }

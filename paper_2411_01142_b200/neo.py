@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libneo.so")
+LIB_PATH = os.environ.get("NEO_LIB") or os.path.join(_HERE, "libneo.so")   # NEO_LIB: A/B builds
 
 NEO_OK, NEO_ERR_INVALID_ARG, NEO_ERR_OUT_OF_PAGES, NEO_ERR_UNSUPPORTED, NEO_ERR_CUDA, NEO_ERR_INTERNAL = range(6)
 NEO_GPU, NEO_HOST = 0, 1
