@@ -148,12 +148,9 @@ NEO_API neo_status neo_kv_layer_view(const neo_kv_pool* pool, int32_t layer, voi
  *               the library default neo_decode_attn_default_chunk().  The result for
  *               request b depends only on (its inputs, C): outputs are bitwise
  *               deterministic run to run (fixed merge order, no float atomics).
- *   workspace   device scratch of >= neo_decode_attn_workspace_bytes(...) bytes for
- *               the split-K partials (needs no initialisation).  One workspace per
- *               concurrently running stream.
- * Work: one attention kernel, plus -- when some request spans more than one
- * chunk -- a combine kernel launched behind it on the same stream (both with
- * programmatic dependent launch; each waits for its predecessor before reading).
+ *   workspace   device scratch of >= neo_decode_attn_workspace_bytes(...) bytes,
+ *               initialised ONCE with neo_decode_attn_workspace_init(); the kernel
+ *               leaves it re-usable.  One workspace per concurrently running stream.
  * Errors: NEO_ERR_INVALID_ARG (nulls, misalignment, Hq % Hkv != 0, max_seq_len >
  * max_blocks*P, workspace too small); NEO_ERR_UNSUPPORTED (D != 128, P % 16 != 0,
  * G > 8, C invalid); NEO_ERR_CUDA.  batch == 0 is a no-op. */
@@ -172,8 +169,8 @@ NEO_API neo_status neo_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_
                                                    int32_t head_dim, int32_t max_seq_len, int32_t chunk_tokens,
                                                    size_t* bytes);
 
-/* Zero a workspace (enqueued on `stream`).  Optional: the attention path keeps
- * no state in it between calls. */
+/* Zero the workspace's completion counters (enqueued on `stream`).  Call once
+ * after allocating a workspace. */
 NEO_API neo_status neo_decode_attn_workspace_init(void* workspace, size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------------------------ swap

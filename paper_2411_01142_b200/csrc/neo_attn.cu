@@ -43,6 +43,7 @@ struct KArgs {
   const int32_t* seq_lens;
   float* ws_acc;
   float2* ws_ml;
+  int32_t* ws_cnt;
   int32_t batch, hq, hkv, G, page_size, max_blocks, chunk_tiles, max_chunks;
   float scale_log2;
 };
@@ -287,9 +288,8 @@ __device__ __forceinline__ void write_zero_row(const KArgs& a, int b, int g, int
   for (int e = lane * 8; e < a.G * kHeadDim; e += 32 * 8) *reinterpret_cast<uint4*>(o + e) = make_uint4(0, 0, 0, 0);
 }
 
-// End of a unit: single-chunk units write the output (a6 bypass); others only
-// store their fp32 partial -- the combine (a7) is a separate dependent launch,
-// so no fence or atomic sits on this kernel's critical path.
+// End of a unit: single-chunk units write the output (a6 bypass); others write
+// the partial and the last-arriving warp of (b, g) runs the combine (a7).
 __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g, int c, int n_chunks, int lane,
                                             int r, int qd) {
   const int G = a.G;
@@ -343,28 +343,17 @@ __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g
     p2[1] = make_float4(s.o[4][3], s.o[5][3], s.o[6][3], s.o[7][3]);
     if (r == 0) a.ws_ml[slot * G + h1] = make_float2(s.m1, s.l1);
   }
-}
-
-
-
-// (a7) combine: one warp per (b, g) with more than one chunk merges the partials
-// in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c.
-// Launched right after decode_attn_kernel with programmatic dependent launch:
-// griddepcontrol.wait returns once the attention grid has completed and its
-// partial stores are visible.  Latency-parallel: pass 1 spreads the (chunk, head)
-// statistics over the lanes (G divides 32, so lane L only ever sees head L % G);
-// pass 2 walks the chunks in order with independent loads, four per batch.
-__global__ void __launch_bounds__(128) combine_kernel(const KArgs a) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int lane = threadIdx.x & 31;
-  const int bg = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (bg >= a.batch * a.hkv) return;
-  const int b = bg / a.hkv, g = bg - b * a.hkv;
-  const int G = a.G;
-  const int ctx = __ldg(a.seq_lens + b);
-  const int n_chunks = ctx > 0 ? ((ctx + kTileTokens - 1) / kTileTokens + a.chunk_tiles - 1) / a.chunk_tiles : 0;
-  if (n_chunks <= 1) return;
+  __threadfence();
+  __syncwarp();
+  int prev = 0;
+  if (lane == 0) prev = atomicAdd(a.ws_cnt + bg, 1);
+  prev = __shfl_sync(kFull, prev, 0);
+  if (prev != n_chunks - 1) return;
+  __threadfence();
+  // combine in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c.
+  // Latency-parallel: pass 1 spreads the (chunk, head) statistics over the lanes
+  // (G divides 32, so lane L only ever sees head L % G); pass 2 walks the chunks in
+  // order with independent loads, four chunks per batch, all heads at once.
   const int64_t slot0 = static_cast<int64_t>(bg) * a.max_chunks;
   const float2* ml = a.ws_ml + slot0 * G;
   const int ne = n_chunks * G;
@@ -416,6 +405,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const KArgs a) {
     pk.y = pack_bf16(s4[h].z * inv[h], s4[h].w * inv[h]);
     *reinterpret_cast<uint2*>(a.out + (static_cast<int64_t>(b) * a.hq + g * G + h) * kHeadDim + 4 * lane) = pk;
   }
+  if (lane == 0) a.ws_cnt[bg] = 0;  // leave the workspace re-usable
 }
 
 __device__ __forceinline__ void init_ring(uint32_t bar0, int stages, int lane) {
@@ -538,23 +528,38 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
 
 }  // namespace
 
+size_t workspace_counter_cap(size_t ws_bytes) { return (ws_bytes / 64) & ~size_t(255); }
+
 static size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
 
-WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t ws_bytes) {
+static void data_bytes(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t* ml, size_t* acc) {
   const int64_t G = hkv > 0 ? hq / hkv : 0;
   const int64_t units = static_cast<int64_t>(batch) * hkv * max_chunks;
   const bool split = max_chunks > 1;
+  *ml = split ? up256(static_cast<size_t>(units * G) * sizeof(float2)) : 0;
+  *acc = split ? up256(static_cast<size_t>(units * G * kHeadDim) * sizeof(float)) : 0;
+}
+
+WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t ws_bytes) {
+  size_t ml, acc;
+  data_bytes(batch, hq, hkv, max_chunks, &ml, &acc);
   WorkspaceLayout w;
-  w.ml_off = 0;
-  w.acc_off = split ? up256(static_cast<size_t>(units * G) * sizeof(float2)) : 0;
-  w.total = w.acc_off + (split ? up256(static_cast<size_t>(units * G * kHeadDim) * sizeof(float)) : 0);
-  if (w.total == 0) w.total = 256;
-  w.fits = w.total <= ws_bytes;
+  w.cnt_off = 0;
+  w.cnt_cap = workspace_counter_cap(ws_bytes);
+  w.ml_off = w.cnt_cap;
+  w.acc_off = w.ml_off + ml;
+  w.total = w.acc_off + acc;
+  w.fits = w.total <= ws_bytes && static_cast<size_t>(batch) * hkv * sizeof(int32_t) <= w.cnt_cap;
   return w;
 }
 
 size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks) {
-  return workspace_layout(batch, hq, hkv, max_chunks, 0).total;
+  size_t ml, acc;
+  data_bytes(batch, hq, hkv, max_chunks, &ml, &acc);
+  const size_t need_cnt = up256(static_cast<size_t>(batch) * hkv * sizeof(int32_t));
+  size_t S = up256(ml + acc + need_cnt + 256);
+  while (!workspace_layout(batch, hq, hkv, max_chunks, S).fits) S = up256(S + std::max<size_t>(256, S / 128));
+  return S;
 }
 
 // NEO_PDL=0 disables programmatic dependent launch (default on).
@@ -591,18 +596,6 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
   cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S, kStreamOnly>, tmk, tmv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
-  if (a.max_chunks > 1 && !kStreamOnly) {
-    cudaLaunchConfig_t cc{};
-    cc.gridDim = dim3(static_cast<unsigned>((static_cast<int64_t>(a.batch) * a.hkv + 3) / 4));
-    cc.blockDim = dim3(128);
-    cc.dynamicSmemBytes = 0;
-    cc.stream = stream;
-    cc.attrs = attr;
-    cc.numAttrs = 1;
-    cudaLaunchKernelEx(&cc, combine_kernel, a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "combine_kernel launch");
-  }
   return NEO_OK;
 }
 
@@ -631,6 +624,7 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.out = static_cast<uint16_t*>(L.out);
   a.block_table = L.block_table;
   a.seq_lens = L.seq_lens;
+  a.ws_cnt = reinterpret_cast<int32_t*>(ws + w.cnt_off);
   a.ws_ml = reinterpret_cast<float2*>(ws + w.ml_off);
   a.ws_acc = reinterpret_cast<float*>(ws + w.acc_off);
   a.batch = L.batch;

@@ -35,12 +35,15 @@ struct AttnLaunch {
   float scale;
   cudaStream_t stream;
 };
-// Byte layout of a workspace of `ws_bytes` bytes for a call shape: the split-K
-// partials (m, l) [B*Hkv*max_chunks*G] float2 | acc [B*Hkv*max_chunks*G*D] fp32.
+// Byte layout of a workspace of `ws_bytes` bytes for a call shape.  The
+// completion counters occupy [0, counter_cap(ws_bytes)) -- a region fixed by the
+// workspace size alone, so calls of different shapes sharing one workspace
+// never alias one call's counters with another call's partials.
 struct WorkspaceLayout {
-  size_t ml_off, acc_off, total;
+  size_t cnt_off, cnt_cap, ml_off, acc_off, total;
   bool fits;
 };
+size_t workspace_counter_cap(size_t ws_bytes);
 size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks);
 WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t ws_bytes);
 neo_status launch_decode_attn(const AttnLaunch& a, const CUtensorMap& tmk, const CUtensorMap& tmv);

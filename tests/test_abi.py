@@ -80,12 +80,15 @@ def test_workspace_bytes_and_default_chunk():
     assert neo.default_chunk(512, 1, 2252) == 256
     assert neo.default_chunk(128, 8, 8192) == 512
     assert neo.default_chunk(4, 32, 128) == 64
-    # single chunk: nothing to store (minimum 256 B); split: (m, l) + fp32 partials
-    assert neo.workspace_bytes(4, 32, 32, 64, chunk_tokens=64) == 256
+    # single chunk: counters only; split: counters + (m, l) + fp32 partials.  The
+    # counter region is size/64 (fixed by the workspace size) and must hold B*Hkv ints.
+    small = neo.workspace_bytes(4, 32, 32, 64, chunk_tokens=64)
+    assert small // 64 >= 4 * 32 * 4
     big = neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=256)
     units = 256 * 8 * 5
-    up = lambda x: (x + 255) // 256 * 256
-    assert big == up(units * 4 * 8) + up(units * 4 * 128 * 4)
+    data = units * 4 * 8 + units * 4 * 128 * 4
+    assert big >= data + 256 * 8 * 4 and (big // 64) & ~255 >= 256 * 8 * 4
+    assert big <= 1.05 * data + 65536
 
 
 def test_pool_bytes_and_layer_view():
