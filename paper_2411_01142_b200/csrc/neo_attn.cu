@@ -600,17 +600,18 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
 }
 
 // Kernel shape: kWarps independent warps per CTA x kStages TMA stages per warp.
-// (4, 2) -> 65 KiB of stages per CTA, 3 CTAs (12 warps, 24 tiles in flight) per
-// SM; it measured best or within 1% of best on c2-c5 (profiles/r01_sweep.md).
-// NEO_ATTN_CFG="uW,S" selects another compiled shape for tuning experiments;
-// "sW,S" the stream-only roofline probe.
+// Default, from same-box sweeps (profiles/r01_sweep.md): (4, 3) -- 97 KiB of
+// stages, 2 CTAs/SM -- when every request spans <= 3 chunks (c2: +2 % over
+// (4, 2)); (4, 2) -- 65 KiB, 3 CTAs/SM -- for longer contexts (c5: +3 % over
+// (4, 3); c3 ties).  NEO_ATTN_CFG="uW,S" forces a compiled shape for tuning
+// experiments; "sW,S" selects the stream-only roofline probe.
 static int attn_cfg() {
   static int cfg = [] {
     const char* v = std::getenv("NEO_ATTN_CFG");
-    if (!v) return 42;
+    if (!v) return 0;
     int w = 0, s = 0;
     char kind = 'u';
-    if (std::sscanf(v, "%c%d,%d", &kind, &w, &s) != 3) return 42;
+    if (std::sscanf(v, "%c%d,%d", &kind, &w, &s) != 3) return 0;
     return (kind == 's' ? 1000 : 0) + w * 10 + s;
   }();
   return cfg;
@@ -637,7 +638,9 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.max_chunks = L.max_chunks;
   a.scale_log2 = L.scale * 1.4426950408889634f;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
-  switch (attn_cfg()) {
+  int cfg = attn_cfg();
+  if (cfg == 0) cfg = L.max_chunks <= 3 ? 43 : 42;
+  switch (cfg) {
     case 1042: return launch_unit<4, 2, true>(a, tmk, tmv, units, L.stream);
     case 1043: return launch_unit<4, 3, true>(a, tmk, tmv, units, L.stream);
     case 1044: return launch_unit<4, 4, true>(a, tmk, tmv, units, L.stream);
