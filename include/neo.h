@@ -161,6 +161,20 @@ NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const voi
                                    float scale, int32_t chunk_tokens, void* workspace, size_t workspace_bytes,
                                    void* stream);
 
+/* Append this decode step's K and V rows to the paged cache (the
+ * decoding stage "read-and-appends the KV cache"), before neo_decode_attn:
+ *   for b < batch with seq_lens[b] >= 1, t = seq_lens[b] - 1 (seq_lens already
+ *   count the new token):  page block_table[b][t / P], slot t % P, kv-head g
+ *   receives k_new[b][g][:] and v_new[b][g][:]  (bit copy).
+ * k_pages/v_pages/page_stride/num_pages/block_table/max_blocks/seq_lens as for
+ * neo_decode_attn; k_new, v_new: [batch][Hkv][D] bf16 device, 16-byte aligned.
+ * Asynchronous on `stream`; the caller allocates the page (neo_kv_alloc) when t
+ * crosses a page boundary (S:265-273 extend). */
+NEO_API neo_status neo_kv_append(void* k_pages, void* v_pages, int64_t page_stride, int64_t num_pages,
+                                 const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                                 const void* k_new, const void* v_new, int32_t batch, int32_t num_kv_heads,
+                                 int32_t head_dim, int32_t page_size, void* stream);
+
 /* Default split-K chunk length for a call shape (deterministic in its inputs). */
 NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
 

@@ -78,7 +78,59 @@ __global__ void __launch_bounds__(256) zero_copy_kernel(const ZcArgs a, const Sw
   }
 }
 
+struct AppendArgs {
+  uint16_t* k;
+  uint16_t* v;
+  const uint16_t* k_new;
+  const uint16_t* v_new;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  int64_t page_stride;
+  int32_t max_blocks, hkv, page_size;
+};
+
+// grid (batch), block 256: request b's new token, all kv-heads, K and V; 16-byte copies.
+__global__ void __launch_bounds__(256) append_kernel(const AppendArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int b = blockIdx.x;
+  const int n = a.seq_lens[b];
+  if (n <= 0) return;
+  const int t = n - 1;
+  const int64_t pid = a.block_table[static_cast<int64_t>(b) * a.max_blocks + t / a.page_size];
+  const int slot = t % a.page_size;
+  const int nvec = a.hkv * (kHeadDim / 8);  // 16-byte vectors per K (or V) row set
+  for (int e = threadIdx.x; e < 2 * nvec; e += blockDim.x) {
+    const int kv = e >= nvec;
+    const int i = kv ? e - nvec : e;
+    const int g = i / (kHeadDim / 8), w = i % (kHeadDim / 8);
+    const uint4* src = reinterpret_cast<const uint4*>((kv ? a.v_new : a.k_new) +
+                                                      (static_cast<int64_t>(b) * a.hkv + g) * kHeadDim) + w;
+    uint4* dst = reinterpret_cast<uint4*>((kv ? a.v : a.k) + pid * a.page_stride +
+                                          (static_cast<int64_t>(g) * a.page_size + slot) * kHeadDim) + w;
+    *dst = *src;
+  }
+}
+
 }  // namespace
+
+neo_status launch_append(uint16_t* k, uint16_t* v, int64_t page_stride, const int32_t* block_table, int32_t max_blocks,
+                         const int32_t* seq_lens, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,
+                         int32_t hkv, int32_t page_size, cudaStream_t s) {
+  AppendArgs a{k, v, k_new, v_new, block_table, seq_lens, page_stride, max_blocks, hkv, page_size};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(batch);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, append_kernel, a);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? NEO_OK : cuda_fail(e, "append kernel launch");
+}
 
 neo_status launch_zero_copy(bool to_host, uint16_t* gpu_base, uint16_t* host_dev, const SwapPairs& ids, int32_t n,
                             int64_t num_gpu_pages, int64_t page_elems, int32_t num_layers, int32_t l0, int32_t l1,

@@ -25,7 +25,8 @@ STATUS_NAMES = {0: "NEO_OK", 1: "NEO_ERR_INVALID_ARG", 2: "NEO_ERR_OUT_OF_PAGES"
 EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_create", "neo_kv_pool_destroy",
             "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
             "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
-            "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn"]
+            "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
+            "neo_kv_append"]
 
 
 class NeoError(RuntimeError):
@@ -69,6 +70,7 @@ def lib() -> ctypes.CDLL:
                 "neo_kv_swap_in": [P, i32, P, P, i32, i32, P, sz, P],
                 "neo_kv_swap_staging_bytes": [P, i32, i32, i32, P],
                 "neo_cpu_decode_attn": [P, i32, P, P, i32, P, P, i32, i32, ctypes.c_float, i32],
+                "neo_kv_append": [P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
             }
             for name, args in sig.items():
                 f = getattr(L, name)
@@ -172,6 +174,24 @@ def decode_attn(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, *,
         seq_lens.data_ptr(), out.data_ptr(), B, hq, hkv, d, P, int(max_seq_len), float(scale), int(chunk_tokens),
         workspace.data_ptr(), workspace.numel(), _stream(stream)))
     return out
+
+
+def kv_append(k_pages, v_pages, block_table, seq_lens, k_new, v_new, stream=None, num_pages=None):
+    """neo_kv_append: write k_new/v_new [B][Hkv][D] (bf16, cuda) at
+    token seq_lens[b]-1 of each request's pages."""
+    import torch
+    for name, t in (("k_pages", k_pages), ("v_pages", v_pages), ("block_table", block_table), ("seq_lens", seq_lens),
+                    ("k_new", k_new), ("v_new", v_new)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if k_new.dtype != torch.bfloat16 or v_new.dtype != torch.bfloat16 or not k_new.is_contiguous() \
+            or not v_new.is_contiguous():
+        raise ValueError("k_new / v_new must be contiguous bf16")
+    npages, hkv, P, d = k_pages.shape
+    check(lib().neo_kv_append(k_pages.data_ptr(), v_pages.data_ptr(), k_pages.stride(0),
+                              int(num_pages if num_pages is not None else npages), block_table.data_ptr(),
+                              block_table.shape[1], seq_lens.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
+                              k_new.shape[0], hkv, d, P, _stream(stream)))
 
 
 # ------------------------------------------------------------------ KV pool

@@ -214,3 +214,30 @@ def test_debug_validate_rejects_bad_metadata(monkeypatch):
     sl[0] = case.max_seq_len + 1
     with pytest.raises(neo.NeoError):
         neo.decode_attn(case.q_dev, case.k_dev, case.v_dev, case.bt_dev, sl, case.max_seq_len)
+
+
+@pytest.mark.parametrize("P", [16, 32])
+def test_kv_append_then_attend(P):
+    """neo_kv_append (P:109-110 read-and-append): poison the new token's slot,
+    append its K/V, check the bits landed, then attend over the grown context."""
+    import torch
+    from paper_2411_01142_b200 import neo
+    ctx_new = [1, 16, 17, 33, 200, 512]                    # contexts INCLUDING the new token
+    case = Case(ctx_new, 32, 8, P=P, seed=31 + P)
+    k_new = np.stack([case.k_req[b][n - 1] for b, n in enumerate(ctx_new)])   # [B][Hkv][D]
+    v_new = np.stack([case.v_req[b][n - 1] for b, n in enumerate(ctx_new)])
+    for b, n in enumerate(ctx_new):                         # poison the slot the append will fill
+        t = n - 1
+        case.k_dev[case.table[b, t // P], :, t % P] = float("nan")
+        case.v_dev[case.table[b, t // P], :, t % P] = float("nan")
+    kn = torch.from_numpy(k_new.view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(v_new.view(np.int16)).cuda().view(torch.bfloat16)
+    neo.kv_append(case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, kn, vn)
+    torch.cuda.synchronize()
+    for b, n in enumerate(ctx_new):
+        t = n - 1
+        got = case.k_dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy()
+        assert np.array_equal(got.view(np.uint16), k_new[b])
+        got = case.v_dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy()
+        assert np.array_equal(got.view(np.uint16), v_new[b])
+    check_case(case, 64, f"append P={P}")
