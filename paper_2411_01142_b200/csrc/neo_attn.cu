@@ -343,13 +343,15 @@ __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g
     p2[1] = make_float4(s.o[4][3], s.o[5][3], s.o[6][3], s.o[7][3]);
     if (r == 0) a.ws_ml[slot * G + h1] = make_float2(s.m1, s.l1);
   }
-  __threadfence();
+  // publish: the warp barrier orders every lane's partial stores before lane 0's
+  // acq_rel atomic (release at GPU scope, cumulative); the last arriver's acquire
+  // makes all partials of (b, g) visible to the __ldcg reads below
   __syncwarp();
   int prev = 0;
-  if (lane == 0) prev = atomicAdd(a.ws_cnt + bg, 1);
+  if (lane == 0)
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ws_cnt + bg) : "memory");
   prev = __shfl_sync(kFull, prev, 0);
   if (prev != n_chunks - 1) return;
-  __threadfence();
   // combine in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c.
   // Latency-parallel: pass 1 spreads the (chunk, head) statistics over the lanes
   // (G divides 32, so lane L only ever sees head L % G); pass 2 walks the chunks in
