@@ -232,6 +232,65 @@ NEO_API neo_status neo_cpu_decode_attn(const neo_kv_pool* pool, int32_t layer, c
                                        void* out, int32_t batch, int32_t num_q_heads, float scale,
                                        int32_t num_threads);
 
+/* ------------------------------------------------- scheduler (NEXT-4)
+ * NEO's load-aware scheduler for one iteration.  Cost model
+ * (P:271-279), all times per layer in seconds, tables interpolated linearly
+ * (extrapolated linearly, clamped >= 0, 0 for an empty sub-batch):
+ *   T_l  = lin(tokens of the sub-batch: 1 per decoding request + prompt tokens)
+ *   T_ga0 = gdec(sum over batch-0's GPU decoding requests of ctx+1)
+ *           + sum over prefills of (gpre_a t^2 + gpre_b t)
+ *   T_ca = cdec(sum over the sub-batch's CPU decoding requests of ctx+1)
+ *   T    = T_prl + max(L (max{T_l0, T_ca1} + max{T_l1 + T_ga0, T_ca0}), T_swap) + T_pol
+ *   T_swap = pages moved * P * kv_bytes_per_token_layer * L / pcie_bytes_per_s
+ * Six steps: (1) empty batch-0 / batch-1; (2) every GPU decoding
+ * request into batch-0, LIFO swap-out until its new KV fits, else FIFO swap-in
+ * while free pages stay > 0; (3) FIFO prefills into batch-0 within
+ * max_batch_tokens, KV on the GPU or marked for swap-out; (4) FIFO CPU decoding
+ * requests into batch-1, else batch-0, keeping T_ca1 <= T_l0 and
+ * T_ca0 <= T_l1 + T_ga0, else skipped; (5) swap-out prefills dropped from the
+ * tail while the inequalities hold; (6) the two-batch plan is kept iff its x/T
+ * beats the GPU-only plan (batch-0 without step 4's requests).  Readings:
+ * DESIGN.md s1-s8.  Pure host function; deterministic. */
+typedef struct {
+  int32_t num_layers;                    /* L */
+  double t_pre_layer_s, t_post_layer_s;  /* T_prl, T_pol */
+  const double* lin_tokens;              /* linear stage table: tokens -> s/layer */
+  const double* lin_s;
+  int32_t lin_n;
+  const double* gdec_tokens;             /* GPU decode attention: KV tokens -> s/layer */
+  const double* gdec_s;
+  int32_t gdec_n;
+  double gpre_a, gpre_b;                 /* GPU prefill attention: a t^2 + b t s/layer */
+  const double* cdec_tokens;             /* CPU decode attention: KV tokens -> s/layer */
+  const double* cdec_s;
+  int32_t cdec_n;
+  int32_t page_size;
+  int64_t max_batch_tokens;
+  double pcie_bytes_per_s, kv_bytes_per_token_layer;
+} neo_cost_model;
+
+enum { NEO_REQ_WAITING = 0, NEO_REQ_GPU_DECODE = 1, NEO_REQ_CPU_DECODE = 2 };
+
+typedef struct {
+  int64_t id;
+  int32_t kind; /* NEO_REQ_*; the array order is the queue order */
+  int32_t ctx;  /* KV tokens held (decoding) or prompt tokens (waiting) */
+} neo_sched_request;
+
+typedef struct {
+  int32_t two_batch; /* 1 = asymmetric pipelining plan, 0 = GPU-only */
+  int32_t x;         /* requests producing a token this iteration */
+  int32_t n_batch0, n_batch1, n_swap_out, n_swap_in;
+  double t_iter, t_l0, t_l1, t_ga0, t_ca0, t_ca1;
+} neo_sched_plan;
+
+/* reqs[n]; batch0/batch1/swap_out/swap_in: caller arrays of n ids each, filled
+ * with the plan (counts in *plan).  gpu/cpu_free_pages: free pages of the two
+ * caches (neo_kv_free_count). */
+NEO_API neo_status neo_schedule(const neo_cost_model* model, const neo_sched_request* reqs, int32_t n,
+                                int64_t gpu_free_pages, int64_t cpu_free_pages, int64_t* batch0, int64_t* batch1,
+                                int64_t* swap_out, int64_t* swap_in, neo_sched_plan* plan);
+
 /* Staging bytes that let a swap of n_pages over the layer range run in one chunk. */
 NEO_API neo_status neo_kv_swap_staging_bytes(const neo_kv_pool* pool, int32_t n_pages, int32_t layer_begin,
                                              int32_t layer_end, size_t* bytes);

@@ -26,7 +26,7 @@ EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_c
             "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
             "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
             "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
-            "neo_kv_append"]
+            "neo_kv_append", "neo_schedule"]
 
 
 class NeoError(RuntimeError):
@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
                 "neo_kv_swap_staging_bytes": [P, i32, i32, i32, P],
                 "neo_cpu_decode_attn": [P, i32, P, P, i32, P, P, i32, i32, ctypes.c_float, i32],
                 "neo_kv_append": [P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
+                "neo_schedule": [P, P, i32, i64, i64, P, P, P, P, P],
             }
             for name, args in sig.items():
                 f = getattr(L, name)
@@ -192,6 +193,58 @@ def kv_append(k_pages, v_pages, block_table, seq_lens, k_new, v_new, stream=None
                               int(num_pages if num_pages is not None else npages), block_table.data_ptr(),
                               block_table.shape[1], seq_lens.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
                               k_new.shape[0], hkv, d, P, _stream(stream)))
+
+
+# ------------------------------------------------------------------ scheduler
+
+
+class CostModel(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("t_pre_layer_s", ctypes.c_double),
+                ("t_post_layer_s", ctypes.c_double), ("lin_tokens", ctypes.c_void_p), ("lin_s", ctypes.c_void_p),
+                ("lin_n", ctypes.c_int32), ("gdec_tokens", ctypes.c_void_p), ("gdec_s", ctypes.c_void_p),
+                ("gdec_n", ctypes.c_int32), ("gpre_a", ctypes.c_double), ("gpre_b", ctypes.c_double),
+                ("cdec_tokens", ctypes.c_void_p), ("cdec_s", ctypes.c_void_p), ("cdec_n", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("max_batch_tokens", ctypes.c_int64),
+                ("pcie_bytes_per_s", ctypes.c_double), ("kv_bytes_per_token_layer", ctypes.c_double)]
+
+
+class SchedPlan(ctypes.Structure):
+    _fields_ = [("two_batch", ctypes.c_int32), ("x", ctypes.c_int32), ("n_batch0", ctypes.c_int32),
+                ("n_batch1", ctypes.c_int32), ("n_swap_out", ctypes.c_int32), ("n_swap_in", ctypes.c_int32),
+                ("t_iter", ctypes.c_double), ("t_l0", ctypes.c_double), ("t_l1", ctypes.c_double),
+                ("t_ga0", ctypes.c_double), ("t_ca0", ctypes.c_double), ("t_ca1", ctypes.c_double)]
+
+
+class SchedRequest(ctypes.Structure):
+    _fields_ = [("id", ctypes.c_int64), ("kind", ctypes.c_int32), ("ctx", ctypes.c_int32)]
+
+
+def schedule(profile: dict, reqs, gpu_free_pages: int, cpu_free_pages: int) -> dict:
+    """neo_schedule.  profile: L, t_prl, t_pol, lin/gdec/cdec tables
+    [(tokens, s)], gpre_a, gpre_b, page_size, max_batch_tokens, pcie_bytes_per_s,
+    kv_bytes_per_token_layer.  reqs: [(id, kind, ctx)] in queue order (kind 0 =
+    waiting, 1 = GPU decoding, 2 = CPU decoding)."""
+    tabs = {}
+    for name in ("lin", "gdec", "cdec"):
+        t = np.ascontiguousarray(np.asarray(profile[name], dtype=np.float64).reshape(-1, 2).T)
+        tabs[name] = (np.ascontiguousarray(t[0]), np.ascontiguousarray(t[1]))
+    m = CostModel(int(profile["L"]), float(profile["t_prl"]), float(profile["t_pol"]),
+                  tabs["lin"][0].ctypes.data, tabs["lin"][1].ctypes.data, len(tabs["lin"][0]),
+                  tabs["gdec"][0].ctypes.data, tabs["gdec"][1].ctypes.data, len(tabs["gdec"][0]),
+                  float(profile["gpre_a"]), float(profile["gpre_b"]),
+                  tabs["cdec"][0].ctypes.data, tabs["cdec"][1].ctypes.data, len(tabs["cdec"][0]),
+                  int(profile["page_size"]), int(profile["max_batch_tokens"]),
+                  float(profile["pcie_bytes_per_s"]), float(profile["kv_bytes_per_token_layer"]))
+    n = len(reqs)
+    arr = (SchedRequest * max(n, 1))(*[SchedRequest(int(i), int(k), int(c)) for i, k, c in reqs])
+    outs = [np.zeros(max(n, 1), dtype=np.int64) for _ in range(4)]
+    plan = SchedPlan()
+    check(lib().neo_schedule(ctypes.byref(m), arr, n, int(gpu_free_pages), int(cpu_free_pages),
+                             *[o.ctypes.data for o in outs], ctypes.byref(plan)))
+    return {"two_batch": bool(plan.two_batch), "x": plan.x, "batch0": outs[0][:plan.n_batch0].tolist(),
+            "batch1": outs[1][:plan.n_batch1].tolist(), "swap_out": outs[2][:plan.n_swap_out].tolist(),
+            "swap_in": outs[3][:plan.n_swap_in].tolist(), "t_iter": plan.t_iter, "t_l0": plan.t_l0,
+            "t_l1": plan.t_l1, "t_ga0": plan.t_ga0, "t_ca0": plan.t_ca0, "t_ca1": plan.t_ca1}
 
 
 # ------------------------------------------------------------------ KV pool
