@@ -129,7 +129,7 @@ def main():
             "kv_bytes_per_token_layer": HKV * D * 2 * 2,
             "note": "lin: cuBLAS GEMMs of one LLaMa-3.1-8B layer; gdec: neo_decode_attn; gpre: torch SDPA causal; "
                     "cdec: neo_cpu_decode_attn; t_prl/t_pol assumed (embedding, LM head)"}
-    path = os.path.join(ROOT, "profiles", "cost_profile_b200_llama8b.json")
+    path = os.environ.get("NEO_PROFILE_OUT") or os.path.join(ROOT, "profiles", "cost_profile_b200_llama8b.json")
     json.dump(prof, open(path, "w"), indent=1)
     print(json.dumps(prof, indent=1))
 
