@@ -241,3 +241,34 @@ def test_kv_append_then_attend(P):
         got = case.v_dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy()
         assert np.array_equal(got.view(np.uint16), v_new[b])
     check_case(case, 64, f"append P={P}")
+
+
+def test_cuda_graph_capture_matches_eager():
+    """decode_attn launches (PDL attribute, fused combine counters) captured in a
+    CUDA graph and replayed give the eager results bit for bit, replay after replay."""
+    import torch
+    from paper_2411_01142_b200 import neo
+    cases = [Case([5, 300, 1100, 40], 32, 8, seed=60 + i) for i in range(3)]
+    ws = neo.make_workspace(4, 32, 8, 1100, chunk_tokens=64)
+    eager = [c.run(chunk_tokens=64, workspace=ws).clone() for c in cases]
+    outs = [torch.empty_like(e) for e in eager]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):                                  # warm-up on the capture stream
+        for c, o in zip(cases, outs):
+            neo.decode_attn(c.q_dev, c.k_dev, c.v_dev, c.bt_dev, c.sl_dev, c.max_seq_len, out=o, chunk_tokens=64,
+                            workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for c, o in zip(cases, outs):
+            neo.decode_attn(c.q_dev, c.k_dev, c.v_dev, c.bt_dev, c.sl_dev, c.max_seq_len, out=o, chunk_tokens=64,
+                            workspace=ws)
+    for rep in range(3):
+        for o in outs:
+            o.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for e, o in zip(eager, outs):
+            assert torch.equal(e.view(torch.int16), o.view(torch.int16)), rep
