@@ -137,6 +137,15 @@ def shard_plan(wl, rank, world, fraction):
     return ctx, np.arange(rank * wl.batch, (rank + 1) * wl.batch), None, None, "weak", f"dp{world} (by request)"
 
 
+def batch_total(wl, gb, world, fraction, ctx_all):
+    """Requests served per step over all ranks."""
+    if wl.name == "c4":
+        return int(gb.B)                        # head-sharded: every rank serves the whole batch
+    if wl.name == "c5":
+        return int(round(fraction * len(ctx_all)))
+    return int(gb.B * world)                    # weak scaling: one batch per rank
+
+
 def layers_per_step(wl):
     """c1 is a single-layer latency config; the others run every layer of the model."""
     return 1 if wl.name == "c1" else wl.num_layers
@@ -257,7 +266,7 @@ def run_neo(args):
     achieved = algo / avg_launch / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if world == 1 and os.path.exists(tpath):       # the committed ncu captures are 1-GPU launches
         try:
             traffic = json.load(open(tpath)).get(args.config)
         except Exception:
@@ -302,8 +311,7 @@ def run_neo(args):
             "pct_of_nominal_hbm": round(100 * value / world / NOMINAL_HBM_GBS, 2),
             "config": {
                 "workload": f"{wl.name}: {wl.model} {wl.note}",
-                "batch": int(gb.B if wl.name == "c4" else gb.B * world) if wl.name != "c5" else int(
-                    round(args.fraction * len(ctx_all))),
+                "batch": batch_total(wl, gb, world, args.fraction, ctx_all),
                 "batch_per_rank": gb.B,
                 "q_heads": wl.hq, "kv_heads": wl.hkv, "head_dim": 128, "page_size": wl.page_size,
                 "seq_len_mean": round(float(gb.ctx.mean()), 1), "seq_len_min": int(gb.ctx.min()),
