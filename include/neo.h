@@ -175,6 +175,22 @@ NEO_API neo_status neo_kv_append(void* k_pages, void* v_pages, int64_t page_stri
                                  const void* k_new, const void* v_new, int32_t batch, int32_t num_kv_heads,
                                  int32_t head_dim, int32_t page_size, void* stream);
 
+/* neo_kv_append with rotary position embedding fused in (RoFormer
+ * rotate-half convention as in LLaMa): for each request b at position
+ * t = seq_lens[b] - 1 and each dim pair (i, i + D/2), i < D/2, with
+ * theta_i = t * inv_freq[i] (angle and sin/cos in fp64, rotation in fp32):
+ *   x'[i]       = x[i] cos theta_i - x[i + D/2] sin theta_i
+ *   x'[i + D/2] = x[i + D/2] cos theta_i + x[i] sin theta_i
+ * applied to every q head (q_inout [batch][Hq][D], rotated in place) and to k_new
+ * before it is written to the page slot; v_new is written unrotated.
+ * inv_freq: device float[D/2] (the model's frequency table, any scaling already
+ * applied by the caller).  Other arguments and errors as neo_kv_append. */
+NEO_API neo_status neo_rope_append(void* q_inout, int32_t num_q_heads, const float* inv_freq, void* k_pages,
+                                   void* v_pages, int64_t page_stride, int64_t num_pages, const int32_t* block_table,
+                                   int32_t max_blocks, const int32_t* seq_lens, const void* k_new, const void* v_new,
+                                   int32_t batch, int32_t num_kv_heads, int32_t head_dim, int32_t page_size,
+                                   void* stream);
+
 /* Default split-K chunk length for a call shape (deterministic in its inputs). */
 NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
 

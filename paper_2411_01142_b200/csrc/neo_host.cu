@@ -435,6 +435,34 @@ NEO_API neo_status neo_kv_append(void* k_pages, void* v_pages, int64_t page_stri
                             static_cast<const uint16_t*>(v_new), batch, hkv, page_size, s);
 }
 
+NEO_API neo_status neo_rope_append(void* q_inout, int32_t hq, const float* inv_freq, void* k_pages, void* v_pages,
+                                   int64_t page_stride, int64_t num_pages, const int32_t* block_table,
+                                   int32_t max_blocks, const int32_t* seq_lens, const void* k_new, const void* v_new,
+                                   int32_t batch, int32_t hkv, int32_t d, int32_t page_size, void* stream) {
+  if (hq < 1 || hkv < 1 || hq % hkv) return fail(NEO_ERR_INVALID_ARG, "num_q_heads must be a multiple of num_kv_heads");
+  if (batch > 0 && (!q_inout || !inv_freq)) return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
+  // shared argument checks (and the no-op for batch == 0) via neo_kv_append's validation path
+  if (d != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
+  if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
+  if (batch < 0) return fail(NEO_ERR_INVALID_ARG, "batch >= 0 required");
+  if (batch == 0) return NEO_OK;
+  if (!k_pages || !v_pages || !block_table || !seq_lens || !k_new || !v_new)
+    return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
+  if (page_stride % 8 != 0 || page_stride < static_cast<int64_t>(hkv) * page_size * d)
+    return fail(NEO_ERR_INVALID_ARG, "page_stride must be a multiple of 8 elements and >= Hkv*P*D");
+  if (num_pages < 1 || max_blocks < 1) return fail(NEO_ERR_INVALID_ARG, "num_pages and max_blocks must be >= 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (neo::debug_validate_enabled()) {
+    neo_status st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_blocks * page_size,
+                                             num_pages, s);
+    if (st != NEO_OK) return st;
+  }
+  return neo::launch_rope_append(static_cast<uint16_t*>(q_inout), hq, inv_freq, static_cast<uint16_t*>(k_pages),
+                                 static_cast<uint16_t*>(v_pages), page_stride, block_table, max_blocks, seq_lens,
+                                 static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), batch, hkv,
+                                 page_size, s);
+}
+
 // ======================================================================= swap
 
 NEO_API neo_status neo_kv_swap_staging_bytes(const neo_kv_pool* pool, int32_t n, int32_t l0, int32_t l1,

@@ -57,6 +57,11 @@ neo_status launch_append(uint16_t* k, uint16_t* v, int64_t page_stride, const in
                          const int32_t* seq_lens, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,
                          int32_t hkv, int32_t page_size, cudaStream_t s);
 
+neo_status launch_rope_append(uint16_t* q, int32_t hq, const float* inv_freq, uint16_t* k, uint16_t* v,
+                              int64_t page_stride, const int32_t* block_table, int32_t max_blocks,
+                              const int32_t* seq_lens, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,
+                              int32_t hkv, int32_t page_size, cudaStream_t s);
+
 // ---- swap (neo_swap.cu)
 constexpr int kMaxSwapIdsPerLaunch = 960;  // page ids passed by value in the kernel params
 struct SwapBatch {

@@ -112,7 +112,87 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendArgs a) {
   }
 }
 
+struct RopeArgs {
+  uint16_t* q;
+  const float* inv_freq;
+  uint16_t* k;
+  uint16_t* v;
+  const uint16_t* k_new;
+  const uint16_t* v_new;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  int64_t page_stride;
+  int32_t max_blocks, hq, hkv, page_size;
+};
+
+__device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
+__device__ __forceinline__ uint16_t f2bf(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+
+// grid (batch), block 256: thread = (head row, dim pair i); rows 0..Hq-1 are q
+// heads (rotated in place), Hq..Hq+Hkv-1 the new k heads (rotated into the page),
+// then the v heads (copied).
+__global__ void __launch_bounds__(256) rope_append_kernel(const RopeArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int b = blockIdx.x;
+  const int n = a.seq_lens[b];
+  if (n <= 0) return;
+  const int t = n - 1;
+  constexpr int kHalf = kHeadDim / 2;
+  const int64_t pid = a.block_table[static_cast<int64_t>(b) * a.max_blocks + t / a.page_size];
+  const int slot = t % a.page_size;
+  const int rows = a.hq + 2 * a.hkv;
+  for (int e = threadIdx.x; e < rows * kHalf; e += blockDim.x) {
+    const int row = e / kHalf, i = e % kHalf;
+    if (row >= a.hq + a.hkv) {                       // v: plain copy of the pair
+      const int g = row - a.hq - a.hkv;
+      const uint16_t* src = a.v_new + (static_cast<int64_t>(b) * a.hkv + g) * kHeadDim;
+      uint16_t* dst = a.v + pid * a.page_stride + (static_cast<int64_t>(g) * a.page_size + slot) * kHeadDim;
+      dst[i] = src[i];
+      dst[i + kHalf] = src[i + kHalf];
+      continue;
+    }
+    double sd, cd;
+    sincos(static_cast<double>(t) * static_cast<double>(a.inv_freq[i]), &sd, &cd);
+    const float s = static_cast<float>(sd), c = static_cast<float>(cd);
+    uint16_t* src;
+    uint16_t* dst;
+    if (row < a.hq) {
+      src = dst = a.q + (static_cast<int64_t>(b) * a.hq + row) * kHeadDim;
+    } else {
+      const int g = row - a.hq;
+      src = const_cast<uint16_t*>(a.k_new) + (static_cast<int64_t>(b) * a.hkv + g) * kHeadDim;
+      dst = a.k + pid * a.page_stride + (static_cast<int64_t>(g) * a.page_size + slot) * kHeadDim;
+    }
+    const float x0 = bf2f(src[i]), x1 = bf2f(src[i + kHalf]);
+    dst[i] = f2bf(x0 * c - x1 * s);
+    dst[i + kHalf] = f2bf(x1 * c + x0 * s);
+  }
+}
+
 }  // namespace
+
+neo_status launch_rope_append(uint16_t* q, int32_t hq, const float* inv_freq, uint16_t* k, uint16_t* v,
+                              int64_t page_stride, const int32_t* block_table, int32_t max_blocks,
+                              const int32_t* seq_lens, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,
+                              int32_t hkv, int32_t page_size, cudaStream_t s) {
+  RopeArgs a{q, inv_freq, k, v, k_new, v_new, block_table, seq_lens, page_stride, max_blocks, hq, hkv, page_size};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(batch);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, rope_append_kernel, a);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? NEO_OK : cuda_fail(e, "rope append kernel launch");
+}
 
 neo_status launch_append(uint16_t* k, uint16_t* v, int64_t page_stride, const int32_t* block_table, int32_t max_blocks,
                          const int32_t* seq_lens, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,

@@ -26,7 +26,7 @@ EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_c
             "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
             "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
             "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
-            "neo_kv_append", "neo_schedule"]
+            "neo_kv_append", "neo_schedule", "neo_rope_append"]
 
 
 class NeoError(RuntimeError):
@@ -72,6 +72,7 @@ def lib() -> ctypes.CDLL:
                 "neo_cpu_decode_attn": [P, i32, P, P, i32, P, P, i32, i32, ctypes.c_float, i32],
                 "neo_kv_append": [P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
                 "neo_schedule": [P, P, i32, i64, i64, P, P, P, P, P],
+                "neo_rope_append": [P, i32, P, P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
             }
             for name, args in sig.items():
                 if os.environ.get("NEO_LIB") and not hasattr(L, name):
@@ -195,6 +196,22 @@ def kv_append(k_pages, v_pages, block_table, seq_lens, k_new, v_new, stream=None
                               int(num_pages if num_pages is not None else npages), block_table.data_ptr(),
                               block_table.shape[1], seq_lens.data_ptr(), k_new.data_ptr(), v_new.data_ptr(),
                               k_new.shape[0], hkv, d, P, _stream(stream)))
+
+
+def rope_append(q, inv_freq, k_pages, v_pages, block_table, seq_lens, k_new, v_new, stream=None, num_pages=None):
+    """neo_rope_append: rotate q (in place) and k_new at position seq_lens[b]-1 with
+    the frequency table inv_freq (float32 [D/2], cuda), write k/v into the pages."""
+    import torch
+    for name, t in (("q", q), ("inv_freq", inv_freq), ("k_pages", k_pages), ("k_new", k_new), ("v_new", v_new)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if inv_freq.dtype != torch.float32 or not q.is_contiguous():
+        raise ValueError("inv_freq must be float32 and q contiguous")
+    npages, hkv, P, d = k_pages.shape
+    check(lib().neo_rope_append(q.data_ptr(), q.shape[1], inv_freq.data_ptr(), k_pages.data_ptr(),
+                                v_pages.data_ptr(), k_pages.stride(0), int(num_pages if num_pages is not None else npages),
+                                block_table.data_ptr(), block_table.shape[1], seq_lens.data_ptr(), k_new.data_ptr(),
+                                v_new.data_ptr(), q.shape[0], hkv, d, P, _stream(stream)))
 
 
 # ------------------------------------------------------------------ scheduler

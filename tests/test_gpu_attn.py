@@ -272,3 +272,45 @@ def test_cuda_graph_capture_matches_eager():
         torch.cuda.synchronize()
         for e, o in zip(eager, outs):
             assert torch.equal(e.view(torch.int16), o.view(torch.int16)), rep
+
+
+def test_rope_append_then_attend():
+    """neo_rope_append: q rotated in place and k rotated into its page slot match the
+    fp64 RoPE oracle (tolerance rule), v lands bit-exact, and attention over the
+    grown cache matches the oracle on the oracle's rotated inputs."""
+    import torch
+    from oracle import rope as orope
+    import oracle
+    from paper_2411_01142_b200 import neo
+    ctx_new = [1, 17, 300, 4096]
+    case = Case(ctx_new, 32, 8, seed=71)
+    P = case.P
+    f = orope.llama_inv_freq()
+    inv = torch.from_numpy(f).cuda()
+    k_new = np.stack([case.k_req[b][n - 1] for b, n in enumerate(ctx_new)])
+    v_new = np.stack([case.v_req[b][n - 1] for b, n in enumerate(ctx_new)])
+    kn = torch.from_numpy(k_new.view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(v_new.view(np.int16)).cuda().view(torch.bfloat16)
+    q = case.q_dev.clone()
+    neo.rope_append(q, inv, case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, kn, vn)
+    torch.cuda.synchronize()
+    q_got = ni.bf16_bits_to_f64(q.view(torch.int16).cpu().numpy().view(np.uint16))
+    for b, n in enumerate(ctx_new):
+        t = n - 1
+        ref_q = orope.rope(ni.bf16_bits_to_f64(case.q[b]), t, f)
+        assert within_tol(q_got[b], ref_q)[0]
+        k_pg = case.k_dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        ref_k = orope.rope(ni.bf16_bits_to_f64(k_new[b]), t, f)
+        assert within_tol(ni.bf16_bits_to_f64(k_pg), ref_k)[0]
+        v_pg = case.v_dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(v_pg, v_new[b])
+    out = neo.decode_attn(q, case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.max_seq_len)
+    torch.cuda.synchronize()
+    got = case.out_f64(out)
+    for b, n in enumerate(ctx_new):
+        t = n - 1
+        qr = ni.f32_to_bf16_bits(orope.rope(ni.bf16_bits_to_f64(case.q[b]), t, f).astype(np.float32))
+        kr = case.k_req[b].copy()
+        kr[t] = ni.f32_to_bf16_bits(orope.rope(ni.bf16_bits_to_f64(k_new[b]), t, f).astype(np.float32))
+        ref = oracle.decode_attention(qr, kr, case.v_req[b], np.float32(case.scale))
+        assert within_tol(got[b], ref)[0]

@@ -238,3 +238,37 @@ def test_gather_pages_definition():
     host = rng.integers(0, 65535, size=(6, L, 2, H, P, D), dtype=np.uint16)
     hr = oracle.host_record(host, [5, 0], 0, 2)
     assert np.array_equal(hr[0], host[5, 0:2]) and np.array_equal(hr[1], host[0, 0:2])
+
+
+# ---- RoPE oracle pins (oracle/rope.py)
+def test_rope_identity_at_position_zero():
+    from oracle import rope as orope
+    rng = np.random.default_rng(20)
+    x = rng.standard_normal((4, 128))
+    assert np.array_equal(orope.rope(x, 0, orope.llama_inv_freq()), x)
+
+
+def test_rope_preserves_pair_norms_and_matches_complex_form():
+    from oracle import rope as orope
+    rng = np.random.default_rng(21)
+    x = rng.standard_normal((3, 128))
+    f = orope.llama_inv_freq()
+    for pos in (1, 17, 4095, 16383):
+        y = orope.rope(x, pos, f)
+        n0 = x[:, :64] ** 2 + x[:, 64:] ** 2
+        n1 = y[:, :64] ** 2 + y[:, 64:] ** 2
+        np.testing.assert_allclose(n1, n0, rtol=1e-12)
+        z = (x[:, :64] + 1j * x[:, 64:]) * np.exp(1j * pos * f.astype(np.float64))
+        np.testing.assert_allclose(y, np.concatenate([z.real, z.imag], axis=1), rtol=1e-12, atol=1e-12)
+
+
+def test_rope_relative_position_property():
+    """<R_m q, R_n k> = <q, R_{n-m} k>: attention scores depend only on n - m."""
+    from oracle import rope as orope
+    rng = np.random.default_rng(22)
+    q, k = rng.standard_normal(128), rng.standard_normal(128)
+    f = orope.llama_inv_freq()
+    for m, n in ((3, 10), (100, 5000), (7000, 7001)):
+        lhs = orope.rope(q, m, f) @ orope.rope(k, n, f)
+        rhs = q @ orope.rope(k, n - m, f)
+        assert abs(lhs - rhs) <= 1e-9 * (abs(rhs) + np.linalg.norm(q) * np.linalg.norm(k))
