@@ -8,6 +8,9 @@ CUDA library; the CUDA path never imports it.
 * ``decode_attention`` / ``decode_attention_batch`` / ``softmax_weights`` /
   ``partial`` / ``merge`` -- fp64 C (``neo_oracle.c``), unpaged K/V; cites
   P:97-98, P:109-110, P:122, P:307 and S:451, S:468-471 (see the C header).
+* ``prefill_attention`` -- causal prefill (P:237-239 prefill in batch-0; row i
+  of the prompt chunk sees the tokens up to its own position), the decode
+  definition applied row by row.
 * ``gather_pages`` / ``host_record`` -- the page-swap definition (P:235
   "entirely in the GPU-cache ... or entirely in the CPU-cache", P:240
   layer-wise swapping, P:285-288 swap-out/in): a bit copy of the request's pages
@@ -56,8 +59,9 @@ def _load():
             lib.oracle_partial.argtypes = [P, P, P, i32, i32, i32, i32, i64, i64, f64, P, P, P]
             lib.oracle_merge.argtypes = [i32, P, P, P, i32, P]
             lib.oracle_decode_attention_batch.argtypes = [P, P, P, P, i64, i32, i32, i32, f64, P, i32]
+            lib.oracle_prefill_attention.argtypes = [P, P, P, i64, i64, i32, i32, i32, f64, P, i32]
             for f in (lib.oracle_decode_attention, lib.oracle_softmax_weights, lib.oracle_partial,
-                      lib.oracle_merge, lib.oracle_decode_attention_batch):
+                      lib.oracle_merge, lib.oracle_decode_attention_batch, lib.oracle_prefill_attention):
                 f.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -141,6 +145,23 @@ def decode_attention_batch(q_bits, k_list, v_list, scale: float, nthreads: int =
                                                int(nthreads))
     if rc:
         raise ValueError(f"oracle_decode_attention_batch rc={rc}")
+    return out
+
+
+def prefill_attention(q_bits, k_bits, v_bits, scale: float, nthreads: int = 0) -> np.ndarray:
+    """Causal prefill of one request (neo_oracle.c ``oracle_prefill_attention``).
+    q_bits [n_q][Hq][D]: the last n_q of the n tokens in k_bits/v_bits [n][Hkv][D];
+    row i attends to tokens 0 .. n - n_q + i.  Returns [n_q][Hq][D] float64."""
+    q, qp = _u16(q_bits)
+    k, kp = _u16(k_bits)
+    v, vp = _u16(v_bits)
+    n_q, hq, d = q.shape
+    n, hkv, _ = k.shape
+    out = np.zeros((n_q, hq, d), dtype=np.float64)
+    nth = nthreads or min(32, os.cpu_count() or 1)
+    rc = _load().oracle_prefill_attention(qp, kp, vp, n, n_q, hq, hkv, d, float(scale), out.ctypes.data, nth)
+    if rc:
+        raise ValueError(f"oracle_prefill_attention rc={rc}")
     return out
 
 

@@ -201,3 +201,48 @@ int oracle_decode_attention_batch(const uint16_t* q, const uint16_t* k, const ui
   }
   return rc;
 }
+
+/* ---------------------------------------------------------------- prefill
+ * Causal attention of a prompt chunk (the prefill half of batch-0, P:237-239;
+ * SURVEY NEXT-3).  The request holds n KV tokens, the last n_q of which belong to
+ * the n_q query rows being prefilled; query row i sits at position n - n_q + i
+ * and attends to tokens 0 .. n - n_q + i (causal, P:97-98 autoregression: a
+ * token never sees later ones).  Written as the decode definition above applied
+ * row by row to the visible prefix.  q: [n_q][hq][d]; k, v: [n][hkv][d];
+ * out: [n_q][hq][d].  Rows are dealt to threads round-robin. */
+typedef struct {
+  const uint16_t *q, *k, *v;
+  int64_t n, n_q;
+  int hq, hkv, d, tid, nthreads;
+  double scale;
+  double* out;
+  int rc;
+} prefill_job_t;
+
+static void* run_prefill(void* arg) {
+  prefill_job_t* j = (prefill_job_t*)arg;
+  for (int64_t i = j->tid; i < j->n_q && j->rc == 0; i += j->nthreads)
+    j->rc = oracle_decode_attention(j->q + (size_t)i * j->hq * j->d, j->k, j->v, j->n - j->n_q + i + 1, j->hq,
+                                    j->hkv, j->d, j->scale, j->out + (size_t)i * j->hq * j->d);
+  return NULL;
+}
+
+int oracle_prefill_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v, int64_t n, int64_t n_q,
+                             int hq, int hkv, int d, double scale, double* out, int nthreads) {
+  if (n_q < 0 || n_q > n) return -1;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads > 256) nthreads = 256;
+  pthread_t th[256];
+  prefill_job_t jobs[256];
+  int rc = 0, started = 0;
+  for (int i = 0; i < nthreads; ++i) {
+    jobs[i] = (prefill_job_t){q, k, v, n, n_q, hq, hkv, d, i, nthreads, scale, out, 0};
+    if (pthread_create(&th[i], NULL, run_prefill, &jobs[i]) != 0) return -3;
+    ++started;
+  }
+  for (int i = 0; i < started; ++i) {
+    pthread_join(th[i], NULL);
+    if (jobs[i].rc) rc = jobs[i].rc;
+  }
+  return rc;
+}

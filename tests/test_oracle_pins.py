@@ -272,3 +272,68 @@ def test_rope_relative_position_property():
         lhs = orope.rope(q, m, f) @ orope.rope(k, n, f)
         rhs = q @ orope.rope(k, n - m, f)
         assert abs(lhs - rhs) <= 1e-9 * (abs(rhs) + np.linalg.norm(q) * np.linalg.norm(k))
+
+
+# ---- prefill oracle pins (oracle.prefill_attention)
+@pytest.mark.parametrize("n,n_q,hq,hkv", [(300, 300, 32, 8), (500, 129, 8, 2), (64, 1, 4, 4), (200, 77, 16, 1)])
+def test_prefill_against_torch_sdpa_causal_fp64(n, n_q, hq, hkv):
+    """Library routine: torch SDPA in fp64 with an explicit bottom-right causal mask."""
+    rng = np.random.default_rng(n * 7 + n_q)
+    q = rand_bits(rng, (n_q, hq, 128), 2.0)
+    k = rand_bits(rng, (n, hkv, 128))
+    v = rand_bits(rng, (n, hkv, 128))
+    scale = 1 / math.sqrt(128)
+    got = oracle.prefill_attention(q, k, v, scale)
+    G = hq // hkv
+    tq = torch.from_numpy(widen(q)).permute(1, 0, 2)                                  # [Hq][n_q][D]
+    tk = torch.from_numpy(widen(k)).permute(1, 0, 2).repeat_interleave(G, 0)          # [Hq][n][D]
+    tv = torch.from_numpy(widen(v)).permute(1, 0, 2).repeat_interleave(G, 0)
+    mask = torch.arange(n)[None, :] <= (n - n_q + torch.arange(n_q))[:, None]        # [n_q][n]
+    ref = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, attn_mask=mask, scale=scale)
+    np.testing.assert_allclose(got, ref.permute(1, 0, 2).numpy(), rtol=1e-12, atol=1e-13)
+
+
+def test_prefill_first_row_of_full_prompt_is_v0():
+    """A whole-prompt prefill: row 0 sees only token 0, so its output is V[0] exactly."""
+    rng = np.random.default_rng(23)
+    q = rand_bits(rng, (40, 8, 128), 3.0)
+    k = rand_bits(rng, (40, 2, 128))
+    v = rand_bits(rng, (40, 2, 128))
+    out = oracle.prefill_attention(q, k, v, 0.1)
+    for h in range(8):
+        assert np.array_equal(out[0, h], widen(v[0, h // 4]))
+
+
+def test_prefill_is_causal():
+    """Changing K/V of tokens after a row's position leaves that row bit-identical,
+    and changes the rows that can see them."""
+    rng = np.random.default_rng(24)
+    n, n_q = 120, 50
+    q = rand_bits(rng, (n_q, 8, 128), 2.0)
+    k = rand_bits(rng, (n, 2, 128))
+    v = rand_bits(rng, (n, 2, 128))
+    a = oracle.prefill_attention(q, k, v, 0.09)
+    cut = n - n_q + 20                                        # rows 0..20 see tokens < cut + 1
+    k2, v2 = k.copy(), v.copy()
+    k2[cut + 1:] = rand_bits(rng, k2[cut + 1:].shape)
+    v2[cut + 1:] = rand_bits(rng, v2[cut + 1:].shape)
+    b = oracle.prefill_attention(q, k2, v2, 0.09)
+    assert np.array_equal(a[:21], b[:21])
+    assert not np.allclose(a[21:], b[21:])
+
+
+@pytest.mark.parametrize("trial", range(4))
+def test_prefill_brute_force_decimal(trial):
+    rng = np.random.default_rng(300 + trial)
+    n = int(rng.integers(1, 7))
+    n_q = int(rng.integers(1, n + 1))
+    hkv, G, d = 1, int(rng.choice([1, 2])), int(rng.integers(1, 6))
+    q = rand_bits(rng, (n_q, hkv * G, d), 2.0)
+    k = rand_bits(rng, (n, hkv, d), 2.0)
+    v = rand_bits(rng, (n, hkv, d))
+    scale = float(np.float32(1 / math.sqrt(d)))
+    got = oracle.prefill_attention(q, k, v, scale)
+    for i in range(n_q):
+        p = n - n_q + i + 1
+        ref = _decimal_attention(widen(q[i]), widen(k[:p]), widen(v[:p]), scale, G)
+        np.testing.assert_allclose(got[i], ref, rtol=1e-13, atol=1e-15)
