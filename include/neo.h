@@ -191,6 +191,50 @@ NEO_API neo_status neo_rope_append(void* q_inout, int32_t num_q_heads, const flo
                                    int32_t batch, int32_t num_kv_heads, int32_t head_dim, int32_t page_size,
                                    void* stream);
 
+/* Causal paged GQA prefill attention (the prefill half of
+ * batch-0; attention as P:97-98): for request b with
+ * n_q = q_offsets[b+1] - q_offsets[b] query tokens that are the LAST n_q of its
+ * n = seq_lens[b] cached tokens, query row i (packed row j = q_offsets[b] + i,
+ * position p = n - n_q + i) and q-head h (kv-head g = h / G):
+ *   out[j][h][:] = sum_{t <= p} softmax_t(scale * q[j][h] . K_b[t][g]) V_b[t][g][:]
+ * K_b[t] lives in page block_table[b][t / P], slot t % P (as neo_decode_attn).
+ * The new tokens' K/V must already be in the pages (neo_prefill_append).
+ *   q, out     [total_tokens][Hq][D] bf16 device, 16-byte aligned
+ *   q_offsets  device int32[batch + 1], 0 = q_offsets[0] <= ... = total_tokens
+ *   max_q_len  >= every n_q (sizes the grid; rows beyond a request's n_q idle)
+ *   G = Hq / Hkv in {1, 2, 4, 8, 16}; D = 128; P a multiple of 16.
+ * Numerics: bf16 x bf16 products exact in fp32 (tcgen05.mma), softmax in fp32
+ * (exp2 domain), P applied as bf16 hi + lo, output RNE to bf16.  Deterministic.
+ * Page-tail slots beyond seq_lens are never read into the result (NaN-safe).
+ * Errors: NEO_ERR_INVALID_ARG, NEO_ERR_UNSUPPORTED, NEO_ERR_CUDA; NEO_DEBUG_VALIDATE=1
+ * checks the metadata on the host.  batch == 0 or total_tokens == 0 is a no-op. */
+NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+                                    int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
+                                    const int32_t* seq_lens, const int32_t* q_offsets, void* out, int32_t batch,
+                                    int32_t total_tokens, int32_t num_q_heads, int32_t num_kv_heads,
+                                    int32_t head_dim, int32_t page_size, int32_t max_q_len, float scale,
+                                    void* stream);
+
+/* Prefill-side store (P:237-239 prefill in batch-0): write the
+ * K and V rows of a packed batch of prompt chunks into the paged cache, with
+ * optional RoPE (same convention and precision as neo_rope_append).
+ *   request b owns packed tokens j in [q_offsets[b], q_offsets[b+1]) (device
+ *   int32[batch + 1], q_offsets[0] = 0, q_offsets[batch] = total_tokens); its
+ *   n_q = q_offsets[b+1] - q_offsets[b] new tokens are the LAST n_q of its
+ *   seq_lens[b] tokens: token j sits at position t = seq_lens[b] - n_q +
+ *   (j - q_offsets[b]), written to page block_table[b][t / P], slot t % P.
+ *   k_new, v_new: [total_tokens][Hkv][D]; q_inout: [total_tokens][Hq][D].
+ *   inv_freq NULL: plain copy, q untouched (may be NULL).  Otherwise q rows are
+ *   rotated in place and k rows rotated before the store; v is copied.
+ * Errors as neo_rope_append; NEO_DEBUG_VALIDATE=1 also checks q_offsets.
+ * batch == 0 or total_tokens == 0 is a no-op. */
+NEO_API neo_status neo_prefill_append(void* q_inout, int32_t num_q_heads, const float* inv_freq, void* k_pages,
+                                      void* v_pages, int64_t page_stride, int64_t num_pages,
+                                      const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                                      const int32_t* q_offsets, const void* k_new, const void* v_new, int32_t batch,
+                                      int32_t total_tokens, int32_t num_kv_heads, int32_t head_dim,
+                                      int32_t page_size, void* stream);
+
 /* Default split-K chunk length for a call shape (deterministic in its inputs). */
 NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
 

@@ -43,13 +43,15 @@ static bool debug_validate_enabled() {
 // ----------------------------------------------------------------- tensor maps
 namespace {
 
+enum TmKind : int32_t { kTmDecodeKV = 0, kTmPrefillKV = 1, kTmPrefillQ = 2 };
+
 struct TmKey {
   const void* ptr;
   int64_t page_stride, num_pages;
-  int32_t hkv, page_size;
+  int32_t hkv, page_size, kind;
   bool operator==(const TmKey& o) const {
     return ptr == o.ptr && page_stride == o.page_stride && num_pages == o.num_pages && hkv == o.hkv &&
-           page_size == o.page_size;
+           page_size == o.page_size && kind == o.kind;
   }
 };
 struct TmKeyHash {
@@ -58,6 +60,7 @@ struct TmKeyHash {
     h ^= std::hash<int64_t>()(k.page_stride) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
     h ^= std::hash<int64_t>()(k.num_pages) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
     h ^= std::hash<int64_t>()((static_cast<int64_t>(k.hkv) << 32) | k.page_size) + (h << 6) + (h >> 2);
+    h ^= std::hash<int32_t>()(k.kind) + (h << 6) + (h >> 2);
     return h;
   }
 };
@@ -77,12 +80,8 @@ neo_status get_encoder() {
   return NEO_OK;
 }
 
-// View of a layer's K (or V) pages as a 5-D tensor {64 el, 2 halves, P tokens,
-// Hkv heads, num_pages} with box {64, 2, 16, 1, 1}: one TMA load = one 16-token
-// tile (4 KiB) of one (page, kv-head), written to shared memory 128B-swizzled.
-neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,
-                      CUtensorMap* out) {
-  TmKey key{ptr, page_stride, num_pages, hkv, P};
+neo_status encode_cached(const TmKey& key, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
+                         const cuuint32_t* box, CUtensorMap* out) {
   std::lock_guard<std::mutex> lk(g_tm_mu);
   auto it = g_tm_cache.find(key);
   if (it != g_tm_cache.end()) {
@@ -93,20 +92,55 @@ neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, i
   if (st != NEO_OK) return st;
   CUtensorMap tm;
   std::memset(&tm, 0, sizeof tm);
-  cuuint64_t dims[5] = {64, 2, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(hkv),
-                        static_cast<cuuint64_t>(num_pages)};
-  cuuint64_t strides[4] = {128, 256, static_cast<cuuint64_t>(P) * 256, static_cast<cuuint64_t>(page_stride) * 2};
-  cuuint32_t box[5] = {64, 2, 16, 1, 1};
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = g_encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = g_encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(key.ptr), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(NEO_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   if (g_tm_cache.size() > 4096) g_tm_cache.clear();
   g_tm_cache.emplace(key, tm);
   *out = tm;
   return NEO_OK;
 }
+
+}  // namespace
+
+// View of a layer's K (or V) pages as a 5-D tensor {64 el, 2 halves, P tokens,
+// Hkv heads, num_pages} with box {64, 2, 16, 1, 1}: one TMA load = one 16-token
+// tile (4 KiB) of one (page, kv-head), written to shared memory 128B-swizzled.
+neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,
+                      CUtensorMap* out) {
+  const cuuint64_t dims[5] = {64, 2, static_cast<cuuint64_t>(P), static_cast<cuuint64_t>(hkv),
+                              static_cast<cuuint64_t>(num_pages)};
+  const cuuint64_t strides[4] = {128, 256, static_cast<cuuint64_t>(P) * 256,
+                                 static_cast<cuuint64_t>(page_stride) * 2};
+  const cuuint32_t box[5] = {64, 2, 16, 1, 1};
+  return encode_cached(TmKey{ptr, page_stride, num_pages, hkv, P, kTmDecodeKV}, 5, dims, strides, box, out);
+}
+
+// Prefill view of the same pages: {64 el, P tokens, 2 halves, Hkv, num_pages}
+// with box {64, 16, 1, 1, 1}: one TMA load = one dim-half of 16 tokens (2 KiB),
+// landing as 16 rows of 128 B -- the canonical SW128 operand layout of tcgen05.
+neo_status tensor_map_prefill_kv(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,
+                                 CUtensorMap* out) {
+  const cuuint64_t dims[5] = {64, static_cast<cuuint64_t>(P), 2, static_cast<cuuint64_t>(hkv),
+                              static_cast<cuuint64_t>(num_pages)};
+  const cuuint64_t strides[4] = {256, 128, static_cast<cuuint64_t>(P) * 256, static_cast<cuuint64_t>(page_stride) * 2};
+  const cuuint32_t box[5] = {64, 16, 1, 1, 1};
+  return encode_cached(TmKey{ptr, page_stride, num_pages, hkv, P, kTmPrefillKV}, 5, dims, strides, box, out);
+}
+
+// Packed prefill queries q[T][Hq][128] as {64 el, Hq, T, 2 halves} with box
+// {64, G, 128 / G, 1}: one load = one dim-half of a 128-row M tile whose row
+// r = (token r / G, head r % G of the kv group), rows of 128 B.
+neo_status tensor_map_prefill_q(const void* ptr, int32_t total_tokens, int32_t hq, int32_t G, CUtensorMap* out) {
+  const cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(hq), static_cast<cuuint64_t>(total_tokens), 2};
+  const cuuint64_t strides[3] = {256, static_cast<cuuint64_t>(hq) * 256, 128};
+  const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(128 / G), 1};
+  return encode_cached(TmKey{ptr, total_tokens, hq, G, 0, kTmPrefillQ}, 4, dims, strides, box, out);
+}
+
+namespace {
 
 int32_t default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
   // Aim for ~3 waves of one-warp units over 148 SMs x 12 resident warps (the
@@ -151,6 +185,22 @@ neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, c
                                              "] = " + std::to_string(id) + " outside [0, num_pages)");
     }
   }
+  return NEO_OK;
+}
+
+// q_offsets [batch + 1]: 0 = q_offsets[0] <= ... <= q_offsets[batch] = total, and
+// each request's new tokens fit its context (q_len_b <= seq_lens[b]).
+neo_status debug_validate_offsets(const int32_t* q_offsets, const int32_t* seq_lens, int32_t batch, int32_t total,
+                                  cudaStream_t stream) {
+  std::vector<int32_t> off(batch + 1), sl(batch);
+  cudaError_t e = cudaMemcpyAsync(off.data(), q_offsets, sizeof(int32_t) * (batch + 1), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(sl.data(), seq_lens, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return cuda_fail(e, "NEO_DEBUG_VALIDATE copy");
+  if (off[0] != 0 || off[batch] != total) return fail(NEO_ERR_INVALID_ARG, "q_offsets must run from 0 to total_tokens");
+  for (int32_t b = 0; b < batch; ++b)
+    if (off[b + 1] < off[b] || off[b + 1] - off[b] > sl[b])
+      return fail(NEO_ERR_INVALID_ARG, "request " + std::to_string(b) + ": q length negative or above seq_lens");
   return NEO_OK;
 }
 
@@ -409,6 +459,49 @@ NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const voi
   return neo::launch_decode_attn(L, tmk, tmv);
 }
 
+NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+                                    int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
+                                    const int32_t* seq_lens, const int32_t* q_offsets, void* out, int32_t batch,
+                                    int32_t total_tokens, int32_t hq, int32_t hkv, int32_t d, int32_t page_size,
+                                    int32_t max_q_len, float scale, void* stream) {
+  if (d != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
+  if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
+  if (batch < 0 || total_tokens < 0 || hq < 1 || hkv < 1 || hq % hkv)
+    return fail(NEO_ERR_INVALID_ARG, "batch, total_tokens >= 0 and num_q_heads a multiple of num_kv_heads required");
+  const int32_t G = hq / hkv;
+  if (G > 16 || (G & (G - 1))) return fail(NEO_ERR_UNSUPPORTED, "G = Hq / Hkv must be 1, 2, 4, 8 or 16");
+  if (batch == 0 || total_tokens == 0) return NEO_OK;
+  if (batch > 65535) return fail(NEO_ERR_UNSUPPORTED, "batch <= 65535");
+  if (!q || !k_pages || !v_pages || !block_table || !seq_lens || !q_offsets || !out)
+    return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
+  if (!neo::aligned16(q) || !neo::aligned16(k_pages) || !neo::aligned16(v_pages) || !neo::aligned16(out))
+    return fail(NEO_ERR_INVALID_ARG, "q, pages and out must be 16-byte aligned");
+  if (page_stride % 8 != 0 || page_stride < static_cast<int64_t>(hkv) * page_size * d)
+    return fail(NEO_ERR_INVALID_ARG, "page_stride must be a multiple of 8 elements and >= Hkv*P*D");
+  if (num_pages < 1 || max_blocks < 1 || max_q_len < 1)
+    return fail(NEO_ERR_INVALID_ARG, "num_pages, max_blocks and max_q_len must be >= 1");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(NEO_ERR_INVALID_ARG, "scale must be finite and > 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  neo_status st;
+  if (neo::debug_validate_enabled()) {
+    st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_blocks * page_size,
+                                  num_pages, s);
+    if (st != NEO_OK) return st;
+    st = neo::debug_validate_offsets(q_offsets, seq_lens, batch, total_tokens, s);
+    if (st != NEO_OK) return st;
+  }
+  CUtensorMap tmq, tmk, tmv;
+  st = neo::tensor_map_prefill_q(q, total_tokens, hq, G, &tmq);
+  if (st != NEO_OK) return st;
+  st = neo::tensor_map_prefill_kv(k_pages, page_stride, num_pages, hkv, page_size, &tmk);
+  if (st != NEO_OK) return st;
+  st = neo::tensor_map_prefill_kv(v_pages, page_stride, num_pages, hkv, page_size, &tmv);
+  if (st != NEO_OK) return st;
+  neo::PrefillLaunch L{out, block_table, seq_lens, q_offsets, batch, hq, hkv, page_size, max_blocks, max_q_len, scale,
+                       s};
+  return neo::launch_prefill_attn(L, tmq, tmk, tmv);
+}
+
 NEO_API neo_status neo_kv_append(void* k_pages, void* v_pages, int64_t page_stride, int64_t num_pages,
                                  const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
                                  const void* k_new, const void* v_new, int32_t batch, int32_t hkv, int32_t d,
@@ -435,32 +528,74 @@ NEO_API neo_status neo_kv_append(void* k_pages, void* v_pages, int64_t page_stri
                             static_cast<const uint16_t*>(v_new), batch, hkv, page_size, s);
 }
 
+namespace {
+// argument checks shared by neo_rope_append and neo_prefill_append
+neo_status check_rope_store(const void* q, int32_t hq, const float* inv_freq, const void* k_pages,
+                            const void* v_pages, int64_t page_stride, int64_t num_pages, const int32_t* block_table,
+                            int32_t max_blocks, const int32_t* seq_lens, const void* k_new, const void* v_new,
+                            int32_t hkv, int32_t d, int32_t page_size) {
+  if (d != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
+  if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
+  if (hkv < 1) return fail(NEO_ERR_INVALID_ARG, "num_kv_heads >= 1 required");
+  if (inv_freq && (hq < 1 || hq % hkv || !q)) return fail(NEO_ERR_INVALID_ARG,
+                                                          "RoPE needs q and num_q_heads a multiple of num_kv_heads");
+  if (!k_pages || !v_pages || !block_table || !seq_lens || !k_new || !v_new)
+    return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
+  if (!neo::aligned16(k_pages) || !neo::aligned16(v_pages) || !neo::aligned16(k_new) || !neo::aligned16(v_new) ||
+      (inv_freq && !neo::aligned16(q)))
+    return fail(NEO_ERR_INVALID_ARG, "pages, q and k_new/v_new must be 16-byte aligned");
+  if (page_stride % 8 != 0 || page_stride < static_cast<int64_t>(hkv) * page_size * d)
+    return fail(NEO_ERR_INVALID_ARG, "page_stride must be a multiple of 8 elements and >= Hkv*P*D");
+  if (num_pages < 1 || max_blocks < 1) return fail(NEO_ERR_INVALID_ARG, "num_pages and max_blocks must be >= 1");
+  return NEO_OK;
+}
+}  // namespace
+
 NEO_API neo_status neo_rope_append(void* q_inout, int32_t hq, const float* inv_freq, void* k_pages, void* v_pages,
                                    int64_t page_stride, int64_t num_pages, const int32_t* block_table,
                                    int32_t max_blocks, const int32_t* seq_lens, const void* k_new, const void* v_new,
                                    int32_t batch, int32_t hkv, int32_t d, int32_t page_size, void* stream) {
-  if (hq < 1 || hkv < 1 || hq % hkv) return fail(NEO_ERR_INVALID_ARG, "num_q_heads must be a multiple of num_kv_heads");
-  if (batch > 0 && (!q_inout || !inv_freq)) return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
-  // shared argument checks (and the no-op for batch == 0) via neo_kv_append's validation path
-  if (d != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
-  if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
   if (batch < 0) return fail(NEO_ERR_INVALID_ARG, "batch >= 0 required");
   if (batch == 0) return NEO_OK;
-  if (!k_pages || !v_pages || !block_table || !seq_lens || !k_new || !v_new)
-    return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
-  if (page_stride % 8 != 0 || page_stride < static_cast<int64_t>(hkv) * page_size * d)
-    return fail(NEO_ERR_INVALID_ARG, "page_stride must be a multiple of 8 elements and >= Hkv*P*D");
-  if (num_pages < 1 || max_blocks < 1) return fail(NEO_ERR_INVALID_ARG, "num_pages and max_blocks must be >= 1");
+  if (!inv_freq) return fail(NEO_ERR_INVALID_ARG, "NULL inv_freq");
+  neo_status st = check_rope_store(q_inout, hq, inv_freq, k_pages, v_pages, page_stride, num_pages, block_table,
+                                   max_blocks, seq_lens, k_new, v_new, hkv, d, page_size);
+  if (st != NEO_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (neo::debug_validate_enabled()) {
-    neo_status st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_blocks * page_size,
-                                             num_pages, s);
+    st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_blocks * page_size,
+                                  num_pages, s);
     if (st != NEO_OK) return st;
   }
   return neo::launch_rope_append(static_cast<uint16_t*>(q_inout), hq, inv_freq, static_cast<uint16_t*>(k_pages),
                                  static_cast<uint16_t*>(v_pages), page_stride, block_table, max_blocks, seq_lens,
-                                 static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new), batch, hkv,
-                                 page_size, s);
+                                 nullptr, static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new),
+                                 batch, batch, hkv, page_size, s);
+}
+
+NEO_API neo_status neo_prefill_append(void* q_inout, int32_t hq, const float* inv_freq, void* k_pages,
+                                      void* v_pages, int64_t page_stride, int64_t num_pages,
+                                      const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                                      const int32_t* q_offsets, const void* k_new, const void* v_new, int32_t batch,
+                                      int32_t total_tokens, int32_t hkv, int32_t d, int32_t page_size, void* stream) {
+  if (batch < 0 || total_tokens < 0) return fail(NEO_ERR_INVALID_ARG, "batch >= 0 and total_tokens >= 0 required");
+  if (batch == 0 || total_tokens == 0) return NEO_OK;
+  if (!q_offsets) return fail(NEO_ERR_INVALID_ARG, "NULL q_offsets");
+  neo_status st = check_rope_store(q_inout, hq, inv_freq, k_pages, v_pages, page_stride, num_pages, block_table,
+                                   max_blocks, seq_lens, k_new, v_new, hkv, d, page_size);
+  if (st != NEO_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (neo::debug_validate_enabled()) {
+    st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_blocks * page_size,
+                                  num_pages, s);
+    if (st != NEO_OK) return st;
+    st = neo::debug_validate_offsets(q_offsets, seq_lens, batch, total_tokens, s);
+    if (st != NEO_OK) return st;
+  }
+  return neo::launch_rope_append(static_cast<uint16_t*>(q_inout), hq, inv_freq, static_cast<uint16_t*>(k_pages),
+                                 static_cast<uint16_t*>(v_pages), page_stride, block_table, max_blocks, seq_lens,
+                                 q_offsets, static_cast<const uint16_t*>(k_new), static_cast<const uint16_t*>(v_new),
+                                 batch, total_tokens, hkv, page_size, s);
 }
 
 // ======================================================================= swap

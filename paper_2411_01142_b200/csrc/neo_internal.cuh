@@ -51,6 +51,28 @@ neo_status launch_decode_attn(const AttnLaunch& a, const CUtensorMap& tmk, const
 neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
                                int32_t batch, int32_t page_size, int32_t max_seq_len, int64_t num_pages,
                                cudaStream_t stream);
+neo_status debug_validate_offsets(const int32_t* q_offsets, const int32_t* seq_lens, int32_t batch, int32_t total,
+                                  cudaStream_t stream);
+
+// ---- tensor maps (neo_host.cu; cached by pointer and shape)
+neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,
+                      CUtensorMap* out);
+neo_status tensor_map_prefill_kv(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,
+                                 CUtensorMap* out);
+neo_status tensor_map_prefill_q(const void* ptr, int32_t total_tokens, int32_t hq, int32_t G, CUtensorMap* out);
+
+// ---- prefill attention (neo_prefill.cu)
+struct PrefillLaunch {
+  void* out;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  const int32_t* q_offsets;
+  int32_t batch, hq, hkv, page_size, max_blocks, max_q_len;
+  float scale;
+  cudaStream_t stream;
+};
+neo_status launch_prefill_attn(const PrefillLaunch& a, const CUtensorMap& tmq, const CUtensorMap& tmk,
+                               const CUtensorMap& tmv);
 
 // ---- KV append (neo_swap.cu)
 neo_status launch_append(uint16_t* k, uint16_t* v, int64_t page_stride, const int32_t* block_table, int32_t max_blocks,
@@ -59,8 +81,9 @@ neo_status launch_append(uint16_t* k, uint16_t* v, int64_t page_stride, const in
 
 neo_status launch_rope_append(uint16_t* q, int32_t hq, const float* inv_freq, uint16_t* k, uint16_t* v,
                               int64_t page_stride, const int32_t* block_table, int32_t max_blocks,
-                              const int32_t* seq_lens, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,
-                              int32_t hkv, int32_t page_size, cudaStream_t s);
+                              const int32_t* seq_lens, const int32_t* q_offsets, const uint16_t* k_new,
+                              const uint16_t* v_new, int32_t batch, int32_t tokens, int32_t hkv, int32_t page_size,
+                              cudaStream_t s);
 
 // ---- swap (neo_swap.cu)
 constexpr int kMaxSwapIdsPerLaunch = 960;  // page ids passed by value in the kernel params

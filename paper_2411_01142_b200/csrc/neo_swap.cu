@@ -114,15 +114,16 @@ __global__ void __launch_bounds__(256) append_kernel(const AppendArgs a) {
 
 struct RopeArgs {
   uint16_t* q;
-  const float* inv_freq;
+  const float* inv_freq;     // NULL: no rotation (plain multi-token append)
   uint16_t* k;
   uint16_t* v;
   const uint16_t* k_new;
   const uint16_t* v_new;
   const int32_t* block_table;
   const int32_t* seq_lens;
+  const int32_t* q_offsets;  // [batch + 1]; NULL: token j is request j's single new token
   int64_t page_stride;
-  int32_t max_blocks, hq, hkv, page_size;
+  int32_t batch, max_blocks, hq, hkv, page_size;
 };
 
 __device__ __forceinline__ float bf2f(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
@@ -130,46 +131,87 @@ __device__ __forceinline__ uint16_t f2bf(float f) {
   const uint32_t u = __float_as_uint(f);
   return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
 }
+__device__ __forceinline__ float lo_f(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float hi_f(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  return static_cast<uint32_t>(f2bf(lo)) | (static_cast<uint32_t>(f2bf(hi)) << 16);
+}
 
-// grid (batch), block 256: thread = (head row, dim pair i); rows 0..Hq-1 are q
-// heads (rotated in place), Hq..Hq+Hkv-1 the new k heads (rotated into the page),
-// then the v heads (copied).
-__global__ void __launch_bounds__(256) rope_append_kernel(const RopeArgs a) {
+// grid (tokens), block 128: one packed token j of request b at position t.
+// sin/cos of theta_i = t * inv_freq[i] (fp64) are computed once per token into
+// shared memory; then work item (row, oct) rotates the 8 dim pairs
+// (8 oct + e, 8 oct + e + D/2) of one head row with two 16-byte loads / stores.
+// Rows 0..Hq-1 are q heads (rotated in place), Hq..Hq+Hkv-1 the new k heads
+// (rotated into the page slot), then the v heads (copied).
+__global__ void __launch_bounds__(128) rope_append_kernel(const RopeArgs a) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int b = blockIdx.x;
-  const int n = a.seq_lens[b];
-  if (n <= 0) return;
-  const int t = n - 1;
   constexpr int kHalf = kHeadDim / 2;
+  __shared__ float cs[kHalf], sn[kHalf];
+  const int j = blockIdx.x;
+  int b = j, n_q = 1, i_q = 0;
+  if (a.q_offsets) {                      // request of packed token j: last b with q_offsets[b] <= j
+    int lo = 0, hi = a.batch - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.q_offsets[mid] <= j) lo = mid;
+      else hi = mid - 1;
+    }
+    b = lo;
+    n_q = a.q_offsets[b + 1] - a.q_offsets[b];
+    i_q = j - a.q_offsets[b];
+  }
+  const int n = a.seq_lens[b];
+  if (n <= 0 || i_q >= n_q) return;
+  const int t = n - n_q + i_q;
+  const bool rope = a.inv_freq != nullptr;
+  if (rope) {
+    for (int i = threadIdx.x; i < kHalf; i += blockDim.x) {
+      double sd, cd;
+      sincos(static_cast<double>(t) * static_cast<double>(a.inv_freq[i]), &sd, &cd);
+      cs[i] = static_cast<float>(cd);
+      sn[i] = static_cast<float>(sd);
+    }
+    __syncthreads();
+  }
   const int64_t pid = a.block_table[static_cast<int64_t>(b) * a.max_blocks + t / a.page_size];
   const int slot = t % a.page_size;
-  const int rows = a.hq + 2 * a.hkv;
-  for (int e = threadIdx.x; e < rows * kHalf; e += blockDim.x) {
-    const int row = e / kHalf, i = e % kHalf;
-    if (row >= a.hq + a.hkv) {                       // v: plain copy of the pair
-      const int g = row - a.hq - a.hkv;
-      const uint16_t* src = a.v_new + (static_cast<int64_t>(b) * a.hkv + g) * kHeadDim;
-      uint16_t* dst = a.v + pid * a.page_stride + (static_cast<int64_t>(g) * a.page_size + slot) * kHeadDim;
-      dst[i] = src[i];
-      dst[i + kHalf] = src[i + kHalf];
+  const int q_rows = rope ? a.hq : 0;
+  const int rows = q_rows + 2 * a.hkv;
+  for (int e = threadIdx.x; e < rows * 8; e += blockDim.x) {
+    const int row = e >> 3, oct = e & 7;
+    const uint16_t* src;
+    uint16_t* dst;
+    bool rotate = rope;
+    if (row < q_rows) {
+      src = dst = a.q + (static_cast<int64_t>(j) * a.hq + row) * kHeadDim;
+    } else {
+      const int kv = row - q_rows >= a.hkv;
+      const int g = row - q_rows - (kv ? a.hkv : 0);
+      src = (kv ? a.v_new : a.k_new) + (static_cast<int64_t>(j) * a.hkv + g) * kHeadDim;
+      dst = (kv ? a.v : a.k) + pid * a.page_stride + (static_cast<int64_t>(g) * a.page_size + slot) * kHeadDim;
+      rotate = rope && !kv;
+    }
+    const uint4 x0 = *reinterpret_cast<const uint4*>(src + oct * 8);
+    const uint4 x1 = *reinterpret_cast<const uint4*>(src + kHalf + oct * 8);
+    if (!rotate) {
+      *reinterpret_cast<uint4*>(dst + oct * 8) = x0;
+      *reinterpret_cast<uint4*>(dst + kHalf + oct * 8) = x1;
       continue;
     }
-    double sd, cd;
-    sincos(static_cast<double>(t) * static_cast<double>(a.inv_freq[i]), &sd, &cd);
-    const float s = static_cast<float>(sd), c = static_cast<float>(cd);
-    uint16_t* src;
-    uint16_t* dst;
-    if (row < a.hq) {
-      src = dst = a.q + (static_cast<int64_t>(b) * a.hq + row) * kHeadDim;
-    } else {
-      const int g = row - a.hq;
-      src = const_cast<uint16_t*>(a.k_new) + (static_cast<int64_t>(b) * a.hkv + g) * kHeadDim;
-      dst = a.k + pid * a.page_stride + (static_cast<int64_t>(g) * a.page_size + slot) * kHeadDim;
+    const uint32_t w0[4] = {x0.x, x0.y, x0.z, x0.w}, w1[4] = {x1.x, x1.y, x1.z, x1.w};
+    uint32_t y0[4], y1[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int i = oct * 8 + 2 * w;
+      const float a0 = lo_f(w0[w]), a1 = hi_f(w0[w]);   // x[i], x[i + 1]
+      const float b0 = lo_f(w1[w]), b1 = hi_f(w1[w]);   // x[i + D/2], x[i + 1 + D/2]
+      const float c0 = cs[i], s0 = sn[i], c1 = cs[i + 1], s1 = sn[i + 1];
+      y0[w] = pack2(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
+      y1[w] = pack2(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
     }
-    const float x0 = bf2f(src[i]), x1 = bf2f(src[i + kHalf]);
-    dst[i] = f2bf(x0 * c - x1 * s);
-    dst[i + kHalf] = f2bf(x1 * c + x0 * s);
+    *reinterpret_cast<uint4*>(dst + oct * 8) = make_uint4(y0[0], y0[1], y0[2], y0[3]);
+    *reinterpret_cast<uint4*>(dst + kHalf + oct * 8) = make_uint4(y1[0], y1[1], y1[2], y1[3]);
   }
 }
 
@@ -177,12 +219,14 @@ __global__ void __launch_bounds__(256) rope_append_kernel(const RopeArgs a) {
 
 neo_status launch_rope_append(uint16_t* q, int32_t hq, const float* inv_freq, uint16_t* k, uint16_t* v,
                               int64_t page_stride, const int32_t* block_table, int32_t max_blocks,
-                              const int32_t* seq_lens, const uint16_t* k_new, const uint16_t* v_new, int32_t batch,
-                              int32_t hkv, int32_t page_size, cudaStream_t s) {
-  RopeArgs a{q, inv_freq, k, v, k_new, v_new, block_table, seq_lens, page_stride, max_blocks, hq, hkv, page_size};
+                              const int32_t* seq_lens, const int32_t* q_offsets, const uint16_t* k_new,
+                              const uint16_t* v_new, int32_t batch, int32_t tokens, int32_t hkv, int32_t page_size,
+                              cudaStream_t s) {
+  RopeArgs a{q,         inv_freq, k,     v,          k_new, v_new, block_table, seq_lens,
+             q_offsets, page_stride, batch, max_blocks, hq,    hkv,   page_size};
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(batch);
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3(tokens);
+  cfg.blockDim = dim3(128);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -26,7 +26,7 @@ EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_c
             "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
             "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
             "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
-            "neo_kv_append", "neo_schedule", "neo_rope_append"]
+            "neo_kv_append", "neo_schedule", "neo_rope_append", "neo_prefill_append", "neo_prefill_attn"]
 
 
 class NeoError(RuntimeError):
@@ -73,6 +73,9 @@ def lib() -> ctypes.CDLL:
                 "neo_kv_append": [P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
                 "neo_schedule": [P, P, i32, i64, i64, P, P, P, P, P],
                 "neo_rope_append": [P, i32, P, P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
+                "neo_prefill_attn": [P, P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, i32, i32, i32,
+                                     ctypes.c_float, P],
+                "neo_prefill_append": [P, i32, P, P, P, i64, i64, P, i32, P, P, P, P, i32, i32, i32, i32, i32, P],
             }
             for name, args in sig.items():
                 if os.environ.get("NEO_LIB") and not hasattr(L, name):
@@ -212,6 +215,59 @@ def rope_append(q, inv_freq, k_pages, v_pages, block_table, seq_lens, k_new, v_n
                                 v_pages.data_ptr(), k_pages.stride(0), int(num_pages if num_pages is not None else npages),
                                 block_table.data_ptr(), block_table.shape[1], seq_lens.data_ptr(), k_new.data_ptr(),
                                 v_new.data_ptr(), q.shape[0], hkv, d, P, _stream(stream)))
+
+
+def prefill_attn(q, k_pages, v_pages, block_table, seq_lens, q_offsets, max_q_len, out=None, scale=None,
+                 stream=None, num_pages=None):
+    """neo_prefill_attn: causal attention of the packed prompt-chunk rows q
+    [T][Hq][D] (bf16, cuda) over each request's paged KV; q_offsets [B+1] int32."""
+    import torch
+    for name, t in (("q", q), ("k_pages", k_pages), ("v_pages", v_pages), ("block_table", block_table),
+                    ("seq_lens", seq_lens), ("q_offsets", q_offsets)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if q.dtype != torch.bfloat16 or not q.is_contiguous():
+        raise ValueError("q must be contiguous bf16")
+    if q_offsets.dtype != torch.int32 or seq_lens.dtype != torch.int32 or block_table.dtype != torch.int32:
+        raise ValueError("q_offsets, seq_lens and block_table must be int32")
+    T, hq, d = q.shape
+    npages, hkv, P, _ = k_pages.shape
+    if k_pages.stride()[1:] != (P * d, d, 1) or v_pages.stride() != k_pages.stride():
+        raise ValueError("each page's [Hkv][P][D] block must be contiguous, K and V alike")
+    if out is None:
+        out = torch.empty_like(q)
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    check(lib().neo_prefill_attn(q.data_ptr(), k_pages.data_ptr(), v_pages.data_ptr(), k_pages.stride(0),
+                                 int(num_pages if num_pages is not None else npages), block_table.data_ptr(),
+                                 block_table.shape[1], seq_lens.data_ptr(), q_offsets.data_ptr(), out.data_ptr(),
+                                 seq_lens.shape[0], T, hq, hkv, d, P, int(max_q_len), float(scale), _stream(stream)))
+    return out
+
+
+def prefill_append(k_pages, v_pages, block_table, seq_lens, q_offsets, k_new, v_new, q=None, inv_freq=None,
+                   stream=None, num_pages=None):
+    """neo_prefill_append: store the packed prompt-chunk rows k_new/v_new
+    [T][Hkv][D] at the last q_len_b positions of each request (q_offsets [B+1]
+    int32 cuda); with inv_freq, q [T][Hq][D] and k are RoPE-rotated first."""
+    import torch
+    for name, t in (("k_pages", k_pages), ("v_pages", v_pages), ("block_table", block_table), ("seq_lens", seq_lens),
+                    ("q_offsets", q_offsets), ("k_new", k_new), ("v_new", v_new)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if q_offsets.dtype != torch.int32 or not q_offsets.is_contiguous():
+        raise ValueError("q_offsets must be contiguous int32")
+    if k_new.dtype != torch.bfloat16 or not k_new.is_contiguous() or not v_new.is_contiguous():
+        raise ValueError("k_new / v_new must be contiguous bf16")
+    if inv_freq is not None and (q is None or not q.is_cuda or not q.is_contiguous() or inv_freq.dtype != torch.float32):
+        raise ValueError("RoPE needs a contiguous cuda q and a float32 inv_freq")
+    npages, hkv, P, d = k_pages.shape
+    check(lib().neo_prefill_append(q.data_ptr() if q is not None else None, q.shape[1] if q is not None else 0,
+                                   inv_freq.data_ptr() if inv_freq is not None else None, k_pages.data_ptr(),
+                                   v_pages.data_ptr(), k_pages.stride(0),
+                                   int(num_pages if num_pages is not None else npages), block_table.data_ptr(),
+                                   block_table.shape[1], seq_lens.data_ptr(), q_offsets.data_ptr(), k_new.data_ptr(),
+                                   v_new.data_ptr(), seq_lens.shape[0], k_new.shape[0], hkv, d, P, _stream(stream)))
 
 
 # ------------------------------------------------------------------ scheduler

@@ -93,3 +93,39 @@ class Case:
     def oracle(self, b):
         import oracle
         return oracle.decode_attention(self.q[b], self.k_req[b], self.v_req[b], np.float32(self.scale))
+
+
+class PrefillCase(Case):
+    """Prompt chunks: request b's last q_lens[b] tokens (of ctx[b]) are the query
+    rows, packed as q [T][Hq][D] with offsets q_off [B+1]; the pool already holds
+    all ctx[b] tokens (as neo_prefill_append leaves it)."""
+
+    def __init__(self, ctx, q_lens, hq, hkv, **kw):
+        import torch
+        super().__init__(ctx, hq, hkv, **kw)
+        self.q_lens = np.asarray(q_lens, dtype=np.int32)
+        assert np.all(self.q_lens <= self.ctx) and np.all(self.q_lens >= 0)
+        self.q_off = np.zeros(self.B + 1, dtype=np.int32)
+        self.q_off[1:] = np.cumsum(self.q_lens)
+        self.T = int(self.q_off[-1])
+        self.max_q_len = max(int(self.q_lens.max()) if self.B else 0, 1)
+        # per-token q rows: global token ids offset so they never collide with decode q rows
+        self.qp = ni.q_bits(self.seed, self.layer, np.arange(self.T) + 1_000_000 + 4096 * self.b_offset, hq, D,
+                            variant=self.variant)
+        self.qp_dev = torch.from_numpy(self.qp.view(np.int16)).cuda().view(torch.bfloat16)
+        self.qo_dev = torch.from_numpy(self.q_off).cuda()
+
+    def run(self, out=None, scale=None):
+        from paper_2411_01142_b200 import neo
+        import torch
+        o = neo.prefill_attn(self.qp_dev, self.k_dev, self.v_dev, self.bt_dev, self.sl_dev, self.qo_dev,
+                             self.max_q_len, out=out, scale=self.scale if scale is None else scale)
+        torch.cuda.synchronize()
+        return o
+
+    def rows(self, b):
+        return slice(int(self.q_off[b]), int(self.q_off[b + 1]))
+
+    def oracle(self, b):
+        import oracle
+        return oracle.prefill_attention(self.qp[self.rows(b)], self.k_req[b], self.v_req[b], np.float32(self.scale))

@@ -1,0 +1,121 @@
+"""GPU parity of the prefill side of batch-0 through
+the C ABI: neo_prefill_append (ragged multi-token KV store, optional RoPE)
+against the fp64 RoPE oracle / bit copies, and neo_prefill_attn against the
+fp64 causal prefill oracle under the north-star tolerance rule."""
+import numpy as np
+import pytest
+
+import neo_inputs as ni
+from harness import PrefillCase, within_tol
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2411_01142_b200 import build
+    build.build()
+
+
+def _page_row(dev, case, b, t):
+    P = case.P
+    import torch
+    return dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("rope", [False, True])
+def test_prefill_append(rope):
+    import torch
+    from oracle import rope as orope
+    from paper_2411_01142_b200 import neo
+    ctx = [1, 40, 300, 129, 1000, 17]
+    q_lens = [1, 40, 100, 1, 1000, 0]          # whole prompts, a chunk after a prefix, single tokens, empty
+    case = PrefillCase(ctx, q_lens, 32, 8, seed=91 + rope)
+    f = orope.llama_inv_freq()
+    k_new = np.concatenate([case.k_req[b][n - m:] for b, (n, m) in enumerate(zip(ctx, q_lens))])
+    v_new = np.concatenate([case.v_req[b][n - m:] for b, (n, m) in enumerate(zip(ctx, q_lens))])
+    for b, (n, m) in enumerate(zip(ctx, q_lens)):              # poison the slots the store fills
+        for t in range(n - m, n):
+            case.k_dev[case.table[b, t // case.P], :, t % case.P] = float("nan")
+            case.v_dev[case.table[b, t // case.P], :, t % case.P] = float("nan")
+    kn = torch.from_numpy(k_new.view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(v_new.view(np.int16)).cuda().view(torch.bfloat16)
+    q = case.qp_dev.clone()
+    neo.prefill_append(case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.qo_dev, kn, vn,
+                       q=q if rope else None, inv_freq=torch.from_numpy(f).cuda() if rope else None)
+    torch.cuda.synchronize()
+    q_got = q.view(torch.int16).cpu().numpy().view(np.uint16)
+    if not rope:
+        assert np.array_equal(q_got, case.qp)
+    for b, (n, m) in enumerate(zip(ctx, q_lens)):
+        for i, t in enumerate(range(n - m, n)):
+            j = case.q_off[b] + i
+            assert np.array_equal(_page_row(case.v_dev, case, b, t), case.v_req[b][t])
+            kg = _page_row(case.k_dev, case, b, t)
+            if not rope:
+                assert np.array_equal(kg, case.k_req[b][t])
+                continue
+            assert within_tol(ni.bf16_bits_to_f64(kg), orope.rope(ni.bf16_bits_to_f64(case.k_req[b][t]), t, f))[0]
+            assert within_tol(ni.bf16_bits_to_f64(q_got[j]), orope.rope(ni.bf16_bits_to_f64(case.qp[j]), t, f))[0]
+
+
+def check_prefill(case, tag=""):
+    out = case.run()
+    got = ni.bf16_bits_to_f64(out.view(__import__("torch").int16).cpu().numpy().view(np.uint16))
+    worst = 0.0
+    for b in range(case.B):
+        if case.q_lens[b] == 0:
+            continue
+        ok, ratio = within_tol(got[case.rows(b)], case.oracle(b))
+        worst = max(worst, ratio)
+        assert ok, f"{tag} b={b} ctx={case.ctx[b]} q_len={case.q_lens[b]} err/tol={ratio:.3f}"
+    return out, worst
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (8, 8), (16, 8), (64, 8), (16, 1)])
+def test_prefill_parity_whole_prompts(hq, hkv):
+    ctx = [1, 7, 64, 65, 128, 300, 1000]
+    check_prefill(PrefillCase(ctx, ctx, hq, hkv, seed=100 + hq + hkv), f"hq={hq} hkv={hkv}")
+
+
+@pytest.mark.parametrize("P", [16, 32, 64])
+def test_prefill_parity_chunks_after_prefix(P):
+    ctx = [500, 200, 129, 64, 1500, 33]
+    q_lens = [100, 1, 64, 0, 257, 33]        # chunked prefill after a cached prefix, a single token, an empty slot
+    check_prefill(PrefillCase(ctx, q_lens, 32, 8, P=P, seed=200 + P), f"P={P}")
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_prefill_parity_variants(variant):
+    ctx = [700, 96, 1200]
+    check_prefill(PrefillCase(ctx, [700, 50, 300], 32, 8, variant=variant, seed=300 + variant), f"variant={variant}")
+
+
+def test_prefill_determinism_and_nan_tails():
+    import torch
+    ctx = [77, 1000, 513]
+    case = PrefillCase(ctx, ctx, 32, 8, seed=400)            # page tails are NaN-poisoned by the harness
+    a = case.run().clone()
+    b = case.run()
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    assert torch.isfinite(a.float()).all()
+
+
+def test_prefill_last_row_matches_decode():
+    """The last prompt row at position n-1 is exactly a decode query over all n tokens:
+    prefill and decode kernels agree within the tolerance on it."""
+    import torch
+    from paper_2411_01142_b200 import neo
+    ctx = [300, 1024, 77]
+    case = PrefillCase(ctx, ctx, 32, 8, seed=500)
+    out = case.run()
+    last = torch.stack([case.qp_dev[case.q_off[b + 1] - 1] for b in range(case.B)]).contiguous()
+    dec = neo.decode_attn(last, case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.max_seq_len)
+    torch.cuda.synchronize()
+    for b in range(case.B):
+        a = ni.bf16_bits_to_f64(out[case.q_off[b + 1] - 1].view(torch.int16).cpu().numpy().view(np.uint16))
+        d = ni.bf16_bits_to_f64(dec[b].view(torch.int16).cpu().numpy().view(np.uint16))
+        assert within_tol(a, d)[0]
