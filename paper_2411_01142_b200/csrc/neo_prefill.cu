@@ -1,24 +1,30 @@
 // Causal paged GQA prefill attention for sm_100a on the 5th-generation tensor
 // cores (the prefill half of batch-0).
 //
-// CTA = (request b, kv-head g, M tile of 128 query rows).  Row r of the tile is
-// (query token i0 + r / G, q-head g*G + r % G): the G heads sharing a KV head
-// are packed into the M dimension so each K/V tile is read once per M tile.
-// Key tiles of kBN = 64 tokens stream through a kStages-deep TMA ring straight
-// from the KV pages (one 2 KiB box per 16 tokens and dim-half).
+// CTA = (request b, kv-head g, two M tiles of 128 query rows).  Row r of a tile
+// is (query token, q-head g*G + r % G): the G heads sharing a KV head are packed
+// into M, so each K/V tile is read once for 2 x 128 rows.  Key tiles of kBN =
+// 128 tokens stream through a 2-stage TMA ring straight from the KV pages (one
+// 2 KiB box per 16 tokens and dim-half).
 //
-//   warp 4     TMA producer: Q once, then K and V tiles (block-table lookups)
-//   warp 5     TMEM owner + MMA issuer (one lane):
-//                S_j  = Q . K_j^T          tcgen05.mma M128 N64  K128 -> TMEM (2 buffers)
-//                O   += P_j . V_j          tcgen05.mma M128 N128 K64  -> TMEM, P = hi + lo
-//   warps 0-3  softmax: thread r owns row r (TMEM lane r): scores via tcgen05.ld,
-//              causal mask, online softmax in the exp2 domain with a lazy
-//              rescale (only when the row max grows by > 2^8), P written to
-//              shared memory as bf16 hi + lo parts (two MMAs keep ~16 mantissa
-//              bits of P, the SURVEY §8(c) rule), O rescaled in TMEM when needed,
-//              final O / l stored as bf16.
-// S_{j+1} runs on the tensor core while the softmax warps work on S_j; P is
-// double-buffered so PV_j overlaps softmax j+1.
+//   warp 8     TMA producer: Q once, then K and V tiles (block-table lookups)
+//   warp 9     TMEM owner + MMA issuer (one lane), ping-pong over the two tiles:
+//                S_j(t)  = Q_t . K_j^T     tcgen05.mma SS  M128 N128 K128 -> TMEM
+//                O(t)   += P_j(t) . V_j    tcgen05.mma TS  M128 N128 K128, P read
+//                                          from TMEM (aliasing S_j(t)), hi + lo
+//              issue order PV_j(0) S_j+1(0) PV_j(1) S_j+1(1): the tensor core runs
+//              one tile's PV + next S while the other tile's softmax runs.
+//   warps 0-3  softmax of tile 0, warps 4-7 of tile 1: thread = row = TMEM lane.
+//              Scores via tcgen05.ld, causal mask, online softmax in the exp2
+//              domain (scale folded into one FFMA) with a lazy rescale (only
+//              when the row max grows by > 2^8; O rescaled in TMEM), P split into
+//              bf16 hi + lo by truncation (hi = top 16 bits, lo = top 16 bits
+//              of the exact remainder: ~16 significant bits, the SURVEY §8(c)
+//              rule for P.V on tensor cores) and written back over S with
+//              tcgen05.st; final O / l stored as bf16.
+// tcgen05 ops of the issuing thread complete in order, so the commit that
+// signals S_j+1(t) also proves PV_j(t) done: the softmax may rescale O then,
+// and S_j+1(t) may overwrite P_j(t) without further barriers.
 #include <cuda_bf16.h>
 
 #include <cstdio>
@@ -29,28 +35,28 @@
 namespace neo {
 namespace {
 
-constexpr int kBM = 128;                        // query rows per CTA (TMEM lanes)
-constexpr int kBN = 64;                         // keys per tile
-constexpr int kStages = 3;                      // K/V ring depth
-constexpr int kQHalf = kBM * 128;               // 16 KiB: one dim-half of Q
-constexpr int kKVHalf = kBN * 128;              // 8 KiB: one dim-half of a K or V tile
-constexpr int kKVBytes = 2 * kKVHalf;
-constexpr int kPBytes = kBM * kBN * 2;          // 16 KiB: P hi (or lo) of one tile
-constexpr int kOffK = 2 * kQHalf;
-constexpr int kOffV = kOffK + kStages * kKVBytes;
-constexpr int kOffP = kOffV + kStages * kKVBytes;
-constexpr int kSmemBytes = kOffP + 2 * 2 * kPBytes;   // 192 KiB
-constexpr int kSmemAlloc = kSmemBytes + 1024;          // + alignment slack
-constexpr uint32_t kTmemCols = 256;                    // S[2] (2 x 64) + O (128)
-constexpr uint32_t kColO = 2 * kBN;
+constexpr int kBM = 128;                        // query rows per tile (TMEM lanes)
+constexpr int kTiles = 2;                       // tiles per CTA (ping-pong)
+constexpr int kBN = 128;                        // keys per tile
+constexpr int kStages = 2;                      // K/V ring depth
+constexpr int kQHalf = kBM * 128;               // 16 KiB: one dim-half of a Q tile
+constexpr int kKVHalf = kBN * 128;              // 16 KiB: one dim-half of a K or V tile
+constexpr int kOffK = kTiles * 2 * kQHalf;      // 64 KiB of Q
+constexpr int kStageBytes = 4 * kKVHalf;        // K then V: 64 KiB
+constexpr int kSmemBytes = kOffK + kStages * kStageBytes;   // 192 KiB
+constexpr int kSmemAlloc = kSmemBytes + 1024;               // + alignment slack
+constexpr uint32_t kTmemCols = 512;             // per tile: S/P (128) + O (128)
+constexpr uint32_t kTileCols = 256;
+constexpr uint32_t kColO = 128;
 constexpr uint32_t kIdescS = umma::idesc_bf16_f32(kBM, kBN, false, false);
 constexpr uint32_t kIdescO = umma::idesc_bf16_f32(kBM, 128, false, true);
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;
+constexpr int kProducerWarp = 8, kMmaWarp = 9;
 
 // barrier slots
 constexpr int kBarQ = 0, kBarKFull = 1, kBarVFull = kBarKFull + kStages, kBarKVEmpty = kBarVFull + kStages,
-              kBarSFull = kBarKVEmpty + kStages, kBarSFree = kBarSFull + 2, kBarPFull = kBarSFree + 2,
-              kBarPVDone = kBarPFull + 2, kNumBars = kBarPVDone + 2;
+              kBarSFull = kBarKVEmpty + kStages, kBarPFull = kBarSFull + kTiles, kBarODone = kBarPFull + kTiles,
+              kNumBars = kBarODone + kTiles;
 
 struct PArgs {
   uint16_t* out;
@@ -112,8 +118,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
-__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -132,13 +136,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int q0 = a.q_offsets[b];
   const int q_len = a.q_offsets[b + 1] - q0;
-  const int n_mt = (q_len + rows_tok - 1) / rows_tok;
-  const int mt = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);   // longest tiles first
-  if (mt >= n_mt) return;
+  const int n_ct = (q_len + kTiles * rows_tok - 1) / (kTiles * rows_tok);
+  const int ct = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);   // longest CTAs first
+  if (ct >= n_ct) return;
   const int ctx = a.seq_lens[b];
-  const int i0 = mt * rows_tok;
-  const int pos_last = ctx - q_len + min(i0 + rows_tok, q_len) - 1;
-  const int nt = pos_last / kBN + 1;
+  const int i0 = ct * kTiles * rows_tok;
+  // key tiles each M tile needs (0: the tile holds no query row)
+  auto tiles_of = [&](int t) {
+    const int first = i0 + t * rows_tok;
+    return first < q_len ? (ctx - q_len + min(first + rows_tok, q_len) - 1) / kBN + 1 : 0;
+  };
+  const int nt0 = tiles_of(0), nt1 = tiles_of(1);
+  const int nt = max(nt0, nt1);
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
@@ -152,15 +161,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(kBarVFull + s), 1);
       mbar_init(bar(kBarKVEmpty + s), 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(kBarSFull + i), 1);
-      mbar_init(bar(kBarSFree + i), 4);
-      mbar_init(bar(kBarPFull + i), 4);
-      mbar_init(bar(kBarPVDone + i), 1);
+    for (int t = 0; t < kTiles; ++t) {
+      mbar_init(bar(kBarSFull + t), 1);
+      mbar_init(bar(kBarPFull + t), 4);
+      mbar_init(bar(kBarODone + t), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     umma::tmem_alloc(smem_u32(&tmem_sh), kTmemCols);
     umma::tmem_relinquish();
   }
@@ -169,207 +177,229 @@ __global__ void __launch_bounds__(kThreads, 1)
   umma::fence_after_sync();
   const uint32_t tmem = tmem_sh;
 
-  if (warp == 4) {
+  if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
-      mbar_expect_tx(bar(kBarQ), 2 * kQHalf);
-      for (int h = 0; h < 2; ++h) tma_load_4d(sb + h * kQHalf, &tmq, 0, g * G, q0 + i0, h, bar(kBarQ));
-      const int32_t* bt = a.block_table + static_cast<int64_t>(b) * a.max_blocks;
-      for (int j = 0; j < nt; ++j) {
-        const int st = j % kStages;
-        if (j >= kStages) mbar_wait(bar(kBarKVEmpty + st), ((j / kStages) - 1) & 1);
-        const int kv0 = j * kBN;
-        const int groups = min(kBN / 16, (ctx - kv0 + 15) / 16);
-        const uint32_t bytes = static_cast<uint32_t>(groups) * 2 * 2048;
-        int page[kBN / 16], slot[kBN / 16];
-        for (int u = 0; u < groups; ++u) {
-          const int t = kv0 + 16 * u;
-          page[u] = bt[t / a.page_size];
-          slot[u] = t % a.page_size;
-        }
-        const uint32_t dk = sb + kOffK + st * kKVBytes, dv = sb + kOffV + st * kKVBytes;
-        mbar_expect_tx(bar(kBarKFull + st), bytes);
-        for (int u = 0; u < groups; ++u)
-          for (int h = 0; h < 2; ++h)
-            tma_load_5d(dk + h * kKVHalf + u * 2048, &tmk, 0, slot[u], h, g, page[u], bar(kBarKFull + st));
-        mbar_expect_tx(bar(kBarVFull + st), bytes);
-        for (int u = 0; u < groups; ++u)
-          for (int h = 0; h < 2; ++h)
-            tma_load_5d(dv + h * kKVHalf + u * 2048, &tmv, 0, slot[u], h, g, page[u], bar(kBarVFull + st));
-      }
+      const int nq = nt1 > 0 ? 2 : 1;
+      mbar_expect_tx(bar(kBarQ), nq * 2 * kQHalf);
+      for (int t = 0; t < nq; ++t)
+        for (int h = 0; h < 2; ++h)
+          tma_load_4d(sb + (t * 2 + h) * kQHalf, &tmq, 0, g * G, q0 + i0 + t * rows_tok, h, bar(kBarQ));
     }
-  } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issuer
-    mbar_wait(bar(kBarQ), 0);
-    umma::fence_after_sync();
-    for (int j = 0; j <= nt; ++j) {
-      if (j < nt) {
-        const int st = j % kStages;
-        mbar_wait(bar(kBarKFull + st), (j / kStages) & 1);
-        if (j >= 2) mbar_wait(bar(kBarSFree + (j & 1)), ((j - 2) >> 1) & 1);
-        umma::fence_after_sync();
-        if (lane == 0) {
-          const uint32_t kb = sb + kOffK + st * kKVBytes;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t ad = umma::desc_sw128(sb + (kk >> 2) * kQHalf + (kk & 3) * 32, 16, 1024);
-            const uint64_t bd = umma::desc_sw128(kb + (kk >> 2) * kKVHalf + (kk & 3) * 32, 16, 1024);
-            umma::mma_bf16(tmem + (j & 1) * kBN, ad, bd, kIdescS, kk > 0);
-          }
-          umma::commit(bar(kBarSFull + (j & 1)));
-        }
-        __syncwarp();
+    const int32_t* bt = a.block_table + static_cast<int64_t>(b) * a.max_blocks;
+    for (int j = 0; j < nt; ++j) {
+      const int st = j % kStages;
+      const int kv0 = j * kBN;
+      const int groups = min(kBN / 16, (ctx - kv0 + 15) / 16);
+      int page = 0, slot = 0;
+      if (lane < groups) {                       // lane u: page and slot of token group u
+        const int t = kv0 + 16 * lane;
+        page = bt[t / a.page_size];
+        slot = t % a.page_size;
       }
-      if (j >= 1) {
-        const int i = j - 1, st = i % kStages;
-        mbar_wait(bar(kBarPFull + (i & 1)), (i >> 1) & 1);
-        mbar_wait(bar(kBarVFull + st), (i / kStages) & 1);
-        const int nvalid = min(kBN, ctx - i * kBN);
-        const int ksteps = (nvalid + 15) / 16;
-        const uint32_t vb = sb + kOffV + st * kKVBytes;
-        if (nvalid & 15) {
-          // rows nvalid .. 16*ksteps-1 hold page-tail slots: zero them (P is 0
-          // there, but 0 * NaN would poison O)
-          const int r0 = nvalid, nrows = 16 * ksteps - nvalid;
-          for (int e = lane; e < nrows * 2 * 8; e += 32) {
-            const int row = r0 + e / 16, h = (e / 8) & 1, c = e & 7;
-            sts128(vb + h * kKVHalf + row * 128 + c * 16, 0, 0, 0, 0);
-          }
-          umma::fence_proxy_async_smem();
+      if (j >= kStages) mbar_wait(bar(kBarKVEmpty + st), ((j / kStages) - 1) & 1);
+      const uint32_t dk = sb + kOffK + st * kStageBytes, dv = dk + 2 * kKVHalf;
+      const uint32_t bytes = static_cast<uint32_t>(groups) * 2 * 2048;
+      if (lane == 0) mbar_expect_tx(bar(kBarKFull + st), bytes);
+      __syncwarp();
+      if (lane < groups)
+        for (int h = 0; h < 2; ++h)
+          tma_load_5d(dk + h * kKVHalf + lane * 2048, &tmk, 0, slot, h, g, page, bar(kBarKFull + st));
+      if (lane == 0) mbar_expect_tx(bar(kBarVFull + st), bytes);
+      __syncwarp();
+      if (lane < groups)
+        for (int h = 0; h < 2; ++h)
+          tma_load_5d(dv + h * kKVHalf + lane * 2048, &tmv, 0, slot, h, g, page, bar(kBarVFull + st));
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    auto issue_s = [&](int t, int st) {
+      const uint32_t kb = sb + kOffK + st * kStageBytes;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t ad = umma::desc_sw128(sb + (t * 2 + (kk >> 2)) * kQHalf + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = umma::desc_sw128(kb + (kk >> 2) * kKVHalf + (kk & 3) * 32, 16, 1024);
+        umma::mma_bf16(tmem + t * kTileCols, ad, bd, kIdescS, kk > 0);
+      }
+    };
+    mbar_wait(bar(kBarQ), 0);
+    mbar_wait(bar(kBarKFull), 0);
+    umma::fence_after_sync();
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < kTiles; ++t)
+        if ((t ? nt1 : nt0) > 0) {
+          issue_s(t, 0);
+          umma::commit(bar(kBarSFull + t));
         }
-        __syncwarp();
+    }
+    __syncwarp();
+    for (int j = 0; j < nt; ++j) {
+      const int st = j % kStages;
+      mbar_wait(bar(kBarVFull + st), (j / kStages) & 1);
+      const int nvalid = min(kBN, ctx - j * kBN);
+      const int ksteps = (nvalid + 15) / 16;
+      const uint32_t vb = sb + kOffK + st * kStageBytes + 2 * kKVHalf;
+      if (nvalid & 15) {
+        // rows nvalid .. 16*ksteps-1 hold page-tail slots: zero them (P is 0
+        // there, but 0 * NaN would poison O)
+        const int nrows = 16 * ksteps - nvalid;
+        for (int e = lane; e < nrows * 2 * 8; e += 32) {
+          const int row = nvalid + e / 16, h = (e / 8) & 1, c = e & 7;
+          sts128(vb + h * kKVHalf + row * 128 + c * 16, 0, 0, 0, 0);
+        }
+        umma::fence_proxy_async_smem();
+      }
+      __syncwarp();
+      bool next_ready = false;
+#pragma unroll
+      for (int t = 0; t < kTiles; ++t) {
+        const int ntt = t ? nt1 : nt0;
+        if (j >= ntt) continue;
+        mbar_wait(bar(kBarPFull + t), j & 1);
+        const bool more = j + 1 < ntt;
+        if (more && !next_ready) {
+          mbar_wait(bar(kBarKFull + (j + 1) % kStages), ((j + 1) / kStages) & 1);
+          next_ready = true;
+        }
         umma::fence_after_sync();
         if (lane == 0) {
-          const uint32_t pb = sb + kOffP + (i & 1) * 2 * kPBytes;
+          const uint32_t tp = tmem + t * kTileCols;
           for (int k = 0; k < ksteps; ++k) {
             const uint64_t vd = umma::desc_sw128(vb + k * 2048, kKVHalf, 1024);
-            const uint64_t ph = umma::desc_sw128(pb + k * 32, 16, 1024);
-            const uint64_t pl = umma::desc_sw128(pb + kPBytes + k * 32, 16, 1024);
-            umma::mma_bf16(tmem + kColO, ph, vd, kIdescO, i > 0 || k > 0);
-            umma::mma_bf16(tmem + kColO, pl, vd, kIdescO, true);
+            umma::mma_bf16_ts(tp + kColO, tp + k * 8, vd, kIdescO, j > 0 || k > 0);
+            umma::mma_bf16_ts(tp + kColO, tp + 64 + k * 8, vd, kIdescO, true);
           }
-          umma::commit(bar(kBarPVDone + (i & 1)));
-          umma::commit(bar(kBarKVEmpty + st));
+          if (more) {
+            issue_s(t, (j + 1) % kStages);
+            umma::commit(bar(kBarSFull + t));
+          } else {
+            umma::commit(bar(kBarODone + t));
+          }
         }
         __syncwarp();
       }
+      if (lane == 0) umma::commit(bar(kBarKVEmpty + st));
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    const int r = threadIdx.x;                      // row == TMEM lane
-    const int i_row = i0 + r / G;
-    const bool valid_row = i_row < q_len;
-    const int pos = ctx - q_len + min(i_row, q_len - 1);
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-    const float sl = a.scale_log2;
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < nt; ++j) {
-      mbar_wait(bar(kBarSFull + (j & 1)), (j >> 1) & 1);
-      umma::fence_after_sync();
-      uint32_t s0[32], s1[32];
-      umma::ld32(tmem + lane_base + (j & 1) * kBN, s0);
-      umma::ld32(tmem + lane_base + (j & 1) * kBN + 32, s1);
-      umma::wait_ld();
-      umma::fence_before_sync();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(kBarSFree + (j & 1)));
-
-      const int kv0 = j * kBN;
-      float x[kBN];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        x[c] = __uint_as_float(s0[c]) * sl;
-        x[c + 32] = __uint_as_float(s1[c]) * sl;
-      }
-      if (kv0 + kBN - 1 > pos) {
-#pragma unroll
-        for (int c = 0; c < kBN; ++c)
-          if (kv0 + c > pos) x[c] = -INFINITY;
-      }
-      float mx = x[0];
-#pragma unroll
-      for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, x[c]);
-      const float m_new = fmaxf(m_ref, mx);
-      bool resc = false;
-      float alpha = 1.f;
-      if (j == 0) {
-        m_ref = m_new;
-      } else if (m_new > m_ref + 8.f) {
-        resc = true;
-        alpha = ex2(m_ref - m_new);
-        m_ref = m_new;
-        l *= alpha;
-      }
-      if (j >= 2) mbar_wait(bar(kBarPVDone + (j & 1)), ((j - 2) >> 1) & 1);   // P buffer free
-      const uint32_t pb = sb + kOffP + (j & 1) * 2 * kPBytes;
-#pragma unroll
-      for (int c8 = 0; c8 < kBN / 8; ++c8) {
-        uint32_t hw[4], lw[4];
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const float p0 = ex2(x[c8 * 8 + 2 * w] - m_ref);
-          const float p1 = ex2(x[c8 * 8 + 2 * w + 1] - m_ref);
-          l += p0 + p1;
-          hw[w] = pack_bf16(p0, p1);
-          lw[w] = pack_bf16(p0 - bf_lo(hw[w]), p1 - bf_hi(hw[w]));
-        }
-        const uint32_t off = umma::sw128_off(r, c8);
-        sts128(pb + off, hw[0], hw[1], hw[2], hw[3]);
-        sts128(pb + kPBytes + off, lw[0], lw[1], lw[2], lw[3]);
-      }
-      umma::fence_proxy_async_smem();
-      if (__any_sync(0xffffffffu, resc)) {
-        // O must hold PV_{j-1} before it is scaled
-        mbar_wait(bar(kBarPVDone + ((j - 1) & 1)), ((j - 1) >> 1) & 1);
+    const int t = warp >> 2, quarter = warp & 3;
+    const int my_nt = t ? nt1 : nt0;
+    if (my_nt > 0) {
+      const int r = quarter * 32 + lane;             // row == TMEM lane
+      const int i_row = i0 + t * rows_tok + r / G;
+      const bool valid_row = i_row < q_len;
+      const int pos = ctx - q_len + min(i_row, q_len - 1);
+      const uint32_t tS = tmem + t * kTileCols + (static_cast<uint32_t>(quarter * 32) << 16);
+      const uint32_t tO = tS + kColO;
+      const float sl = a.scale_log2;
+      float m = -INFINITY, l0 = 0.f, l1 = 0.f;
+      for (int j = 0; j < my_nt; ++j) {
+        mbar_wait(bar(kBarSFull + t), j & 1);
         umma::fence_after_sync();
-#pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t o[32];
-          umma::ld32(tmem + lane_base + kColO + c0, o);
-          umma::wait_ld();
+        float s[kBN];
+        {
+          uint32_t u[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-          umma::st32(tmem + lane_base + kColO + c0, o);
+          for (int c0 = 0; c0 < kBN; c0 += 32) {
+            umma::ld32(tS + c0, u);
+            umma::wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) s[c0 + c] = __uint_as_float(u[c]);
+          }
+        }
+        const int kv0 = j * kBN;
+        if (kv0 + kBN - 1 > pos) {
+#pragma unroll
+          for (int c = 0; c < kBN; ++c)
+            if (kv0 + c > pos) s[c] = -INFINITY;
+        }
+        float mx = s[0];
+#pragma unroll
+        for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
+        const float m_new = fmaxf(m, mx);
+        bool resc = false;
+        float alpha = 1.f;
+        if (j == 0) {
+          m = m_new;
+        } else if ((m_new - m) * sl > 8.f) {
+          resc = true;
+          alpha = ex2((m - m_new) * sl);
+          l0 *= alpha;
+          l1 *= alpha;
+          m = m_new;
+        }
+        const float msl = m * sl;
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          uint32_t hw[16], lw[16];
+#pragma unroll
+          for (int w = 0; w < 16; ++w) {
+            const float p0 = ex2(fmaf(s[c0 + 2 * w], sl, -msl));
+            const float p1 = ex2(fmaf(s[c0 + 2 * w + 1], sl, -msl));
+            l0 += p0;
+            l1 += p1;
+            const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
+            hw[w] = __byte_perm(u0, u1, 0x7632);
+            const float r0 = p0 - __uint_as_float(u0 & 0xffff0000u);
+            const float r1 = p1 - __uint_as_float(u1 & 0xffff0000u);
+            lw[w] = __byte_perm(__float_as_uint(r0), __float_as_uint(r1), 0x7632);
+          }
+          umma::st16(tS + c0 / 2, hw);          // hi: columns [0, 64)
+          umma::st16(tS + 64 + c0 / 2, lw);     // lo: columns [64, 128)
+        }
+        if (__any_sync(0xffffffffu, resc)) {
+          // PV_{j-1} is complete (the S_j commit covers it): scale O in place
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t o[32];
+            umma::ld32(tO + c0, o);
+            umma::wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+            umma::st32(tO + c0, o);
+          }
         }
         umma::wait_st();
         umma::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(kBarPFull + t));
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(kBarPFull + (j & 1)));
-    }
-    // epilogue: O / l -> bf16
-    mbar_wait(bar(kBarPVDone + ((nt - 1) & 1)), ((nt - 1) >> 1) & 1);
-    umma::fence_after_sync();
-    const float inv_l = 1.f / l;
-    uint16_t* orow = a.out + (static_cast<int64_t>(q0 + min(i_row, q_len - 1)) * a.hq + g * G + r % G) * 128;
+      // epilogue: O / l -> bf16
+      mbar_wait(bar(kBarODone + t), 0);
+      umma::fence_after_sync();
+      const float inv_l = 1.f / (l0 + l1);
+      uint16_t* orow = a.out + (static_cast<int64_t>(q0 + min(i_row, q_len - 1)) * a.hq + g * G + r % G) * 128;
 #pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 32) {
-      uint32_t o[32];
-      umma::ld32(tmem + lane_base + kColO + c0, o);
-      umma::wait_ld();
-      if (valid_row) {
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t o[32];
+        umma::ld32(tO + c0, o);
+        umma::wait_ld();
+        if (valid_row) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 8) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(o[c + 0]) * inv_l, __uint_as_float(o[c + 1]) * inv_l);
-          v.y = pack_bf16(__uint_as_float(o[c + 2]) * inv_l, __uint_as_float(o[c + 3]) * inv_l);
-          v.z = pack_bf16(__uint_as_float(o[c + 4]) * inv_l, __uint_as_float(o[c + 5]) * inv_l);
-          v.w = pack_bf16(__uint_as_float(o[c + 6]) * inv_l, __uint_as_float(o[c + 7]) * inv_l);
-          *reinterpret_cast<uint4*>(orow + c0 + c) = v;
+          for (int c = 0; c < 32; c += 8) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[c + 0]) * inv_l, __uint_as_float(o[c + 1]) * inv_l);
+            v.y = pack_bf16(__uint_as_float(o[c + 2]) * inv_l, __uint_as_float(o[c + 3]) * inv_l);
+            v.z = pack_bf16(__uint_as_float(o[c + 4]) * inv_l, __uint_as_float(o[c + 5]) * inv_l);
+            v.w = pack_bf16(__uint_as_float(o[c + 6]) * inv_l, __uint_as_float(o[c + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + c0 + c) = v;
+          }
         }
       }
     }
   }
   umma::fence_before_sync();
   __syncthreads();
-  if (warp == 5) umma::tmem_dealloc(tmem, kTmemCols);
+  if (warp == kMmaWarp) umma::tmem_dealloc(tmem, kTmemCols);
 }
 
 }  // namespace
 
-int prefill_m_tiles(int32_t max_q_len, int32_t G) { return (max_q_len * G + kBM - 1) / kBM; }
+int prefill_ctas(int32_t max_q_len, int32_t G) { return (max_q_len * G + kTiles * kBM - 1) / (kTiles * kBM); }
 
 neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, const CUtensorMap& tmk,
                                const CUtensorMap& tmv) {
@@ -383,7 +413,7 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   PArgs a{static_cast<uint16_t*>(L.out), L.block_table, L.seq_lens, L.q_offsets, L.hq, G, L.page_size, L.max_blocks,
           L.scale * 1.4426950408889634f};
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(prefill_m_tiles(L.max_q_len, G), L.hkv, L.batch);
+  cfg.gridDim = dim3(prefill_ctas(L.max_q_len, G), L.hkv, L.batch);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemAlloc;
   cfg.stream = L.stream;

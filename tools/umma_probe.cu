@@ -1,6 +1,7 @@
 // Probe of the tcgen05 encodings in paper_2411_01142_b200/csrc/umma.cuh on a B200:
 //   mode 0: D[128 x N] = A[128 x 128] . B[N x 128]^T   (A, B K-major SW128)  N in {64, 128, 256}
 //   mode 1: D[128 x 128] = P[128 x 128] . V[128 x 128]  (P K-major, V MN-major SW128)
+//   mode 2: as mode 1 with P in TMEM (written by tcgen05.st, lane = row, column c = pair 2c, 2c+1)
 // Operands are written into shared memory with TMA's SWIZZLE_128B pattern by
 // plain stores, then a single thread issues the MMAs; the 4 warps read the
 // accumulator back with tcgen05.ld 32x32b and the host compares with fp64.
@@ -41,7 +42,7 @@ __global__ void probe(const uint16_t* a, const uint16_t* b, float* d, int mode, 
       const uint32_t off = (k / 64) * (N * 128) + umma::sw128_off(r, (k % 64) / 8) + (k % 8) * 2;
       *reinterpret_cast<uint16_t*>(sb + off) = b[i];
     }
-  } else {  // V: 128 K rows (tokens) x 128 N (dims), MN-major: dim half h at h * 16 KiB
+  } else {  // V (modes 1, 2): 128 K rows (tokens) x 128 N (dims), MN-major: dim half h at h * 16 KiB
     for (int i = tid; i < 128 * 128; i += blockDim.x) {
       const int t = i / 128, n = i % 128;
       const uint32_t off = (n / 64) * 16384 + umma::sw128_off(t, (n % 64) / 8) + (n % 8) * 2;
@@ -61,6 +62,20 @@ __global__ void probe(const uint16_t* a, const uint16_t* b, float* d, int mode, 
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tm = tbase;
+  if (mode == 2) {  // P rows into TMEM columns 128.. (64 columns of bf16 pairs), one row per lane
+    const int row = warp * 32 + (tid & 31);
+    for (int c0 = 0; c0 < 64; c0 += 32) {
+      uint32_t r[32];
+      for (int j = 0; j < 32; ++j)
+        r[j] = static_cast<uint32_t>(a[row * 128 + 2 * (c0 + j)]) |
+               (static_cast<uint32_t>(a[row * 128 + 2 * (c0 + j) + 1]) << 16);
+      umma::st32(umma::taddr(tm, warp * 32, 128 + c0), r);
+    }
+    umma::wait_st();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
   if (tid == 0) {
     const uint32_t A = smem_u32(sa), B = smem_u32(sb);
     for (int k = 0; k < 8; ++k) {
@@ -74,7 +89,8 @@ __global__ void probe(const uint16_t* a, const uint16_t* b, float* d, int mode, 
         bd = umma::desc_sw128(B + k * 2048, 16384, 1024);
         id = umma::idesc_bf16_f32(128, 128, false, true);
       }
-      umma::mma_bf16(tm, ad, bd, id, k > 0);
+      if (mode == 2) umma::mma_bf16_ts(tm, tm + 128 + k * 8, bd, id, k > 0);
+      else umma::mma_bf16(tm, ad, bd, id, k > 0);
     }
     umma::commit(smem_u32(&bar));
   }
@@ -155,6 +171,7 @@ int main() {
   bad += run(0, 128);
   bad += run(0, 256);
   bad += run(1, 128);
+  bad += run(2, 128);
   printf(bad ? "PROBE FAILED\n" : "PROBE OK\n");
   return bad;
 }
