@@ -54,9 +54,9 @@ constexpr int kThreads = 320;
 constexpr int kProducerWarp = 8, kMmaWarp = 9;
 
 // barrier slots
-constexpr int kBarQ = 0, kBarKFull = 1, kBarVFull = kBarKFull + kStages, kBarKVEmpty = kBarVFull + kStages,
-              kBarSFull = kBarKVEmpty + kStages, kBarPFull = kBarSFull + kTiles, kBarODone = kBarPFull + kTiles,
-              kNumBars = kBarODone + kTiles;
+constexpr int kBarQ = 0, kBarKFull = 1, kBarVFull = kBarKFull + kStages, kBarKEmpty = kBarVFull + kStages,
+              kBarVEmpty = kBarKEmpty + kStages, kBarSFull = kBarVEmpty + kStages, kBarPFull = kBarSFull + kTiles,
+              kBarODone = kBarPFull + kTiles, kNumBars = kBarODone + kTiles;
 
 struct PArgs {
   uint16_t* out;
@@ -118,6 +118,37 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2 on sm_100)
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 unf2(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -159,7 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kStages; ++s) {
       mbar_init(bar(kBarKFull + s), 1);
       mbar_init(bar(kBarVFull + s), 1);
-      mbar_init(bar(kBarKVEmpty + s), 1);
+      mbar_init(bar(kBarKEmpty + s), 1);
+      mbar_init(bar(kBarVEmpty + s), 1);
     }
     for (int t = 0; t < kTiles; ++t) {
       mbar_init(bar(kBarSFull + t), 1);
@@ -199,14 +231,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         page = bt[t / a.page_size];
         slot = t % a.page_size;
       }
-      if (j >= kStages) mbar_wait(bar(kBarKVEmpty + st), ((j / kStages) - 1) & 1);
       const uint32_t dk = sb + kOffK + st * kStageBytes, dv = dk + 2 * kKVHalf;
       const uint32_t bytes = static_cast<uint32_t>(groups) * 2 * 2048;
+      if (j >= kStages) mbar_wait(bar(kBarKEmpty + st), ((j / kStages) - 1) & 1);
       if (lane == 0) mbar_expect_tx(bar(kBarKFull + st), bytes);
       __syncwarp();
       if (lane < groups)
         for (int h = 0; h < 2; ++h)
           tma_load_5d(dk + h * kKVHalf + lane * 2048, &tmk, 0, slot, h, g, page, bar(kBarKFull + st));
+      if (j >= kStages) mbar_wait(bar(kBarVEmpty + st), ((j / kStages) - 1) & 1);
       if (lane == 0) mbar_expect_tx(bar(kBarVFull + st), bytes);
       __syncwarp();
       if (lane < groups)
@@ -234,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue_s(t, 0);
           umma::commit(bar(kBarSFull + t));
         }
+      umma::commit(bar(kBarKEmpty));      // K_0 consumed once these S complete
     }
     __syncwarp();
     for (int j = 0; j < nt; ++j) {
@@ -272,17 +306,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma::mma_bf16_ts(tp + kColO, tp + k * 8, vd, kIdescO, j > 0 || k > 0);
             umma::mma_bf16_ts(tp + kColO, tp + 64 + k * 8, vd, kIdescO, true);
           }
+          const bool last_v = t == kTiles - 1 || j >= nt1;        // no later tile reads V_j
+          if (last_v) umma::commit(bar(kBarVEmpty + st));
           if (more) {
             issue_s(t, (j + 1) % kStages);
             umma::commit(bar(kBarSFull + t));
+            if (last_v) umma::commit(bar(kBarKEmpty + (j + 1) % kStages));   // last S on K_{j+1}
           } else {
             umma::commit(bar(kBarODone + t));
           }
         }
         __syncwarp();
       }
-      if (lane == 0) umma::commit(bar(kBarKVEmpty + st));
-      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ softmax warps
@@ -296,7 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tS = tmem + t * kTileCols + (static_cast<uint32_t>(quarter * 32) << 16);
       const uint32_t tO = tS + kColO;
       const float sl = a.scale_log2;
-      float m = -INFINITY, l0 = 0.f, l1 = 0.f;
+      float m = -INFINITY;
+      uint64_t l2 = f2(0.f, 0.f);                   // row sum, two partial lanes
       for (int j = 0; j < my_nt; ++j) {
         mbar_wait(bar(kBarSFull + t), j & 1);
         umma::fence_after_sync();
@@ -328,25 +364,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if ((m_new - m) * sl > 8.f) {
           resc = true;
           alpha = ex2((m - m_new) * sl);
-          l0 *= alpha;
-          l1 *= alpha;
+          l2 = fmul2(l2, f2(alpha, alpha));
           m = m_new;
         }
-        const float msl = m * sl;
+        const uint64_t sl2 = f2(sl, sl), nm2 = f2(-m * sl, -m * sl);
 #pragma unroll
         for (int c0 = 0; c0 < kBN; c0 += 32) {
           uint32_t hw[16], lw[16];
 #pragma unroll
           for (int w = 0; w < 16; ++w) {
-            const float p0 = ex2(fmaf(s[c0 + 2 * w], sl, -msl));
-            const float p1 = ex2(fmaf(s[c0 + 2 * w + 1], sl, -msl));
-            l0 += p0;
-            l1 += p1;
+            const float2 x = unf2(ffma2(f2(s[c0 + 2 * w], s[c0 + 2 * w + 1]), sl2, nm2));
+            const float p0 = ex2(x.x), p1 = ex2(x.y);
+            const uint64_t pp = f2(p0, p1);
+            l2 = fadd2(l2, pp);
             const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
             hw[w] = __byte_perm(u0, u1, 0x7632);
-            const float r0 = p0 - __uint_as_float(u0 & 0xffff0000u);
-            const float r1 = p1 - __uint_as_float(u1 & 0xffff0000u);
-            lw[w] = __byte_perm(__float_as_uint(r0), __float_as_uint(r1), 0x7632);
+            const float2 rr = unf2(fsub2(pp, f2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u))));
+            lw[w] = __byte_perm(__float_as_uint(rr.x), __float_as_uint(rr.y), 0x7632);
           }
           umma::st16(tS + c0 / 2, hw);          // hi: columns [0, 64)
           umma::st16(tS + 64 + c0 / 2, lw);     // lo: columns [64, 128)
@@ -371,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // epilogue: O / l -> bf16
       mbar_wait(bar(kBarODone + t), 0);
       umma::fence_after_sync();
-      const float inv_l = 1.f / (l0 + l1);
+      const float2 lp = unf2(l2);
+      const float inv_l = 1.f / (lp.x + lp.y);
       uint16_t* orow = a.out + (static_cast<int64_t>(q0 + min(i_row, q_len - 1)) * a.hq + g * G + r % G) * 128;
 #pragma unroll 1
       for (int c0 = 0; c0 < 128; c0 += 32) {
