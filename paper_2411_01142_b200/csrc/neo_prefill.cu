@@ -27,6 +27,7 @@
 // and S_j+1(t) may overwrite P_j(t) without further barriers.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "neo_internal.cuh"
@@ -54,7 +55,7 @@ constexpr int kThreads = 320;
 constexpr int kProducerWarp = 8, kMmaWarp = 9;
 
 // barrier slots
-constexpr int kBarQ = 0, kBarKFull = 1, kBarVFull = kBarKFull + kStages, kBarKEmpty = kBarVFull + kStages,
+constexpr int kBarQFull = 0, kBarQEmpty = 1, kBarKFull = 2, kBarVFull = kBarKFull + kStages, kBarKEmpty = kBarVFull + kStages,
               kBarVEmpty = kBarKEmpty + kStages, kBarSFull = kBarVEmpty + kStages, kBarPFull = kBarSFull + kTiles,
               kBarODone = kBarPFull + kTiles, kNumBars = kBarODone + kTiles;
 
@@ -63,7 +64,7 @@ struct PArgs {
   const int32_t* block_table;
   const int32_t* seq_lens;
   const int32_t* q_offsets;
-  int32_t hq, G, page_size, max_blocks;
+  int32_t batch, hq, hkv, G, page_size, max_blocks, n_ct_max;
   float scale_log2;
 };
 
@@ -153,6 +154,34 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// One work item = (request b, kv-head g, CTA tile ct: 2 x 128 rows).
+struct Item {
+  int b, g, q0, q_len, ctx, i0, nt0, nt1;
+};
+
+// Virtual item k in longest-first order: ct descending (later query rows see
+// more keys), then request, then kv-head.  Returns false for a slot past the
+// request's query rows.
+__device__ __forceinline__ bool make_item(const PArgs& a, int k, int rows_tok, Item& it) {
+  const int per_ct = a.batch * a.hkv;
+  const int ct = a.n_ct_max - 1 - k / per_ct;
+  const int rem = k % per_ct;
+  it.b = rem / a.hkv;
+  it.g = rem % a.hkv;
+  it.q0 = a.q_offsets[it.b];
+  it.q_len = a.q_offsets[it.b + 1] - it.q0;
+  if (ct * kTiles * rows_tok >= it.q_len) return false;
+  it.ctx = a.seq_lens[it.b];
+  it.i0 = ct * kTiles * rows_tok;
+  const int f0 = it.i0, f1 = it.i0 + rows_tok;
+  it.nt0 = (it.ctx - it.q_len + min(f0 + rows_tok, it.q_len) - 1) / kBN + 1;
+  it.nt1 = f1 < it.q_len ? (it.ctx - it.q_len + min(f1 + rows_tok, it.q_len) - 1) / kBN + 1 : 0;
+  return true;
+}
+
+// Persistent: one CTA per SM walks its snake-ordered share of the items; the
+// TMA ring, the S/P and O TMEM buffers and all barrier phases run on across
+// items, so one item's epilogue overlaps the next item's loads and first S.
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_attn_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
                         const __grid_constant__ CUtensorMap tmv, const PArgs a) {
@@ -160,25 +189,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t bars[kNumBars];
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.z, g = blockIdx.y;
   const int G = a.G, rows_tok = kBM / G;
-
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int q0 = a.q_offsets[b];
-  const int q_len = a.q_offsets[b + 1] - q0;
-  const int n_ct = (q_len + kTiles * rows_tok - 1) / (kTiles * rows_tok);
-  const int ct = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);   // longest CTAs first
-  if (ct >= n_ct) return;
-  const int ctx = a.seq_lens[b];
-  const int i0 = ct * kTiles * rows_tok;
-  // key tiles each M tile needs (0: the tile holds no query row)
-  auto tiles_of = [&](int t) {
-    const int first = i0 + t * rows_tok;
-    return first < q_len ? (ctx - q_len + min(first + rows_tok, q_len) - 1) / kBN + 1 : 0;
+  const int n_items = a.n_ct_max * a.batch * a.hkv;
+  // snake order over the longest-first item list: round r takes item
+  // r * grid + c (r even) or r * grid + grid - 1 - c (r odd), so the per-CTA
+  // sums of the sorted costs balance
+  auto first_item = [&](int round) {
+    const int c = static_cast<int>(blockIdx.x), n = static_cast<int>(gridDim.x);
+    return round * n + ((round & 1) ? n - 1 - c : c);
   };
-  const int nt0 = tiles_of(0), nt1 = tiles_of(1);
-  const int nt = max(nt0, nt1);
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sb = smem_u32(smem);
@@ -186,7 +205,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto bar = [bar0](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
 
   if (threadIdx.x == 0) {
-    mbar_init(bar(kBarQ), 1);
+    mbar_init(bar(kBarQFull), 1);
+    mbar_init(bar(kBarQEmpty), 1);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(bar(kBarKFull + s), 1);
       mbar_init(bar(kBarVFull + s), 1);
@@ -209,42 +229,57 @@ __global__ void __launch_bounds__(kThreads, 1)
   umma::fence_after_sync();
   const uint32_t tmem = tmem_sh;
 
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // metadata and q may come from the previous kernel
+
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
-      const int nq = nt1 > 0 ? 2 : 1;
-      mbar_expect_tx(bar(kBarQ), nq * 2 * kQHalf);
-      for (int t = 0; t < nq; ++t)
-        for (int h = 0; h < 2; ++h)
-          tma_load_4d(sb + (t * 2 + h) * kQHalf, &tmq, 0, g * G, q0 + i0 + t * rows_tok, h, bar(kBarQ));
     }
-    const int32_t* bt = a.block_table + static_cast<int64_t>(b) * a.max_blocks;
-    for (int j = 0; j < nt; ++j) {
-      const int st = j % kStages;
-      const int kv0 = j * kBN;
-      const int groups = min(kBN / 16, (ctx - kv0 + 15) / 16);
-      int page = 0, slot = 0;
-      if (lane < groups) {                       // lane u: page and slot of token group u
-        const int t = kv0 + 16 * lane;
-        page = bt[t / a.page_size];
-        slot = t % a.page_size;
+    uint32_t kc = 0, items = 0;                      // K/V tiles and items issued so far
+    for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
+      Item it;
+      if (!make_item(a, k, rows_tok, it)) continue;
+      if (items > 0) mbar_wait(bar(kBarQEmpty), (items - 1) & 1);
+      if (lane == 0) {
+        const int nq = it.nt1 > 0 ? 2 : 1;
+        mbar_expect_tx(bar(kBarQFull), nq * 2 * kQHalf);
+        for (int t = 0; t < nq; ++t)
+          for (int h = 0; h < 2; ++h)
+            tma_load_4d(sb + (t * 2 + h) * kQHalf, &tmq, 0, it.g * G, it.q0 + it.i0 + t * rows_tok, h,
+                        bar(kBarQFull));
       }
-      const uint32_t dk = sb + kOffK + st * kStageBytes, dv = dk + 2 * kKVHalf;
-      const uint32_t bytes = static_cast<uint32_t>(groups) * 2 * 2048;
-      if (j >= kStages) mbar_wait(bar(kBarKEmpty + st), ((j / kStages) - 1) & 1);
-      if (lane == 0) mbar_expect_tx(bar(kBarKFull + st), bytes);
-      __syncwarp();
-      if (lane < groups)
-        for (int h = 0; h < 2; ++h)
-          tma_load_5d(dk + h * kKVHalf + lane * 2048, &tmk, 0, slot, h, g, page, bar(kBarKFull + st));
-      if (j >= kStages) mbar_wait(bar(kBarVEmpty + st), ((j / kStages) - 1) & 1);
-      if (lane == 0) mbar_expect_tx(bar(kBarVFull + st), bytes);
-      __syncwarp();
-      if (lane < groups)
-        for (int h = 0; h < 2; ++h)
-          tma_load_5d(dv + h * kKVHalf + lane * 2048, &tmv, 0, slot, h, g, page, bar(kBarVFull + st));
+      ++items;
+      const int32_t* bt = a.block_table + static_cast<int64_t>(it.b) * a.max_blocks;
+      const int nt = max(it.nt0, it.nt1);
+      for (int j = 0; j < nt; ++j, ++kc) {
+        const int st = kc % kStages;
+        const int kv0 = j * kBN;
+        const int groups = min(kBN / 16, (it.ctx - kv0 + 15) / 16);
+        int page = 0, slot = 0;
+        if (lane < groups) {                       // lane u: page and slot of token group u
+          const int t = kv0 + 16 * lane;
+          page = bt[t / a.page_size];
+          slot = t % a.page_size;
+        }
+        const uint32_t dk = sb + kOffK + st * kStageBytes, dv = dk + 2 * kKVHalf;
+        const uint32_t bytes = static_cast<uint32_t>(groups) * 2 * 2048;
+        if (kc >= kStages) mbar_wait(bar(kBarKEmpty + st), ((kc / kStages) - 1) & 1);
+        if (lane == 0) mbar_expect_tx(bar(kBarKFull + st), bytes);
+        __syncwarp();
+        if (lane < groups)
+          for (int h = 0; h < 2; ++h)
+            tma_load_5d(dk + h * kKVHalf + lane * 2048, &tmk, 0, slot, h, it.g, page, bar(kBarKFull + st));
+        if (kc >= kStages) mbar_wait(bar(kBarVEmpty + st), ((kc / kStages) - 1) & 1);
+        if (lane == 0) mbar_expect_tx(bar(kBarVFull + st), bytes);
+        __syncwarp();
+        if (lane < groups)
+          for (int h = 0; h < 2; ++h)
+            tma_load_5d(dv + h * kKVHalf + lane * 2048, &tmv, 0, slot, h, it.g, page, bar(kBarVFull + st));
+      }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
@@ -257,84 +292,103 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma::mma_bf16(tmem + t * kTileCols, ad, bd, kIdescS, kk > 0);
       }
     };
-    mbar_wait(bar(kBarQ), 0);
-    mbar_wait(bar(kBarKFull), 0);
-    umma::fence_after_sync();
-    if (lane == 0) {
-#pragma unroll
-      for (int t = 0; t < kTiles; ++t)
-        if ((t ? nt1 : nt0) > 0) {
-          issue_s(t, 0);
-          umma::commit(bar(kBarSFull + t));
+    uint32_t kc = 0, vc = 0, items = 0, pc0 = 0, pc1 = 0;
+    for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
+      Item it;
+      if (!make_item(a, k, rows_tok, it)) continue;
+      const int nt = max(it.nt0, it.nt1);
+      mbar_wait(bar(kBarQFull), items & 1);
+      ++items;
+      mbar_wait(bar(kBarKFull + kc % kStages), (kc / kStages) & 1);
+      umma::fence_after_sync();
+      if (lane == 0) {
+        issue_s(0, kc % kStages);
+        umma::commit(bar(kBarSFull + 0));
+        if (it.nt1 > 0) {
+          issue_s(1, kc % kStages);
+          umma::commit(bar(kBarSFull + 1));
         }
-      umma::commit(bar(kBarKEmpty));      // K_0 consumed once these S complete
-    }
-    __syncwarp();
-    for (int j = 0; j < nt; ++j) {
-      const int st = j % kStages;
-      mbar_wait(bar(kBarVFull + st), (j / kStages) & 1);
-      const int nvalid = min(kBN, ctx - j * kBN);
-      const int ksteps = (nvalid + 15) / 16;
-      const uint32_t vb = sb + kOffK + st * kStageBytes + 2 * kKVHalf;
-      if (nvalid & 15) {
-        // rows nvalid .. 16*ksteps-1 hold page-tail slots: zero them (P is 0
-        // there, but 0 * NaN would poison O)
-        const int nrows = 16 * ksteps - nvalid;
-        for (int e = lane; e < nrows * 2 * 8; e += 32) {
-          const int row = nvalid + e / 16, h = (e / 8) & 1, c = e & 7;
-          sts128(vb + h * kKVHalf + row * 128 + c * 16, 0, 0, 0, 0);
-        }
-        umma::fence_proxy_async_smem();
+        umma::commit(bar(kBarKEmpty + kc % kStages));      // K tile consumed once these S complete
+        if (nt == 1) umma::commit(bar(kBarQEmpty));        // last S of the item: Q free
       }
       __syncwarp();
-      bool next_ready = false;
-#pragma unroll
-      for (int t = 0; t < kTiles; ++t) {
-        const int ntt = t ? nt1 : nt0;
-        if (j >= ntt) continue;
-        mbar_wait(bar(kBarPFull + t), j & 1);
-        const bool more = j + 1 < ntt;
-        if (more && !next_ready) {
-          mbar_wait(bar(kBarKFull + (j + 1) % kStages), ((j + 1) / kStages) & 1);
-          next_ready = true;
-        }
-        umma::fence_after_sync();
-        if (lane == 0) {
-          const uint32_t tp = tmem + t * kTileCols;
-          for (int k = 0; k < ksteps; ++k) {
-            const uint64_t vd = umma::desc_sw128(vb + k * 2048, kKVHalf, 1024);
-            umma::mma_bf16_ts(tp + kColO, tp + k * 8, vd, kIdescO, j > 0 || k > 0);
-            umma::mma_bf16_ts(tp + kColO, tp + 64 + k * 8, vd, kIdescO, true);
+      ++kc;
+      for (int j = 0; j < nt; ++j, ++vc) {
+        const int st = vc % kStages;
+        mbar_wait(bar(kBarVFull + st), (vc / kStages) & 1);
+        const int nvalid = min(kBN, it.ctx - j * kBN);
+        const int ksteps = (nvalid + 15) / 16;
+        const uint32_t vb = sb + kOffK + st * kStageBytes + 2 * kKVHalf;
+        if (nvalid & 15) {
+          // rows nvalid .. 16*ksteps-1 hold page-tail slots: zero them (P is 0
+          // there, but 0 * NaN would poison O)
+          const int nrows = 16 * ksteps - nvalid;
+          for (int e = lane; e < nrows * 2 * 8; e += 32) {
+            const int row = nvalid + e / 16, h = (e / 8) & 1, c = e & 7;
+            sts128(vb + h * kKVHalf + row * 128 + c * 16, 0, 0, 0, 0);
           }
-          const bool last_v = t == kTiles - 1 || j >= nt1;        // no later tile reads V_j
-          if (last_v) umma::commit(bar(kBarVEmpty + st));
-          if (more) {
-            issue_s(t, (j + 1) % kStages);
-            umma::commit(bar(kBarSFull + t));
-            if (last_v) umma::commit(bar(kBarKEmpty + (j + 1) % kStages));   // last S on K_{j+1}
-          } else {
-            umma::commit(bar(kBarODone + t));
-          }
+          umma::fence_proxy_async_smem();
         }
         __syncwarp();
+        bool next_ready = false;
+#pragma unroll
+        for (int t = 0; t < kTiles; ++t) {
+          const int ntt = t ? it.nt1 : it.nt0;
+          if (j >= ntt) continue;
+          mbar_wait(bar(kBarPFull + t), (t ? pc1 : pc0) & 1);
+          if (t) ++pc1;
+          else ++pc0;
+          const bool more = j + 1 < ntt;
+          if (more && !next_ready) {
+            mbar_wait(bar(kBarKFull + kc % kStages), (kc / kStages) & 1);
+            next_ready = true;
+          }
+          umma::fence_after_sync();
+          if (lane == 0) {
+            const uint32_t tp = tmem + t * kTileCols;
+            for (int kq = 0; kq < ksteps; ++kq) {
+              const uint64_t vd = umma::desc_sw128(vb + kq * 2048, kKVHalf, 1024);
+              umma::mma_bf16_ts(tp + kColO, tp + kq * 8, vd, kIdescO, j > 0 || kq > 0);
+              umma::mma_bf16_ts(tp + kColO, tp + 64 + kq * 8, vd, kIdescO, true);
+            }
+            const bool last_v = t == kTiles - 1 || j >= it.nt1;   // no later tile reads V_j / K_{j+1}
+            if (last_v) umma::commit(bar(kBarVEmpty + st));
+            if (more) {
+              issue_s(t, kc % kStages);
+              umma::commit(bar(kBarSFull + t));
+              if (last_v) {
+                umma::commit(bar(kBarKEmpty + kc % kStages));
+                if (j + 2 == nt) umma::commit(bar(kBarQEmpty));   // last S of the item
+              }
+            } else {
+              umma::commit(bar(kBarODone + t));
+            }
+          }
+          __syncwarp();
+        }
+        if (next_ready) ++kc;
       }
     }
   } else {
     // ------------------------------------------------------------ softmax warps
     const int t = warp >> 2, quarter = warp & 3;
-    const int my_nt = t ? nt1 : nt0;
-    if (my_nt > 0) {
-      const int r = quarter * 32 + lane;             // row == TMEM lane
-      const int i_row = i0 + t * rows_tok + r / G;
-      const bool valid_row = i_row < q_len;
-      const int pos = ctx - q_len + min(i_row, q_len - 1);
-      const uint32_t tS = tmem + t * kTileCols + (static_cast<uint32_t>(quarter * 32) << 16);
-      const uint32_t tO = tS + kColO;
-      const float sl = a.scale_log2;
+    const int r = quarter * 32 + lane;               // row == TMEM lane
+    const uint32_t tS = tmem + t * kTileCols + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t tO = tS + kColO;
+    const float sl = a.scale_log2;
+    uint32_t sc = 0, oc = 0;                         // S tiles and items consumed so far
+    for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
+      Item it;
+      if (!make_item(a, k, rows_tok, it)) continue;
+      const int my_nt = t ? it.nt1 : it.nt0;
+      if (my_nt == 0) continue;
+      const int i_row = it.i0 + t * rows_tok + r / G;
+      const bool valid_row = i_row < it.q_len;
+      const int pos = it.ctx - it.q_len + min(i_row, it.q_len - 1);
       float m = -INFINITY;
       uint64_t l2 = f2(0.f, 0.f);                   // row sum, two partial lanes
-      for (int j = 0; j < my_nt; ++j) {
-        mbar_wait(bar(kBarSFull + t), j & 1);
+      for (int j = 0; j < my_nt; ++j, ++sc) {
+        mbar_wait(bar(kBarSFull + t), sc & 1);
         umma::fence_after_sync();
         float s[kBN];
         {
@@ -379,7 +433,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             l2 = fadd2(l2, pp);
             const uint32_t u0 = __float_as_uint(p0), u1 = __float_as_uint(p1);
             hw[w] = __byte_perm(u0, u1, 0x7632);
-            const float2 rr = unf2(fsub2(pp, f2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u))));
+            const float2 rr =
+                unf2(fsub2(pp, f2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u))));
             lw[w] = __byte_perm(__float_as_uint(rr.x), __float_as_uint(rr.y), 0x7632);
           }
           umma::st16(tS + c0 / 2, hw);          // hi: columns [0, 64)
@@ -402,12 +457,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(kBarPFull + t));
       }
-      // epilogue: O / l -> bf16
-      mbar_wait(bar(kBarODone + t), 0);
+      // epilogue: O / l -> bf16 (the next item's first PV on this tile waits for
+      // this warpgroup's next P, so O stays intact until read)
+      mbar_wait(bar(kBarODone + t), oc & 1);
+      ++oc;
       umma::fence_after_sync();
       const float2 lp = unf2(l2);
       const float inv_l = 1.f / (lp.x + lp.y);
-      uint16_t* orow = a.out + (static_cast<int64_t>(q0 + min(i_row, q_len - 1)) * a.hq + g * G + r % G) * 128;
+      uint16_t* orow =
+          a.out + (static_cast<int64_t>(it.q0 + min(i_row, it.q_len - 1)) * a.hq + it.g * G + r % G) * 128;
 #pragma unroll 1
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t o[32];
@@ -425,6 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      umma::fence_before_sync();
     }
   }
   umma::fence_before_sync();
@@ -434,21 +493,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-int prefill_ctas(int32_t max_q_len, int32_t G) { return (max_q_len * G + kTiles * kBM - 1) / (kTiles * kBM); }
-
 neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, const CUtensorMap& tmk,
                                const CUtensorMap& tmv) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static int num_sms = 0;
+  if (!num_sms) {
     cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e != cudaSuccess) return cuda_fail(e, "prefill smem attribute");
-    attr_set = true;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "SM count");
   }
   const int G = L.hq / L.hkv;
-  PArgs a{static_cast<uint16_t*>(L.out), L.block_table, L.seq_lens, L.q_offsets, L.hq, G, L.page_size, L.max_blocks,
-          L.scale * 1.4426950408889634f};
+  const int n_ct_max = (L.max_q_len * G + kTiles * kBM - 1) / (kTiles * kBM);
+  const int64_t n_items = static_cast<int64_t>(n_ct_max) * L.batch * L.hkv;
+  if (n_items > (int64_t{1} << 30)) return fail(NEO_ERR_UNSUPPORTED, "prefill: too many work items");
+  PArgs a{static_cast<uint16_t*>(L.out), L.block_table, L.seq_lens, L.q_offsets, L.batch, L.hq, L.hkv, G,
+          L.page_size, L.max_blocks, n_ct_max, L.scale * 1.4426950408889634f};
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(prefill_ctas(L.max_q_len, G), L.hkv, L.batch);
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(n_items, num_sms)));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemAlloc;
   cfg.stream = L.stream;
