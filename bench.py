@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-swap", action="store_true", help="c3: skip the concurrent swap-out")
+    p.add_argument("--no-prefill", action="store_true", help="skip the NEXT-3 prefill leg")
     p.add_argument("--graph", action="store_true", help="capture the step's launches in a CUDA graph")
     return p.parse_args()
 
@@ -288,6 +289,10 @@ def run_neo(args):
     if wl.swap_requests and not args.no_swap:
         swap = run_swap(args, gb, L, step, stream)
 
+    prefill = None
+    if rank == 0 and not args.no_prefill:
+        prefill = run_prefill(args)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(gb, target_s=10.0)
@@ -333,12 +338,91 @@ def run_neo(args):
             "swap": swap,
             "reassembly": reassembly,
             "cpu_share": cpu_share,
+            "prefill": prefill,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def tensor_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst)"
+    except Exception:
+        return 2250.0, "nominal dense bf16 2.25 PFLOP/s (no measured peak)"
+
+
+def run_prefill(args):
+    """the prefill half of NEO's batch-0 for one
+    LLaMa-3.1-8B layer -- whole prompts of ~1000 tokens (P:364's synthetic
+    input length, lengths uniform in [0.9 l, 1.1 l]) up to max_batch_tokens 8192:
+    neo_prefill_append (K/V store + RoPE) then neo_prefill_attn, each timed per
+    launch with CUDA events on the launching stream, L2 flushed between reps."""
+    import torch
+
+    from paper_2411_01142_b200 import neo
+    hq, hkv, d, P = 32, 8, 128, 16
+    rng = np.random.default_rng(0x4E454F)
+    lens = []
+    while True:
+        n = int(rng.integers(900, 1101))
+        if sum(lens) + n > 8192:
+            break
+        lens.append(n)
+    B, T = len(lens), sum(lens)
+    npg = [(n + P - 1) // P for n in lens]
+    g = torch.Generator(device="cuda").manual_seed(7)
+    k_pages = torch.randn(sum(npg) + 4, hkv, P, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    v_pages = torch.randn(sum(npg) + 4, hkv, P, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    perm = torch.randperm(sum(npg), device="cuda", generator=g).to(torch.int32)
+    bt = torch.zeros(B, max(npg), dtype=torch.int32, device="cuda")
+    o = 0
+    for b, m in enumerate(npg):
+        bt[b, :m] = perm[o:o + m]
+        o += m
+    sl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    qo = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int32, device="cuda")
+    q = torch.randn(T, hq, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    kn = torch.randn(T, hkv, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    vn = torch.randn(T, hkv, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    inv = (500000.0 ** (-torch.arange(0, d, 2, dtype=torch.float64) / d)).float().cuda()
+    out = torch.empty_like(q)
+    flush = torch.ones(128 << 20, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+    app, att = [], []
+    for rep in range(3 + 10):
+        flush.sum()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        neo.prefill_append(k_pages, v_pages, bt, sl, qo, kn, vn, q=q, inv_freq=inv)
+        e[1].record(stream)
+        neo.prefill_attn(q, k_pages, v_pages, bt, sl, qo, max(lens), out=out)
+        e[2].record(stream)
+        torch.cuda.synchronize()
+        if rep >= 3:
+            app.append(e[0].elapsed_time(e[1]) / 1e3)
+            att.append(e[1].elapsed_time(e[2]) / 1e3)
+    flops = sum(4.0 * d * hq * n * (n + 1) / 2 for n in lens)
+    t_att = float(np.mean(att))
+    peak, src = tensor_peak()
+    achieved = flops / t_att / 1e12
+    return {
+        "workload": f"LLaMa-3.1-8B layer (32/8 heads, D 128, P 16): {B} whole prompts, {T} tokens "
+                    f"(lengths U[900, 1100] up to max_batch_tokens 8192)",
+        "data": "synthetic N(0,1) bf16, seeded",
+        "attn_us": round(t_att * 1e6, 2), "append_rope_us": round(float(np.mean(app)) * 1e6, 2),
+        "gpu_launches": 2 * 10,
+        "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4), "traffic": None, "kernel": "prefill_attn_kernel",
+                     "algorithmic_flops_per_launch": flops, "peak_source": src,
+                     "mma_flops_per_algorithmic_flop": 1.5,
+                     "note": "algorithmic = causal 4*D per (q-head, row, visible key); P.V runs as bf16 hi + lo "
+                             "(two MMAs) for the tolerance, so the tensor core executes 1.5x these flops"},
+        "l2": "flushed (512 MB read) before every rep",
+    }
 
 
 def run_cpu_share(args, wl, ctx_all, n_gpu, t_ga):

@@ -66,7 +66,24 @@ struct PArgs {
   const int32_t* q_offsets;
   int32_t batch, hq, hkv, G, page_size, max_blocks, n_ct_max;
   float scale_log2;
+#ifdef NEO_PREFILL_TRACE
+  long long* trace;   // [2 tiles][64 steps][8] clock64 stamps of CTA 0 (tools/prefill_trace.py)
+#endif
 };
+
+#ifdef NEO_PREFILL_TRACE
+}  // namespace
+long long* g_prefill_trace = nullptr;
+namespace {
+#define TRACE(t, j, slot)                                                                          \
+  do {                                                                                            \
+    if (blockIdx.x == 0 && (j) < 64) a.trace[((t) * 64 + (j)) * 8 + (slot)] = clock64();           \
+  } while (0)
+#else
+#define TRACE(t, j, slot) \
+  do {                    \
+  } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -283,13 +300,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
+    // Descriptors are built once; every MMA then adds a compile-time offset
+    // (start address >> 4 in the low bits), keeping the single-thread issue
+    // path short enough for the tensor core to stay fed (tools/umma_rate.cu).
+    const uint64_t dq0 = umma::desc_sw128(sb, 16, 1024), dq1 = umma::desc_sw128(sb + 2 * kQHalf, 16, 1024);
+    const uint64_t dk0 = umma::desc_sw128(sb + kOffK, 16, 1024);
+    const uint64_t dv0 = umma::desc_sw128(sb + kOffK + 2 * kKVHalf, kKVHalf, 1024);
+    constexpr uint64_t kStageDesc = kStageBytes / 16;
     auto issue_s = [&](int t, int st) {
-      const uint32_t kb = sb + kOffK + st * kStageBytes;
+      const uint64_t aq = t ? dq1 : dq0, bk = dk0 + static_cast<uint64_t>(st) * kStageDesc;
+      const uint32_t d = tmem + t * kTileCols;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const uint64_t ad = umma::desc_sw128(sb + (t * 2 + (kk >> 2)) * kQHalf + (kk & 3) * 32, 16, 1024);
-        const uint64_t bd = umma::desc_sw128(kb + (kk >> 2) * kKVHalf + (kk & 3) * 32, 16, 1024);
-        umma::mma_bf16(tmem + t * kTileCols, ad, bd, kIdescS, kk > 0);
+      for (int kk = 0; kk < 8; ++kk)
+        umma::mma_bf16(d, aq + ((kk >> 2) * kQHalf + (kk & 3) * 32) / 16,
+                       bk + ((kk >> 2) * kKVHalf + (kk & 3) * 32) / 16, kIdescS, kk > 0);
+    };
+    auto issue_pv = [&](int t, int st, int ksteps, bool acc0) {
+      const uint32_t tp = tmem + t * kTileCols;
+      const uint64_t bv = dv0 + static_cast<uint64_t>(st) * kStageDesc;
+      if (ksteps == 8) {
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq) {
+          umma::mma_bf16_ts(tp + kColO, tp + kq * 8, bv + (kq * 2048) / 16, kIdescO, kq > 0 || acc0);
+          umma::mma_bf16_ts(tp + kColO, tp + 64 + kq * 8, bv + (kq * 2048) / 16, kIdescO, true);
+        }
+      } else {
+        for (int kq = 0; kq < ksteps; ++kq) {
+          umma::mma_bf16_ts(tp + kColO, tp + kq * 8, bv + (kq * 2048) / 16, kIdescO, kq > 0 || acc0);
+          umma::mma_bf16_ts(tp + kColO, tp + 64 + kq * 8, bv + (kq * 2048) / 16, kIdescO, true);
+        }
       }
     };
     uint32_t kc = 0, vc = 0, items = 0, pc0 = 0, pc1 = 0;
@@ -335,7 +374,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < kTiles; ++t) {
           const int ntt = t ? it.nt1 : it.nt0;
           if (j >= ntt) continue;
+          if (lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 4);
           mbar_wait(bar(kBarPFull + t), (t ? pc1 : pc0) & 1);
+          if (lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 5);
           if (t) ++pc1;
           else ++pc0;
           const bool more = j + 1 < ntt;
@@ -345,17 +386,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           umma::fence_after_sync();
           if (lane == 0) {
-            const uint32_t tp = tmem + t * kTileCols;
-            for (int kq = 0; kq < ksteps; ++kq) {
-              const uint64_t vd = umma::desc_sw128(vb + kq * 2048, kKVHalf, 1024);
-              umma::mma_bf16_ts(tp + kColO, tp + kq * 8, vd, kIdescO, j > 0 || kq > 0);
-              umma::mma_bf16_ts(tp + kColO, tp + 64 + kq * 8, vd, kIdescO, true);
-            }
+            issue_pv(t, st, ksteps, j > 0);
             const bool last_v = t == kTiles - 1 || j >= it.nt1;   // no later tile reads V_j / K_{j+1}
             if (last_v) umma::commit(bar(kBarVEmpty + st));
             if (more) {
               issue_s(t, kc % kStages);
               umma::commit(bar(kBarSFull + t));
+              if (k == static_cast<int>(blockIdx.x)) TRACE(t, j, 6);
               if (last_v) {
                 umma::commit(bar(kBarKEmpty + kc % kStages));
                 if (j + 2 == nt) umma::commit(bar(kBarQEmpty));   // last S of the item
@@ -388,8 +425,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       float m = -INFINITY;
       uint64_t l2 = f2(0.f, 0.f);                   // row sum, two partial lanes
       for (int j = 0; j < my_nt; ++j, ++sc) {
+        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 0);
         mbar_wait(bar(kBarSFull + t), sc & 1);
         umma::fence_after_sync();
+        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 1);
         float s[kBN];
         {
           uint32_t u[32];
@@ -407,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < kBN; ++c)
             if (kv0 + c > pos) s[c] = -INFINITY;
         }
+        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 2);
         float mx = s[0];
 #pragma unroll
         for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
@@ -455,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma::wait_st();
         umma::fence_before_sync();
         __syncwarp();
+        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 3);
         if (lane == 0) mbar_arrive(bar(kBarPFull + t));
       }
       // epilogue: O / l -> bf16 (the next item's first PV on this tile waits for
@@ -510,6 +551,13 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   if (n_items > (int64_t{1} << 30)) return fail(NEO_ERR_UNSUPPORTED, "prefill: too many work items");
   PArgs a{static_cast<uint16_t*>(L.out), L.block_table, L.seq_lens, L.q_offsets, L.batch, L.hq, L.hkv, G,
           L.page_size, L.max_blocks, n_ct_max, L.scale * 1.4426950408889634f};
+#ifdef NEO_PREFILL_TRACE
+  static long long* trace = nullptr;
+  if (!trace) cudaMalloc(&trace, 2 * 64 * 8 * sizeof(long long));
+  cudaMemsetAsync(trace, 0, 2 * 64 * 8 * sizeof(long long), L.stream);
+  a.trace = trace;
+  g_prefill_trace = trace;
+#endif
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(n_items, num_sms)));
   cfg.blockDim = dim3(kThreads);
@@ -526,3 +574,7 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
 }
 
 }  // namespace neo
+
+#ifdef NEO_PREFILL_TRACE
+extern "C" __attribute__((visibility("default"))) long long* neo_prefill_trace_ptr() { return neo::g_prefill_trace; }
+#endif
