@@ -202,7 +202,8 @@ NEO_API neo_status neo_rope_append(void* q_inout, int32_t num_q_heads, const flo
  *   q, out     [total_tokens][Hq][D] bf16 device, 16-byte aligned
  *   q_offsets  device int32[batch + 1], 0 = q_offsets[0] <= ... = total_tokens
  *   max_q_len  >= every n_q (sizes the grid; rows beyond a request's n_q idle)
- *   G = Hq / Hkv in {1, 2, 4, 8, 16}; D = 128; P a multiple of 16.
+ *   G = Hq / Hkv in {1, 2, 4, 8, 16}; D = 128; P a multiple of 16;
+ *   batch <= 512 and max_q_len * G <= 262144 (the per-CTA schedule table).
  * Numerics: bf16 x bf16 products exact in fp32 (tcgen05.mma), softmax in fp32
  * (exp2 domain), P applied as bf16 hi + lo, output RNE to bf16.  Deterministic.
  * Page-tail slots beyond seq_lens are never read into the result (NaN-safe).

@@ -471,7 +471,8 @@ NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const vo
   const int32_t G = hq / hkv;
   if (G > 16 || (G & (G - 1))) return fail(NEO_ERR_UNSUPPORTED, "G = Hq / Hkv must be 1, 2, 4, 8 or 16");
   if (batch == 0 || total_tokens == 0) return NEO_OK;
-  if (batch > 65535) return fail(NEO_ERR_UNSUPPORTED, "batch <= 65535");
+  if (batch > 512 || static_cast<int64_t>(max_q_len) * G > 262144)
+    return fail(NEO_ERR_UNSUPPORTED, "prefill: batch <= 512 and max_q_len * G <= 262144 per call");
   if (!q || !k_pages || !v_pages || !block_table || !seq_lens || !q_offsets || !out)
     return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
   if (!neo::aligned16(q) || !neo::aligned16(k_pages) || !neo::aligned16(v_pages) || !neo::aligned16(out))

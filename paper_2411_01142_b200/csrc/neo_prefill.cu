@@ -176,24 +176,62 @@ struct Item {
   int b, g, q0, q_len, ctx, i0, nt0, nt1;
 };
 
-// Virtual item k in longest-first order: ct descending (later query rows see
-// more keys), then request, then kv-head.  Returns false for a slot past the
-// request's query rows.
-__device__ __forceinline__ bool make_item(const PArgs& a, int k, int rows_tok, Item& it) {
-  const int per_ct = a.batch * a.hkv;
-  const int ct = a.n_ct_max - 1 - k / per_ct;
-  const int rem = k % per_ct;
-  it.b = rem / a.hkv;
-  it.g = rem % a.hkv;
+// Dense longest-first item list, built per CTA in shared memory by the
+// prologue: level lv = 0, 1, ... is CTA tile ct = n_ct_max - 1 - lv (later
+// query rows see more keys); a level holds every (request, kv-head) whose
+// prompt chunk reaches that tile, requests in descending tile-count order.
+//   req[i]    i-th request by descending tile count (ties: lower index first)
+//   pref[lv]  items before level lv;  pref[n_ct_max] = total items
+constexpr int kMaxSchedBatch = 512, kMaxSchedLevels = 1024;
+struct Sched {
+  int req[kMaxSchedBatch];
+  int pref[kMaxSchedLevels + 1];
+};
+
+__device__ __forceinline__ int tiles_of_request(const PArgs& a, int b, int rows_tok) {
+  const int q_len = a.q_offsets[b + 1] - a.q_offsets[b];
+  return (q_len + kTiles * rows_tok - 1) / (kTiles * rows_tok);
+}
+
+// all threads of the CTA; ends with __syncthreads
+__device__ void build_sched(const PArgs& a, int rows_tok, Sched& sc, int* nct_tmp) {
+  for (int b = threadIdx.x; b < a.batch; b += blockDim.x) nct_tmp[b] = tiles_of_request(a, b, rows_tok);
+  __syncthreads();
+  for (int b = threadIdx.x; b < a.batch; b += blockDim.x) {
+    const int n = nct_tmp[b];
+    int rank = 0;
+    for (int o = 0; o < a.batch; ++o) rank += nct_tmp[o] > n || (nct_tmp[o] == n && o < b);
+    sc.req[rank] = b;
+  }
+  // pref[lv] = hkv * sum_b max(0, lv - (n_ct_max - n_b)): request b is present
+  // on levels lv >= n_ct_max - n_b
+  for (int lv = threadIdx.x; lv <= a.n_ct_max; lv += blockDim.x) {
+    int c = 0;
+    for (int o = 0; o < a.batch; ++o) c += max(0, lv - (a.n_ct_max - nct_tmp[o]));
+    sc.pref[lv] = c * a.hkv;
+  }
+  __syncthreads();
+}
+
+// Item k of the dense list (k < sc.pref[n_ct_max]).
+__device__ __forceinline__ void make_item(const PArgs& a, const Sched& sc, int k, int rows_tok, Item& it) {
+  int lo = 0, hi = a.n_ct_max - 1;                 // last level with pref[lv] <= k
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sc.pref[mid] <= k) lo = mid;
+    else hi = mid - 1;
+  }
+  const int ct = a.n_ct_max - 1 - lo;
+  const int r = k - sc.pref[lo];
+  it.b = sc.req[r / a.hkv];
+  it.g = r % a.hkv;
   it.q0 = a.q_offsets[it.b];
   it.q_len = a.q_offsets[it.b + 1] - it.q0;
-  if (ct * kTiles * rows_tok >= it.q_len) return false;
   it.ctx = a.seq_lens[it.b];
   it.i0 = ct * kTiles * rows_tok;
   const int f0 = it.i0, f1 = it.i0 + rows_tok;
   it.nt0 = (it.ctx - it.q_len + min(f0 + rows_tok, it.q_len) - 1) / kBN + 1;
   it.nt1 = f1 < it.q_len ? (it.ctx - it.q_len + min(f1 + rows_tok, it.q_len) - 1) / kBN + 1 : 0;
-  return true;
 }
 
 // Persistent: one CTA per SM walks its snake-ordered share of the items; the
@@ -207,7 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.G, rows_tok = kBM / G;
-  const int n_items = a.n_ct_max * a.batch * a.hkv;
+  __shared__ Sched sched;
+  __shared__ int nct_tmp[kMaxSchedBatch];
   // snake order over the longest-first item list: round r takes item
   // r * grid + c (r even) or r * grid + grid - 1 - c (r odd), so the per-CTA
   // sums of the sorted costs balance
@@ -248,6 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");   // metadata and q may come from the previous kernel
+  build_sched(a, rows_tok, sched, nct_tmp);
+  const int n_items = sched.pref[a.n_ct_max];
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -259,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t kc = 0, items = 0;                      // K/V tiles and items issued so far
     for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
       Item it;
-      if (!make_item(a, k, rows_tok, it)) continue;
+      make_item(a, sched, k, rows_tok, it);
       if (items > 0) mbar_wait(bar(kBarQEmpty), (items - 1) & 1);
       if (lane == 0) {
         const int nq = it.nt1 > 0 ? 2 : 1;
@@ -307,49 +348,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dk0 = umma::desc_sw128(sb + kOffK, 16, 1024);
     const uint64_t dv0 = umma::desc_sw128(sb + kOffK + 2 * kKVHalf, kKVHalf, 1024);
     constexpr uint64_t kStageDesc = kStageBytes / 16;
+    // all 32 lanes call; one elected lane issues (umma::mma_block_*)
     auto issue_s = [&](int t, int st) {
-      const uint64_t aq = t ? dq1 : dq0, bk = dk0 + static_cast<uint64_t>(st) * kStageDesc;
-      const uint32_t d = tmem + t * kTileCols;
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        umma::mma_bf16(d, aq + ((kk >> 2) * kQHalf + (kk & 3) * 32) / 16,
-                       bk + ((kk >> 2) * kKVHalf + (kk & 3) * 32) / 16, kIdescS, kk > 0);
+      umma::mma_block_k128<kQHalf, kKVHalf>(tmem + t * kTileCols, t ? dq1 : dq0,
+                                            dk0 + static_cast<uint64_t>(st) * kStageDesc, kIdescS);
     };
     auto issue_pv = [&](int t, int st, int ksteps, bool acc0) {
       const uint32_t tp = tmem + t * kTileCols;
       const uint64_t bv = dv0 + static_cast<uint64_t>(st) * kStageDesc;
       if (ksteps == 8) {
-#pragma unroll
-        for (int kq = 0; kq < 8; ++kq) {
-          umma::mma_bf16_ts(tp + kColO, tp + kq * 8, bv + (kq * 2048) / 16, kIdescO, kq > 0 || acc0);
-          umma::mma_bf16_ts(tp + kColO, tp + 64 + kq * 8, bv + (kq * 2048) / 16, kIdescO, true);
-        }
-      } else {
+        umma::mma_block_pv128(tp + kColO, tp, bv, kIdescO, acc0);
+      } else if (lane == 0) {
         for (int kq = 0; kq < ksteps; ++kq) {
           umma::mma_bf16_ts(tp + kColO, tp + kq * 8, bv + (kq * 2048) / 16, kIdescO, kq > 0 || acc0);
           umma::mma_bf16_ts(tp + kColO, tp + 64 + kq * 8, bv + (kq * 2048) / 16, kIdescO, true);
         }
       }
+      __syncwarp();
     };
     uint32_t kc = 0, vc = 0, items = 0, pc0 = 0, pc1 = 0;
     for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
       Item it;
-      if (!make_item(a, k, rows_tok, it)) continue;
+      make_item(a, sched, k, rows_tok, it);
       const int nt = max(it.nt0, it.nt1);
       mbar_wait(bar(kBarQFull), items & 1);
       ++items;
       mbar_wait(bar(kBarKFull + kc % kStages), (kc / kStages) & 1);
       umma::fence_after_sync();
-      if (lane == 0) {
-        issue_s(0, kc % kStages);
-        umma::commit(bar(kBarSFull + 0));
-        if (it.nt1 > 0) {
-          issue_s(1, kc % kStages);
-          umma::commit(bar(kBarSFull + 1));
-        }
-        umma::commit(bar(kBarKEmpty + kc % kStages));      // K tile consumed once these S complete
-        if (nt == 1) umma::commit(bar(kBarQEmpty));        // last S of the item: Q free
+      issue_s(0, kc % kStages);
+      umma::commit_elect(bar(kBarSFull + 0));
+      if (it.nt1 > 0) {
+        issue_s(1, kc % kStages);
+        umma::commit_elect(bar(kBarSFull + 1));
       }
+      umma::commit_elect(bar(kBarKEmpty + kc % kStages));  // K tile consumed once these S complete
+      if (nt == 1) umma::commit_elect(bar(kBarQEmpty));    // last S of the item: Q free
       __syncwarp();
       ++kc;
       for (int j = 0; j < nt; ++j, ++vc) {
@@ -385,21 +418,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             next_ready = true;
           }
           umma::fence_after_sync();
-          if (lane == 0) {
-            issue_pv(t, st, ksteps, j > 0);
-            const bool last_v = t == kTiles - 1 || j >= it.nt1;   // no later tile reads V_j / K_{j+1}
-            if (last_v) umma::commit(bar(kBarVEmpty + st));
-            if (more) {
-              issue_s(t, kc % kStages);
-              umma::commit(bar(kBarSFull + t));
-              if (k == static_cast<int>(blockIdx.x)) TRACE(t, j, 6);
-              if (last_v) {
-                umma::commit(bar(kBarKEmpty + kc % kStages));
-                if (j + 2 == nt) umma::commit(bar(kBarQEmpty));   // last S of the item
-              }
-            } else {
-              umma::commit(bar(kBarODone + t));
+          issue_pv(t, st, ksteps, j > 0);
+          const bool last_v = t == kTiles - 1 || j >= it.nt1;   // no later tile reads V_j / K_{j+1}
+          if (last_v) umma::commit_elect(bar(kBarVEmpty + st));
+          if (more) {
+            issue_s(t, kc % kStages);
+            umma::commit_elect(bar(kBarSFull + t));
+            if (lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 6);
+            if (last_v) {
+              umma::commit_elect(bar(kBarKEmpty + kc % kStages));
+              if (j + 2 == nt) umma::commit_elect(bar(kBarQEmpty));   // last S of the item
             }
+          } else {
+            umma::commit_elect(bar(kBarODone + t));
           }
           __syncwarp();
         }
@@ -416,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t sc = 0, oc = 0;                         // S tiles and items consumed so far
     for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
       Item it;
-      if (!make_item(a, k, rows_tok, it)) continue;
+      make_item(a, sched, k, rows_tok, it);
       const int my_nt = t ? it.nt1 : it.nt0;
       if (my_nt == 0) continue;
       const int i_row = it.i0 + t * rows_tok + r / G;
@@ -547,8 +578,9 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   }
   const int G = L.hq / L.hkv;
   const int n_ct_max = (L.max_q_len * G + kTiles * kBM - 1) / (kTiles * kBM);
-  const int64_t n_items = static_cast<int64_t>(n_ct_max) * L.batch * L.hkv;
-  if (n_items > (int64_t{1} << 30)) return fail(NEO_ERR_UNSUPPORTED, "prefill: too many work items");
+  const int64_t n_items = static_cast<int64_t>(n_ct_max) * L.batch * L.hkv;   // upper bound
+  if (L.batch > kMaxSchedBatch || n_ct_max > kMaxSchedLevels)
+    return fail(NEO_ERR_UNSUPPORTED, "prefill: batch <= 512 and max_q_len * G <= 262144 per call");
   PArgs a{static_cast<uint16_t*>(L.out), L.block_table, L.seq_lens, L.q_offsets, L.batch, L.hq, L.hkv, G,
           L.page_size, L.max_blocks, n_ct_max, L.scale * 1.4426950408889634f};
 #ifdef NEO_PREFILL_TRACE

@@ -83,6 +83,90 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       : "memory");
 }
 
+// ---- whole MMA blocks issued from one PTX block by one elected lane of the
+// calling warp (all 32 lanes must call): the address arithmetic stays in the
+// block, so the issue path is one add + one tcgen05.mma per instruction.
+//
+// S block: D (+)= A . B^T over K = 128 as 8 K16 steps; A, B K-major SW128 with
+// the two 64-element K halves `half_a` / `half_b` bytes apart.
+template <uint32_t kHalfA, uint32_t kHalfB>
+__device__ __forceinline__ void mma_block_k128(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  constexpr uint64_t ha = kHalfA / 16, hb = kHalfB / 16;
+  asm volatile(
+      "{\n"
+      ".reg .pred e, pf, pt;\n"
+      ".reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n"
+      "setp.ne.b32 pf, 0, 0;\n"
+      "setp.eq.b32 pt, 0, 0;\n"
+      "add.s64 a1, %1, 2;\n add.s64 a2, %1, 4;\n add.s64 a3, %1, 6;\n"
+      "add.s64 a4, %1, %4;\n add.s64 a5, a4, 2;\n add.s64 a6, a4, 4;\n add.s64 a7, a4, 6;\n"
+      "add.s64 b1, %2, 2;\n add.s64 b2, %2, 4;\n add.s64 b3, %2, 6;\n"
+      "add.s64 b4, %2, %5;\n add.s64 b5, b4, 2;\n add.s64 b6, b4, 4;\n add.s64 b7, b4, 6;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pf;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, pt;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "n"(ha), "n"(hb)
+      : "memory");
+}
+
+// PV block: D (+)= (A_hi + A_lo) . B over K = 128 as 8 K16 steps, A_hi / A_lo in
+// TMEM at columns a, a + 64 (8 columns per step), B MN-major SW128 advancing
+// 2 KiB per step.  `acc0` = accumulate into D on the first step.
+__device__ __forceinline__ void mma_block_pv128(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                bool acc0) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p0, pt;\n"
+      ".reg .b32 h1, h2, h3, h4, h5, h6, h7, l0, l1, l2, l3, l4, l5, l6, l7;\n"
+      ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n"
+      "setp.ne.b32 p0, %4, 0;\n"
+      "setp.eq.b32 pt, 0, 0;\n"
+      "add.u32 h1, %1, 8;\n add.u32 h2, %1, 16;\n add.u32 h3, %1, 24;\n add.u32 h4, %1, 32;\n"
+      "add.u32 h5, %1, 40;\n add.u32 h6, %1, 48;\n add.u32 h7, %1, 56;\n"
+      "add.u32 l0, %1, 64;\n add.u32 l1, %1, 72;\n add.u32 l2, %1, 80;\n add.u32 l3, %1, 88;\n"
+      "add.u32 l4, %1, 96;\n add.u32 l5, %1, 104;\n add.u32 l6, %1, 112;\n add.u32 l7, %1, 120;\n"
+      "add.s64 b1, %2, 128;\n add.s64 b2, %2, 256;\n add.s64 b3, %2, 384;\n add.s64 b4, %2, 512;\n"
+      "add.s64 b5, %2, 640;\n add.s64 b6, %2, 768;\n add.s64 b7, %2, 896;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l0], %2, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l1], b1, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l2], b2, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l3], b3, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h4], b4, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l4], b4, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h5], b5, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l5], b5, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h6], b6, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l6], b6, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h7], b7, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l7], b7, %3, pt;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(static_cast<uint32_t>(acc0))
+      : "memory");
+}
+
+// commit from one elected lane of the calling warp (all 32 lanes call)
+__device__ __forceinline__ void commit_elect(uint32_t bar_smem) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(bar_smem)
+      : "memory");
+}
+
 // arrive (once) on an mbarrier when every previously issued MMA of this thread completes
 __device__ __forceinline__ void commit(uint32_t bar_smem) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar_smem)

@@ -75,6 +75,39 @@ def test_decode_attn_batch_zero_is_noop():
     assert _attn(B=0, q=0, out=0) == neo.NEO_OK
 
 
+def _prefill(**kw):
+    a = dict(q=16, k=16, v=16, stride=2048 * 8, npages=10, bt=16, maxb=4, sl=16, qo=16, out=16, B=2, T=100, hq=32,
+             hkv=8, d=128, P=16, mql=64, scale=0.088, stream=0)
+    a.update(kw)
+    return neo.lib().neo_prefill_attn(a["q"], a["k"], a["v"], a["stride"], a["npages"], a["bt"], a["maxb"], a["sl"],
+                                      a["qo"], a["out"], a["B"], a["T"], a["hq"], a["hkv"], a["d"], a["P"], a["mql"],
+                                      ctypes.c_float(a["scale"]), a["stream"])
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(d=64), neo.NEO_ERR_UNSUPPORTED),
+    (dict(P=24), neo.NEO_ERR_UNSUPPORTED),
+    (dict(hq=30), neo.NEO_ERR_INVALID_ARG),
+    (dict(hq=24, hkv=8), neo.NEO_ERR_UNSUPPORTED),             # G = 3
+    (dict(hq=256, hkv=8), neo.NEO_ERR_UNSUPPORTED),            # G = 32
+    (dict(B=513), neo.NEO_ERR_UNSUPPORTED),                    # schedule table limit
+    (dict(mql=65537), neo.NEO_ERR_UNSUPPORTED),                # max_q_len * G > 262144
+    (dict(q=0), neo.NEO_ERR_INVALID_ARG),
+    (dict(qo=0), neo.NEO_ERR_INVALID_ARG),
+    (dict(out=24), neo.NEO_ERR_INVALID_ARG),                   # misaligned
+    (dict(stride=2048 * 8 - 8), neo.NEO_ERR_INVALID_ARG),
+    (dict(mql=0), neo.NEO_ERR_INVALID_ARG),
+    (dict(scale=float("nan")), neo.NEO_ERR_INVALID_ARG),
+])
+def test_prefill_attn_validation(kw, status):
+    assert _prefill(**kw) == status
+
+
+def test_prefill_attn_empty_is_noop():
+    assert _prefill(B=0, q=0, out=0) == neo.NEO_OK
+    assert _prefill(T=0, q=0, out=0) == neo.NEO_OK
+
+
 def test_workspace_bytes_and_default_chunk():
     assert neo.default_chunk(256, 8, 1126) == 512
     assert neo.default_chunk(512, 1, 2252) == 256

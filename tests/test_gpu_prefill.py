@@ -119,3 +119,13 @@ def test_prefill_last_row_matches_decode():
         a = ni.bf16_bits_to_f64(out[case.q_off[b + 1] - 1].view(torch.int16).cpu().numpy().view(np.uint16))
         d = ni.bf16_bits_to_f64(dec[b].view(torch.int16).cpu().numpy().view(np.uint16))
         assert within_tol(a, d)[0]
+
+
+def test_prefill_parity_many_ragged_requests():
+    """40 requests of random prompt / prefix lengths (some empty): the dense
+    longest-first schedule table covers every (request, kv-head, tile) once."""
+    rng = np.random.default_rng(600)
+    ctx = rng.integers(1, 400, 40)
+    q_lens = np.minimum(ctx, rng.integers(0, 300, 40))
+    q_lens[::7] = 0
+    check_prefill(PrefillCase(ctx.tolist(), q_lens.tolist(), 32, 8, seed=601), "ragged40")

@@ -4,6 +4,7 @@ importable).  TFLOP/s counts the causal algorithmic work: for every q-head and
 query row at position p, 4 * D * (p + 1) flops (QK^T and PV, multiply + add).
 
 python tools/prefill_time.py [B] [L] [reps]"""
+import itertools
 import math
 import os
 import sys
@@ -29,6 +30,38 @@ def timed(fn, reps):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps / 1e3
+
+
+def run_ragged(lens, reps, flush):
+    """Whole prompts of the given lengths (bench.py's prefill leg shape)."""
+    B = len(lens)
+    npg = [(n + P - 1) // P for n in lens]
+    k_pages = torch.randn(sum(npg), HKV, P, D, device="cuda", dtype=torch.bfloat16)
+    v_pages = torch.randn(sum(npg), HKV, P, D, device="cuda", dtype=torch.bfloat16)
+    bt = torch.zeros(B, max(npg), dtype=torch.int32, device="cuda")
+    o = 0
+    for b, m in enumerate(npg):
+        bt[b, :m] = torch.arange(o, o + m, dtype=torch.int32)
+        o += m
+    sl = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    qo = torch.tensor([0] + list(itertools.accumulate(lens)), dtype=torch.int32, device="cuda")
+    q = torch.randn(sum(lens), HQ, D, device="cuda", dtype=torch.bfloat16)
+    out = torch.empty_like(q)
+    buf = torch.ones(128 << 20, dtype=torch.int32, device="cuda")
+    ts = []
+    for r in range(reps + 3):
+        if flush:
+            buf.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        neo.prefill_attn(q, k_pages, v_pages, bt, sl, qo, max(lens), out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        if r >= 3:
+            ts.append(e0.elapsed_time(e1) / 1e3)
+    t = sum(ts) / len(ts)
+    flops = sum(4.0 * D * HQ * n * (n + 1) / 2 for n in lens)
+    print(f"ragged {lens} flush={flush}: {t * 1e6:.1f} us {flops / t / 1e12:.1f} TF/s")
 
 
 def run(B, L, reps):
@@ -65,6 +98,19 @@ def run(B, L, reps):
 
 
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "ragged":
+        import numpy as np
+        rng = np.random.default_rng(0x4E454F)
+        lens = []
+        while True:
+            n = int(rng.integers(900, 1101))
+            if sum(lens) + n > 8192:
+                break
+            lens.append(n)
+        for flush in (False, True):
+            run_ragged(lens, 20, flush)
+            run_ragged([1024] * 8, 20, flush)
+        return
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 20
     if len(sys.argv) > 2:
         run(int(sys.argv[1]), int(sys.argv[2]), reps)
