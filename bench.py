@@ -407,6 +407,10 @@ def run_prefill(args):
             att.append(e[1].elapsed_time(e[2]) / 1e3)
     flops = sum(4.0 * d * hq * n * (n + 1) / 2 for n in lens)
     t_att = float(np.mean(att))
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):          # ncu --set full of this launch (profiles/r01_ncu_full_prefill.md)
+        traffic = json.load(open(tpath)).get("prefill")
     peak, src = tensor_peak()
     achieved = flops / t_att / 1e12
     return {
@@ -416,8 +420,9 @@ def run_prefill(args):
         "attn_us": round(t_att * 1e6, 2), "append_rope_us": round(float(np.mean(app)) * 1e6, 2),
         "gpu_launches": 2 * 10,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4), "traffic": None, "kernel": "prefill_attn_kernel",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "prefill_attn_kernel",
                      "algorithmic_flops_per_launch": flops, "peak_source": src,
+                     "algorithmic_bytes_per_launch": T * (2 * hq + 2 * hkv) * d * 2,
                      "mma_flops_per_algorithmic_flop": 1.5,
                      "note": "algorithmic = causal 4*D per (q-head, row, visible key); P.V runs as bf16 hi + lo "
                              "(two MMAs) for the tolerance, so the tensor core executes 1.5x these flops"},

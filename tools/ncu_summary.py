@@ -34,6 +34,8 @@ FULL_METRICS = [
     ("smsp__inst_executed.sum", "instructions"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
     ("lts__t_bytes.sum", "L2 bytes"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe"),
 ]
 
 
