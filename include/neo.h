@@ -236,6 +236,26 @@ NEO_API neo_status neo_prefill_append(void* q_inout, int32_t num_q_heads, const 
                                       int32_t total_tokens, int32_t num_kv_heads, int32_t head_dim,
                                       int32_t page_size, void* stream);
 
+/* One-launch decode step (SURVEY NEXT-3 "fused KV append (+ RoPE) + decode
+ * attention"; P:109-110 read-and-append): neo_rope_append (or neo_kv_append when
+ * inv_freq is NULL) and neo_decode_attn fused into one kernel.  With the new
+ * token at t = seq_lens[b] - 1:
+ *   q' = RoPE_t(q[b]) (registers only: q is NOT written back)
+ *   k' = RoPE_t(k_new[b]), v' = v_new[b]; k', v' are stored into the page slot
+ *   of token t AND used as token t's K / V in
+ *   out[b][h] = sum_{t' <= t} softmax(scale q'[h] . K[t'][g]) V[t'][g]
+ * RoPE convention and precision as neo_rope_append (angle reduced in fp64,
+ * sin / cos and rotation in fp32, bf16 RNE).  Other arguments, workspace and
+ * errors as neo_decode_attn; k_new, v_new: [batch][Hkv][D] bf16, 16-byte
+ * aligned; k_pages / v_pages are written (token t's slot only). */
+NEO_API neo_status neo_decode_attn_append(const void* q, const float* inv_freq, const void* k_new, const void* v_new,
+                                          void* k_pages, void* v_pages, int64_t page_stride, int64_t num_pages,
+                                          const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                                          void* out, int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
+                                          int32_t head_dim, int32_t page_size, int32_t max_seq_len, float scale,
+                                          int32_t chunk_tokens, void* workspace, size_t workspace_bytes,
+                                          void* stream);
+
 /* Default split-K chunk length for a call shape (deterministic in its inputs). */
 NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
 

@@ -46,6 +46,13 @@ struct KArgs {
   int32_t* ws_cnt;
   int32_t batch, hq, hkv, G, page_size, max_blocks, chunk_tiles, max_chunks;
   float scale_log2;
+  // fused append (+ RoPE) variant only (neo_decode_attn_append)
+  const float* inv_freq;      // NULL: no rotation
+  const uint16_t* k_new;      // [batch][Hkv][D]
+  const uint16_t* v_new;
+  uint16_t* k_pages;
+  uint16_t* v_pages;
+  int64_t page_stride;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -182,6 +189,38 @@ __device__ __forceinline__ void load_q(const KArgs& a, int b, int g, int r, int 
   } else {
 #pragma unroll
     for (int i = 0; i < 4; ++i) qf[i] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+// RoPE angle theta = t * inv_freq (fp64, reduced to [-pi, pi] in fp64), then
+// sin / cos in fp32 (same convention as neo_rope_append).
+__device__ __forceinline__ void rope_sincos(int t, float f, float& sn, float& cs) {
+  const double th = static_cast<double>(t) * static_cast<double>(f);
+  const double k = rint(th * 0.15915494309189533577);
+  const float red = static_cast<float>(fma(-k, 6.283185307179586232, th));
+  __sincosf(red, &sn, &cs);
+}
+
+// Rotate this lane's q fragment in registers: qf[i] holds dims 8(qd + 4i) .. +7,
+// so the rotate-half partners (d, d + 64) are qf[0] / qf[2] and qf[1] / qf[3].
+__device__ __forceinline__ void rope_q(uint4 (&qf)[4], int qd, int t, const float* inv_freq) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    uint32_t lo[4] = {qf[i].x, qf[i].y, qf[i].z, qf[i].w};
+    uint32_t hi[4] = {qf[i + 2].x, qf[i + 2].y, qf[i + 2].z, qf[i + 2].w};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int d = 8 * (qd + 4 * i) + 2 * w;
+      float s0, c0, s1, c1;
+      rope_sincos(t, __ldg(inv_freq + d), s0, c0);
+      rope_sincos(t, __ldg(inv_freq + d + 1), s1, c1);
+      const float a0 = __uint_as_float(lo[w] << 16), a1 = __uint_as_float(lo[w] & 0xffff0000u);
+      const float b0 = __uint_as_float(hi[w] << 16), b1 = __uint_as_float(hi[w] & 0xffff0000u);
+      lo[w] = pack_bf16(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
+      hi[w] = pack_bf16(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
+    }
+    qf[i] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    qf[i + 2] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
   }
 }
 
@@ -410,6 +449,43 @@ __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g
   if (lane == 0) a.ws_cnt[bg] = 0;  // leave the workspace re-usable
 }
 
+// Fused append: the unit holding the new token t = ctx - 1 overwrites the
+// token's (stale) K and V rows in the landed stage with k_new (rotated when
+// inv_freq is set) and v_new, and stores the same rows into the page slot.
+// Lanes 0..15: K chunk `lane` (its rotate-half partner chunk lane ^ 8 is read
+// too); lanes 16..31: V chunk lane - 16.
+__device__ __forceinline__ void patch_new_token(const KArgs& a, uint32_t sk, int b, int g, int ctx, int lane) {
+  const int t = ctx - 1, slot = t % kTileTokens, ch = lane & 15;
+  const bool is_k = lane < 16;
+  const uint16_t* src = (is_k ? a.k_new : a.v_new) + (static_cast<int64_t>(b) * a.hkv + g) * kHeadDim;
+  uint4 val = __ldg(reinterpret_cast<const uint4*>(src + 8 * ch));
+  if (is_k && a.inv_freq) {
+    const uint4 par = __ldg(reinterpret_cast<const uint4*>(src + 8 * (ch ^ 8)));
+    const uint32_t x[4] = {val.x, val.y, val.z, val.w}, y[4] = {par.x, par.y, par.z, par.w};
+    uint32_t o[4];
+    const float sg = ch < 8 ? -1.f : 1.f;    // x'[i] = x c - x[i+64] s ; x'[i+64] = x[i+64] c + x[i] s
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int i = 8 * (ch & 7) + 2 * w;    // frequency index of the pair
+      float s0, c0, s1, c1;
+      rope_sincos(t, __ldg(a.inv_freq + i), s0, c0);
+      rope_sincos(t, __ldg(a.inv_freq + i + 1), s1, c1);
+      const float a0 = __uint_as_float(x[w] << 16), a1 = __uint_as_float(x[w] & 0xffff0000u);
+      const float p0 = __uint_as_float(y[w] << 16), p1 = __uint_as_float(y[w] & 0xffff0000u);
+      o[w] = pack_bf16(a0 * c0 + sg * p0 * s0, a1 * c1 + sg * p1 * s1);
+    }
+    val = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+  const uint32_t dst = (is_k ? sk : sk + kTileBytes) + swz(slot, ch);
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(val.x), "r"(val.y), "r"(val.z), "r"(val.w)
+               : "memory");
+  const int64_t pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + t / a.page_size);
+  uint16_t* page = (is_k ? a.k_pages : a.v_pages) + pid * a.page_stride +
+                   (static_cast<int64_t>(g) * a.page_size + t % a.page_size) * kHeadDim;
+  *reinterpret_cast<uint4*>(page + 8 * ch) = val;
+  __syncwarp();
+}
+
 __device__ __forceinline__ void init_ring(uint32_t bar0, int stages, int lane) {
   if (lane == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(bar0 + 8 * s, 1);
@@ -439,7 +515,7 @@ constexpr int ctas_per_sm() {
                                                                       : (220 * 1024) / (kWarps * kStages * kStageBytes + 1024);
 }
 
-template <int kWarps, int kStages, bool kStreamOnly = false>
+template <int kWarps, int kStages, bool kStreamOnly = false, bool kFuse = false>
 __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
     decode_attn_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                        const KArgs a) {
@@ -486,6 +562,7 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
     if (c == 0) write_zero_row(a, b, g, lane);
     return;
   }
+  if (kFuse && a.inv_freq && r < a.G) rope_q(qf, qd, ctx - 1, a.inv_freq);
   const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
   const int n_chunks = (ntile_total + a.chunk_tiles - 1) / a.chunk_tiles;
   if (c >= n_chunks) return;
@@ -516,6 +593,7 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
     mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
     // read the tile into registers, hand the stage back to TMA, then do the math:
     // the next load is in flight while this tile is being computed
+    if (kFuse && c == n_chunks - 1 && j == nt - 1) patch_new_token(a, sbase + s * kStageBytes, b, g, ctx, lane);
     Frags f;
     if (!kStreamOnly) load_frags(sbase + s * kStageBytes, r, qd, f);
     __syncwarp();
@@ -573,14 +651,15 @@ static bool pdl_enabled() {
   return on;
 }
 
-template <int W, int S, bool kStreamOnly = false>
+template <int W, int S, bool kStreamOnly = false, bool kFuse = false>
 static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t units,
                               cudaStream_t stream) {
   static bool configured = false;
   constexpr int smem = W * S * kStageBytes + 1024;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(decode_attn_kernel<W, S, kStreamOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(decode_attn_kernel<W, S, kStreamOnly, kFuse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_kernel)");
     configured = true;
   }
@@ -595,7 +674,7 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S, kStreamOnly>, tmk, tmv, a);
+  cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S, kStreamOnly, kFuse>, tmk, tmv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
   return NEO_OK;
@@ -639,7 +718,17 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.chunk_tiles = L.chunk_tokens / kTileTokens;
   a.max_chunks = L.max_chunks;
   a.scale_log2 = L.scale * 1.4426950408889634f;
+  a.inv_freq = L.inv_freq;
+  a.k_new = static_cast<const uint16_t*>(L.k_new);
+  a.v_new = static_cast<const uint16_t*>(L.v_new);
+  a.k_pages = static_cast<uint16_t*>(L.k_pages);
+  a.v_pages = static_cast<uint16_t*>(L.v_pages);
+  a.page_stride = L.page_stride;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
+  if (L.k_new) {   // fused append (+ RoPE): the two default shapes
+    return L.max_chunks <= 3 ? launch_unit<4, 3, false, true>(a, tmk, tmv, units, L.stream)
+                             : launch_unit<4, 2, false, true>(a, tmk, tmv, units, L.stream);
+  }
   int cfg = attn_cfg();
   if (cfg == 0) cfg = L.max_chunks <= 3 ? 43 : 42;
   switch (cfg) {

@@ -420,11 +420,12 @@ NEO_API neo_status neo_decode_attn_workspace_init(void* ws, size_t bytes, void* 
   return e == cudaSuccess ? NEO_OK : neo::cuda_fail(e, "cudaMemsetAsync(workspace)");
 }
 
-NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+static neo_status decode_attn_impl(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
                                    int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
                                    const int32_t* seq_lens, void* out, int32_t batch, int32_t hq, int32_t hkv,
                                    int32_t d, int32_t page_size, int32_t max_seq_len, float scale,
-                                   int32_t chunk_tokens, void* workspace, size_t workspace_bytes, void* stream) {
+                                   int32_t chunk_tokens, void* workspace, size_t workspace_bytes, void* stream,
+                                   const float* inv_freq, const void* k_new, const void* v_new) {
   if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
   neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, page_size);
   if (st != NEO_OK) return st;
@@ -456,7 +457,39 @@ NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const voi
   if (st != NEO_OK) return st;
   neo::AttnLaunch L{q, out, block_table, seq_lens, workspace, workspace_bytes, batch, hq, hkv, page_size,
                     max_blocks, chunk_tokens, max_chunks, scale, s};
+  if (k_new) {
+    L.inv_freq = inv_freq;
+    L.k_new = k_new;
+    L.v_new = v_new;
+    L.k_pages = const_cast<void*>(k_pages);
+    L.v_pages = const_cast<void*>(v_pages);
+    L.page_stride = page_stride;
+  }
   return neo::launch_decode_attn(L, tmk, tmv);
+}
+
+NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+                                   int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
+                                   const int32_t* seq_lens, void* out, int32_t batch, int32_t hq, int32_t hkv,
+                                   int32_t d, int32_t page_size, int32_t max_seq_len, float scale,
+                                   int32_t chunk_tokens, void* workspace, size_t workspace_bytes, void* stream) {
+  return decode_attn_impl(q, k_pages, v_pages, page_stride, num_pages, block_table, max_blocks, seq_lens, out, batch,
+                          hq, hkv, d, page_size, max_seq_len, scale, chunk_tokens, workspace, workspace_bytes, stream,
+                          nullptr, nullptr, nullptr);
+}
+
+NEO_API neo_status neo_decode_attn_append(const void* q, const float* inv_freq, const void* k_new, const void* v_new,
+                                          void* k_pages, void* v_pages, int64_t page_stride, int64_t num_pages,
+                                          const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
+                                          void* out, int32_t batch, int32_t hq, int32_t hkv, int32_t d,
+                                          int32_t page_size, int32_t max_seq_len, float scale, int32_t chunk_tokens,
+                                          void* workspace, size_t workspace_bytes, void* stream) {
+  if (batch > 0 && (!k_new || !v_new)) return fail(NEO_ERR_INVALID_ARG, "NULL k_new / v_new");
+  if (batch > 0 && (!neo::aligned16(k_new) || !neo::aligned16(v_new)))
+    return fail(NEO_ERR_INVALID_ARG, "k_new / v_new must be 16-byte aligned");
+  return decode_attn_impl(q, k_pages, v_pages, page_stride, num_pages, block_table, max_blocks, seq_lens, out, batch,
+                          hq, hkv, d, page_size, max_seq_len, scale, chunk_tokens, workspace, workspace_bytes, stream,
+                          inv_freq, k_new, v_new);
 }
 
 NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
@@ -498,8 +531,9 @@ NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const vo
   if (st != NEO_OK) return st;
   st = neo::tensor_map_prefill_kv(v_pages, page_stride, num_pages, hkv, page_size, &tmv);
   if (st != NEO_OK) return st;
+  const char* cap = std::getenv("NEO_PREFILL_CTAS");       // experiment knob: SM budget of the prefill grid
   neo::PrefillLaunch L{out, block_table, seq_lens, q_offsets, batch, hq, hkv, page_size, max_blocks, max_q_len, scale,
-                       s};
+                       s, cap ? std::atoi(cap) : 0};
   return neo::launch_prefill_attn(L, tmq, tmk, tmv);
 }
 

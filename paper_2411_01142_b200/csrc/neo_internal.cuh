@@ -34,6 +34,13 @@ struct AttnLaunch {
   int32_t batch, hq, hkv, page_size, max_blocks, chunk_tokens, max_chunks;
   float scale;
   cudaStream_t stream;
+  // fused append (+ RoPE): k_new != NULL selects decode_attn_kernel<..., kFuse>
+  const float* inv_freq = nullptr;
+  const void* k_new = nullptr;
+  const void* v_new = nullptr;
+  void* k_pages = nullptr;
+  void* v_pages = nullptr;
+  int64_t page_stride = 0;
 };
 // Byte layout of a workspace of `ws_bytes` bytes for a call shape.  The
 // completion counters occupy [0, counter_cap(ws_bytes)) -- a region fixed by the
@@ -70,6 +77,7 @@ struct PrefillLaunch {
   int32_t batch, hq, hkv, page_size, max_blocks, max_q_len;
   float scale;
   cudaStream_t stream;
+  int32_t max_ctas;   // 0: one CTA per SM
 };
 neo_status launch_prefill_attn(const PrefillLaunch& a, const CUtensorMap& tmq, const CUtensorMap& tmk,
                                const CUtensorMap& tmv);

@@ -591,7 +591,9 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   g_prefill_trace = trace;
 #endif
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(n_items, num_sms)));
+  int ctas = num_sms;
+  if (L.max_ctas > 0) ctas = std::min(ctas, L.max_ctas);   // SM budget when sharing the GPU with decode
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(n_items, ctas)));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemAlloc;
   cfg.stream = L.stream;

@@ -26,7 +26,8 @@ EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_c
             "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
             "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
             "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
-            "neo_kv_append", "neo_schedule", "neo_rope_append", "neo_prefill_append", "neo_prefill_attn"]
+            "neo_kv_append", "neo_schedule", "neo_rope_append", "neo_prefill_append", "neo_prefill_attn",
+            "neo_decode_attn_append"]
 
 
 class NeoError(RuntimeError):
@@ -73,6 +74,8 @@ def lib() -> ctypes.CDLL:
                 "neo_kv_append": [P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
                 "neo_schedule": [P, P, i32, i64, i64, P, P, P, P, P],
                 "neo_rope_append": [P, i32, P, P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
+                "neo_decode_attn_append": [P, P, P, P, P, P, i64, i64, P, i32, P, P, i32, i32, i32, i32, i32, i32,
+                                           ctypes.c_float, i32, P, sz, P],
                 "neo_prefill_attn": [P, P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, i32, i32, i32,
                                      ctypes.c_float, P],
                 "neo_prefill_append": [P, i32, P, P, P, i64, i64, P, i32, P, P, P, P, i32, i32, i32, i32, i32, P],
@@ -180,6 +183,39 @@ def decode_attn(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, *,
         int(num_pages if num_pages is not None else npages), block_table.data_ptr(), block_table.shape[1],
         seq_lens.data_ptr(), out.data_ptr(), B, hq, hkv, d, P, int(max_seq_len), float(scale), int(chunk_tokens),
         workspace.data_ptr(), workspace.numel(), _stream(stream)))
+    return out
+
+
+def decode_attn_append(q, k_pages, v_pages, block_table, seq_lens, max_seq_len, k_new, v_new, inv_freq=None,
+                       out=None, scale=None, chunk_tokens=0, workspace=None, stream=None, num_pages=None):
+    """neo_decode_attn_append: one launch that RoPE-rotates q (registers only) and
+    k_new at position seq_lens[b]-1 (inv_freq float32 [D/2] cuda, or None for a
+    plain append), stores k/v into the page slot and attends over the grown
+    context."""
+    import torch
+    for name, t in (("q", q), ("k_pages", k_pages), ("v_pages", v_pages), ("block_table", block_table),
+                    ("seq_lens", seq_lens), ("k_new", k_new), ("v_new", v_new)):
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if inv_freq is not None and (not inv_freq.is_cuda or inv_freq.dtype != torch.float32):
+        raise ValueError("inv_freq must be a float32 CUDA tensor")
+    if not (q.is_contiguous() and k_new.is_contiguous() and v_new.is_contiguous()):
+        raise ValueError("q, k_new and v_new must be contiguous")
+    B, hq, d = q.shape
+    npages, hkv, P, _ = k_pages.shape
+    if k_pages.stride()[1:] != (P * d, d, 1) or v_pages.stride() != k_pages.stride():
+        raise ValueError("each page's [Hkv][P][D] block must be contiguous, K and V alike")
+    if out is None:
+        out = torch.empty_like(q)
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)
+    if workspace is None:
+        workspace = make_workspace(B, hq, hkv, max_seq_len, chunk_tokens, device=q.device, stream=stream)
+    check(lib().neo_decode_attn_append(
+        q.data_ptr(), inv_freq.data_ptr() if inv_freq is not None else None, k_new.data_ptr(), v_new.data_ptr(),
+        k_pages.data_ptr(), v_pages.data_ptr(), k_pages.stride(0), int(num_pages if num_pages is not None else npages),
+        block_table.data_ptr(), block_table.shape[1], seq_lens.data_ptr(), out.data_ptr(), B, hq, hkv, d, P,
+        int(max_seq_len), float(scale), int(chunk_tokens), workspace.data_ptr(), workspace.numel(), _stream(stream)))
     return out
 
 

@@ -314,3 +314,71 @@ def test_rope_append_then_attend():
         kr[t] = ni.f32_to_bf16_bits(orope.rope(ni.bf16_bits_to_f64(k_new[b]), t, f).astype(np.float32))
         ref = oracle.decode_attention(qr, kr, case.v_req[b], np.float32(case.scale))
         assert within_tol(got[b], ref)[0]
+
+
+@pytest.mark.parametrize("chunk", [0, 64])
+def test_decode_attn_append_plain_equals_separate(chunk):
+    """neo_decode_attn_append without RoPE == neo_kv_append + neo_decode_attn, bit
+    for bit (output and the appended page slots), the new slots poisoned first."""
+    import torch
+    from paper_2411_01142_b200 import neo
+    ctx_new = [1, 16, 17, 300, 1025, 2048]
+    a = Case(ctx_new, 32, 8, seed=81)
+    b = Case(ctx_new, 32, 8, seed=81)
+    k_new = np.stack([a.k_req[i][n - 1] for i, n in enumerate(ctx_new)])
+    v_new = np.stack([a.v_req[i][n - 1] for i, n in enumerate(ctx_new)])
+    kn = torch.from_numpy(k_new.view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(v_new.view(np.int16)).cuda().view(torch.bfloat16)
+    for c in (a, b):
+        for i, n in enumerate(ctx_new):
+            t = n - 1
+            c.k_dev[c.table[i, t // c.P], :, t % c.P] = float("nan")
+            c.v_dev[c.table[i, t // c.P], :, t % c.P] = float("nan")
+    neo.kv_append(a.k_dev, a.v_dev, a.bt_dev, a.sl_dev, kn, vn)
+    ref = a.run(chunk_tokens=chunk)
+    got = neo.decode_attn_append(b.q_dev, b.k_dev, b.v_dev, b.bt_dev, b.sl_dev, b.max_seq_len, kn, vn,
+                                 chunk_tokens=chunk, scale=b.scale)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
+    for i, n in enumerate(ctx_new):
+        t = n - 1
+        for pa, pb in ((a.k_dev, b.k_dev), (a.v_dev, b.v_dev)):
+            assert torch.equal(pa[a.table[i, t // a.P], :, t % a.P].view(torch.int16),
+                               pb[b.table[i, t // b.P], :, t % b.P].view(torch.int16))
+
+
+@pytest.mark.parametrize("chunk,P", [(0, 16), (64, 16), (0, 32)])
+def test_decode_attn_append_rope_vs_oracle(chunk, P):
+    """The one-launch decode step with RoPE: output within tolerance of the oracle
+    over the fp64-rotated q and k (bf16-rounded), the page slot's k within
+    tolerance of the rotated k_new, v bit-exact."""
+    import torch
+    from oracle import rope as orope
+    import oracle
+    from paper_2411_01142_b200 import neo
+    ctx_new = [1, 17, 300, 4096, 700]
+    case = Case(ctx_new, 32, 8, P=P, seed=91 + P)
+    f = orope.llama_inv_freq()
+    k_new = np.stack([case.k_req[b][n - 1] for b, n in enumerate(ctx_new)])
+    v_new = np.stack([case.v_req[b][n - 1] for b, n in enumerate(ctx_new)])
+    kn = torch.from_numpy(k_new.view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(v_new.view(np.int16)).cuda().view(torch.bfloat16)
+    q_before = case.q_dev.clone()
+    out = neo.decode_attn_append(case.q_dev, case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.max_seq_len, kn,
+                                 vn, inv_freq=torch.from_numpy(f).cuda(), chunk_tokens=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(case.q_dev.view(torch.int16), q_before.view(torch.int16))     # q not written back
+    got = case.out_f64(out)
+    for b, n in enumerate(ctx_new):
+        t = n - 1
+        kr = ni.f32_to_bf16_bits(orope.rope(ni.bf16_bits_to_f64(k_new[b]), t, f).astype(np.float32))
+        k_pg = case.k_dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        assert within_tol(ni.bf16_bits_to_f64(k_pg), ni.bf16_bits_to_f64(kr))[0]
+        v_pg = case.v_dev[case.table[b, t // P], :, t % P].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(v_pg, v_new[b])
+        qr = ni.f32_to_bf16_bits(orope.rope(ni.bf16_bits_to_f64(case.q[b]), t, f).astype(np.float32))
+        kreq = case.k_req[b].copy()
+        kreq[t] = kr
+        ref = oracle.decode_attention(qr, kreq, case.v_req[b], np.float32(case.scale))
+        ok, ratio = within_tol(got[b], ref)
+        assert ok, (b, n, ratio)

@@ -129,3 +129,43 @@ def test_prefill_parity_many_ragged_requests():
     q_lens = np.minimum(ctx, rng.integers(0, 300, 40))
     q_lens[::7] = 0
     check_prefill(PrefillCase(ctx.tolist(), q_lens.tolist(), 32, 8, seed=601), "ragged40")
+
+
+def test_prefill_cuda_graph_matches_eager():
+    """neo_prefill_append (RoPE) + neo_prefill_attn -- PDL launches, persistent
+    grid -- captured in a CUDA graph and replayed give the eager bits."""
+    import torch
+    from oracle import rope as orope
+    from paper_2411_01142_b200 import neo
+    ctx = [300, 77, 1000]
+    case = PrefillCase(ctx, [300, 40, 1000], 32, 8, seed=700)
+    inv = torch.from_numpy(orope.llama_inv_freq()).cuda()
+    kn = torch.zeros(case.T, 8, 128, dtype=torch.bfloat16, device="cuda").normal_(generator=torch.Generator("cuda").manual_seed(1))
+    vn = torch.zeros_like(kn).normal_(generator=torch.Generator("cuda").manual_seed(2))
+    q = case.qp_dev.clone()
+    out = torch.empty_like(q)
+
+    def step(stream=None):
+        q.copy_(case.qp_dev)
+        neo.prefill_append(case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.qo_dev, kn, vn, q=q, inv_freq=inv,
+                           stream=stream)
+        neo.prefill_attn(q, case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.qo_dev, case.max_q_len, out=out,
+                         stream=stream)
+
+    step()
+    torch.cuda.synchronize()
+    eager = out.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step(s)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step(torch.cuda.current_stream())
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), eager.view(torch.int16))

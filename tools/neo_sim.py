@@ -5,7 +5,7 @@ GPU-only baseline is the same scheduler with no CPU-cache (NEO degenerates to
 vLLM-style GPU-only serving).  Offline synthetic workload per P:364: input and
 output lengths uniform in [0.9 l, 1.1 l].
 
-python tools/neo_sim.py [profile.json] [n_requests] [l_in] [l_out]"""
+python tools/neo_sim.py [profile.json] [n_requests] [l_in] [l_out] [cpu_speedup]"""
 import json
 import os
 import sys
@@ -117,6 +117,9 @@ def main():
     l_in = int(sys.argv[3]) if len(sys.argv) > 3 else 1000
     l_out = int(sys.argv[4]) if len(sys.argv) > 4 else 300
     prof = json.load(open(path))
+    speedup = float(sys.argv[5]) if len(sys.argv) > 5 else 1.0
+    if speedup != 1.0:                   # hypothetical host: CPU attention `speedup` x faster
+        prof = dict(prof, cdec=[[k, t / speedup] for k, t in prof["cdec"]])
     rng = np.random.default_rng(7)
     lo_i, hi_i = (9 * l_in + 9) // 10, (11 * l_in) // 10
     lo_o, hi_o = (9 * l_out + 9) // 10, (11 * l_out) // 10
@@ -124,7 +127,7 @@ def main():
     page_bytes = prof["page_size"] * prof["kv_bytes_per_token_layer"] * prof["L"]
     cpu_pages = int(512e9 // page_bytes)
     print(f"{prof['model']} on {prof['gpu']}: {n} requests, input ~{l_in}, output ~{l_out}; "
-          f"CPU-cache 512 GB ({prof.get('host_threads')} host threads)")
+          f"CPU-cache 512 GB ({prof.get('host_threads')} host threads, CPU attention x{speedup:g})")
     # GPU-only + swap: same scheduler and CPU-cache, CPU attention priced out of
     # reach, so CPU-resident requests only wait to be swapped back in (the
     # vLLM-with-swap-space baseline); its gap to NEO isolates CPU attention.

@@ -5,7 +5,8 @@ profiles/cost_profile_b200_llama8b.json:
   lin   linear stage per layer (QKV, O, gate/up, down GEMMs: library cuBLAS via
         torch.matmul -- a cost-table measurement, not part of the hot path)
   gdec  GPU decode attention per layer: our neo_decode_attn over batches of ~1K contexts
-  gpre  prefill attention per layer: torch SDPA (flash, causal), fitted to a t^2 + b t
+  gpre  prefill attention per layer: our neo_prefill_attn (paged, causal, one
+        whole prompt of t tokens), fitted to a t^2 + b t
   cdec  CPU decode attention per layer: our neo_cpu_decode_attn on the host cores
   pcie  pinned D2H memcpy bandwidth
 
@@ -77,11 +78,17 @@ def gdec_table():
 
 def gpre_fit():
     pts = []
+    P = 16
     for t in (128, 256, 512, 1024, 2048, 4096):
-        q = torch.randn(1, HQ, t, D, dtype=torch.bfloat16, device="cuda")
-        k = torch.randn(1, HQ, t, D, dtype=torch.bfloat16, device="cuda")
-        v = torch.randn(1, HQ, t, D, dtype=torch.bfloat16, device="cuda")
-        pts.append((t, gpu_time(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True))))
+        npg = (t + P - 1) // P
+        kp = torch.randn(npg, HKV, P, D, dtype=torch.bfloat16, device="cuda")
+        vp = torch.randn(npg, HKV, P, D, dtype=torch.bfloat16, device="cuda")
+        bt = torch.arange(npg, dtype=torch.int32, device="cuda").view(1, -1)
+        sl = torch.tensor([t], dtype=torch.int32, device="cuda")
+        qo = torch.tensor([0, t], dtype=torch.int32, device="cuda")
+        q = torch.randn(t, HQ, D, dtype=torch.bfloat16, device="cuda")
+        o = torch.empty_like(q)
+        pts.append((t, gpu_time(lambda: neo.prefill_attn(q, kp, vp, bt, sl, qo, t, out=o))))
     ts = np.array([p[0] for p in pts], dtype=np.float64)
     ys = np.array([p[1] for p in pts])
     A = np.stack([ts * ts, ts], axis=1)
@@ -127,7 +134,7 @@ def main():
             "lin": lin, "gdec": gdec, "gpre_a": a, "gpre_b": b, "gpre_points": pre, "cdec": cdec,
             "page_size": 16, "max_batch_tokens": 8192, "pcie_bytes_per_s": bw,
             "kv_bytes_per_token_layer": HKV * D * 2 * 2,
-            "note": "lin: cuBLAS GEMMs of one LLaMa-3.1-8B layer; gdec: neo_decode_attn; gpre: torch SDPA causal; "
+            "note": "lin: cuBLAS GEMMs of one LLaMa-3.1-8B layer; gdec: neo_decode_attn; gpre: neo_prefill_attn; "
                     "cdec: neo_cpu_decode_attn; t_prl/t_pol assumed (embedding, LM head)"}
     path = os.environ.get("NEO_PROFILE_OUT") or os.path.join(ROOT, "profiles", "cost_profile_b200_llama8b.json")
     json.dump(prof, open(path, "w"), indent=1)
