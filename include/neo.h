@@ -199,7 +199,7 @@ NEO_API neo_status neo_rope_append(void* q_inout, int32_t num_q_heads, const flo
  *   out[j][h][:] = sum_{t <= p} softmax_t(scale * q[j][h] . K_b[t][g]) V_b[t][g][:]
  * K_b[t] lives in page block_table[b][t / P], slot t % P (as neo_decode_attn).
  * The new tokens' K/V must already be in the pages (neo_prefill_append).
- *   q, out     [total_tokens][Hq][D] bf16 device, 16-byte aligned
+ *   q, out     [total_tokens][Hq][D] bf16 device; q 16-byte, out 32-byte aligned
  *   q_offsets  device int32[batch + 1], 0 = q_offsets[0] <= ... = total_tokens
  *   max_q_len  >= every n_q (sizes the grid; rows beyond a request's n_q idle)
  *   G = Hq / Hkv in {1, 2, 4, 8, 16}; D = 128; P a multiple of 16;

@@ -508,8 +508,9 @@ NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const vo
     return fail(NEO_ERR_UNSUPPORTED, "prefill: batch <= 512 and max_q_len * G <= 262144 per call");
   if (!q || !k_pages || !v_pages || !block_table || !seq_lens || !q_offsets || !out)
     return fail(NEO_ERR_INVALID_ARG, "NULL pointer argument");
-  if (!neo::aligned16(q) || !neo::aligned16(k_pages) || !neo::aligned16(v_pages) || !neo::aligned16(out))
-    return fail(NEO_ERR_INVALID_ARG, "q, pages and out must be 16-byte aligned");
+  if (!neo::aligned16(q) || !neo::aligned16(k_pages) || !neo::aligned16(v_pages) ||
+      (reinterpret_cast<uintptr_t>(out) & 31u))
+    return fail(NEO_ERR_INVALID_ARG, "q and pages must be 16-byte aligned, out 32-byte aligned");
   if (page_stride % 8 != 0 || page_stride < static_cast<int64_t>(hkv) * page_size * d)
     return fail(NEO_ERR_INVALID_ARG, "page_stride must be a multiple of 8 elements and >= Hkv*P*D");
   if (num_pages < 1 || max_blocks < 1 || max_q_len < 1)

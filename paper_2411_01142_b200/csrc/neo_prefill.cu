@@ -67,7 +67,7 @@ struct PArgs {
   int32_t batch, hq, hkv, G, page_size, max_blocks, n_ct_max;
   float scale_log2;
 #ifdef NEO_PREFILL_TRACE
-  long long* trace;   // [2 tiles][64 steps][8] clock64 stamps of CTA 0 (tools/prefill_trace.py)
+  long long* trace;   // [2 tiles][64 steps][16] clock64 stamps of CTA 0 (tools/prefill_trace.py)
 #endif
 };
 
@@ -77,7 +77,7 @@ long long* g_prefill_trace = nullptr;
 namespace {
 #define TRACE(t, j, slot)                                                                          \
   do {                                                                                            \
-    if (blockIdx.x == 0 && (j) < 64) a.trace[((t) * 64 + (j)) * 8 + (slot)] = clock64();           \
+    if (blockIdx.x == 0 && (j) < 64) a.trace[((t) * 64 + (j)) * 16 + (slot)] = clock64();           \
   } while (0)
 #else
 #define TRACE(t, j, slot) \
@@ -407,9 +407,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < kTiles; ++t) {
           const int ntt = t ? it.nt1 : it.nt0;
           if (j >= ntt) continue;
-          if (lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 4);
+          if (lane == 0) TRACE(t, t ? pc1 : pc0, 4);
           mbar_wait(bar(kBarPFull + t), (t ? pc1 : pc0) & 1);
-          if (lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 5);
+          if (lane == 0) TRACE(t, t ? pc1 : pc0, 5);
           if (t) ++pc1;
           else ++pc0;
           const bool more = j + 1 < ntt;
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (more) {
             issue_s(t, kc % kStages);
             umma::commit_elect(bar(kBarSFull + t));
-            if (lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 6);
+            if (lane == 0) TRACE(t, (t ? pc1 : pc0) - 1, 6);
             if (last_v) {
               umma::commit_elect(bar(kBarKEmpty + kc % kStages));
               if (j + 2 == nt) umma::commit_elect(bar(kBarQEmpty));   // last S of the item
@@ -451,15 +451,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int my_nt = t ? it.nt1 : it.nt0;
       if (my_nt == 0) continue;
       const int i_row = it.i0 + t * rows_tok + r / G;
-      const bool valid_row = i_row < it.q_len;
       const int pos = it.ctx - it.q_len + min(i_row, it.q_len - 1);
       float m = -INFINITY;
       uint64_t l2 = f2(0.f, 0.f);                   // row sum, two partial lanes
       for (int j = 0; j < my_nt; ++j, ++sc) {
-        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 0);
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 0);
+        if (quarter == 0 && lane == 0 && j == 0) TRACE(t, sc, 7);     // item start
         mbar_wait(bar(kBarSFull + t), sc & 1);
         umma::fence_after_sync();
-        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 1);
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 1);
         float s[kBN];
         {
           uint32_t u[32];
@@ -471,13 +471,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < 32; ++c) s[c0 + c] = __uint_as_float(u[c]);
           }
         }
-        const int kv0 = j * kBN;
-        if (kv0 + kBN - 1 > pos) {
+        const int lim = pos - j * kBN;               // last visible column of this row in the tile
+        if (lim < kBN - 1) {
 #pragma unroll
-          for (int c = 0; c < kBN; ++c)
-            if (kv0 + c > pos) s[c] = -INFINITY;
+          for (int c = 0; c < kBN; ++c) s[c] = c > lim ? -INFINITY : s[c];
         }
-        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 2);
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 2);
         float mx = s[0];
 #pragma unroll
         for (int c = 1; c < kBN; ++c) mx = fmaxf(mx, s[c]);
@@ -526,36 +525,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         umma::wait_st();
         umma::fence_before_sync();
         __syncwarp();
-        if (quarter == 0 && lane == 0 && k == static_cast<int>(blockIdx.x)) TRACE(t, j, 3);
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 3);
         if (lane == 0) mbar_arrive(bar(kBarPFull + t));
       }
       // epilogue: O / l -> bf16 (the next item's first PV on this tile waits for
       // this warpgroup's next P, so O stays intact until read)
+      if (quarter == 0 && lane == 0) TRACE(t, sc - 1, 8);
       mbar_wait(bar(kBarODone + t), oc & 1);
       ++oc;
       umma::fence_after_sync();
+      if (quarter == 0 && lane == 0) TRACE(t, sc - 1, 9);
       const float2 lp = unf2(l2);
       const float inv_l = 1.f / (lp.x + lp.y);
-      uint16_t* orow =
-          a.out + (static_cast<int64_t>(it.q0 + min(i_row, it.q_len - 1)) * a.hq + it.g * G + r % G) * 128;
+      // 32-byte stores (full sectors): each thread writes its 256-byte row
+      const int tok = it.i0 + t * rows_tok + r / G;
+      uint16_t* orow = a.out + (static_cast<int64_t>(it.q0 + min(tok, it.q_len - 1)) * a.hq + it.g * G + r % G) * 128;
 #pragma unroll 1
       for (int c0 = 0; c0 < 128; c0 += 32) {
         uint32_t o[32];
         umma::ld32(tO + c0, o);
         umma::wait_ld();
-        if (valid_row) {
+        if (tok < it.q_len) {
 #pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(o[c + 0]) * inv_l, __uint_as_float(o[c + 1]) * inv_l);
-            v.y = pack_bf16(__uint_as_float(o[c + 2]) * inv_l, __uint_as_float(o[c + 3]) * inv_l);
-            v.z = pack_bf16(__uint_as_float(o[c + 4]) * inv_l, __uint_as_float(o[c + 5]) * inv_l);
-            v.w = pack_bf16(__uint_as_float(o[c + 6]) * inv_l, __uint_as_float(o[c + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + c0 + c) = v;
+          for (int c = 0; c < 32; c += 16) {
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              w[e] = pack_bf16(__uint_as_float(o[c + 2 * e]) * inv_l, __uint_as_float(o[c + 2 * e + 1]) * inv_l);
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c0 + c), "r"(w[0]),
+                         "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                         : "memory");
           }
         }
       }
       umma::fence_before_sync();
+      if (quarter == 0 && lane == 0) TRACE(t, sc - 1, 10);
     }
   }
   umma::fence_before_sync();
@@ -585,8 +589,8 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
           L.page_size, L.max_blocks, n_ct_max, L.scale * 1.4426950408889634f};
 #ifdef NEO_PREFILL_TRACE
   static long long* trace = nullptr;
-  if (!trace) cudaMalloc(&trace, 2 * 64 * 8 * sizeof(long long));
-  cudaMemsetAsync(trace, 0, 2 * 64 * 8 * sizeof(long long), L.stream);
+  if (!trace) cudaMalloc(&trace, 2 * 64 * 16 * sizeof(long long));
+  cudaMemsetAsync(trace, 0, 2 * 64 * 16 * sizeof(long long), L.stream);
   a.trace = trace;
   g_prefill_trace = trace;
 #endif
