@@ -186,6 +186,8 @@ constexpr int kMaxSchedBatch = 512, kMaxSchedLevels = 1024;
 struct Sched {
   int req[kMaxSchedBatch];
   int pref[kMaxSchedLevels + 1];
+  int q_off[kMaxSchedBatch + 1];   // q_offsets and seq_lens cached: item lookup stays in shared memory
+  int ctx[kMaxSchedBatch];
 };
 
 __device__ __forceinline__ int tiles_of_request(const PArgs& a, int b, int rows_tok) {
@@ -195,7 +197,12 @@ __device__ __forceinline__ int tiles_of_request(const PArgs& a, int b, int rows_
 
 // all threads of the CTA; ends with __syncthreads
 __device__ void build_sched(const PArgs& a, int rows_tok, Sched& sc, int* nct_tmp) {
-  for (int b = threadIdx.x; b < a.batch; b += blockDim.x) nct_tmp[b] = tiles_of_request(a, b, rows_tok);
+  for (int b = threadIdx.x; b < a.batch; b += blockDim.x) {
+    nct_tmp[b] = tiles_of_request(a, b, rows_tok);
+    sc.q_off[b] = a.q_offsets[b];
+    sc.ctx[b] = a.seq_lens[b];
+  }
+  if (threadIdx.x == 0) sc.q_off[a.batch] = a.q_offsets[a.batch];
   __syncthreads();
   for (int b = threadIdx.x; b < a.batch; b += blockDim.x) {
     const int n = nct_tmp[b];
@@ -225,9 +232,9 @@ __device__ __forceinline__ void make_item(const PArgs& a, const Sched& sc, int k
   const int r = k - sc.pref[lo];
   it.b = sc.req[r / a.hkv];
   it.g = r % a.hkv;
-  it.q0 = a.q_offsets[it.b];
-  it.q_len = a.q_offsets[it.b + 1] - it.q0;
-  it.ctx = a.seq_lens[it.b];
+  it.q0 = sc.q_off[it.b];
+  it.q_len = sc.q_off[it.b + 1] - it.q0;
+  it.ctx = sc.ctx[it.b];
   it.i0 = ct * kTiles * rows_tok;
   const int f0 = it.i0, f1 = it.i0 + rows_tok;
   it.nt0 = (it.ctx - it.q_len + min(f0 + rows_tok, it.q_len) - 1) / kBN + 1;
