@@ -43,7 +43,7 @@ static bool debug_validate_enabled() {
 // ----------------------------------------------------------------- tensor maps
 namespace {
 
-enum TmKind : int32_t { kTmDecodeKV = 0, kTmPrefillKV = 1, kTmPrefillQ = 2 };
+enum TmKind : int32_t { kTmDecodeKV = 0, kTmPrefillKV = 1, kTmPrefillQ = 2, kTmPrefillOut = 3 };
 
 struct TmKey {
   const void* ptr;
@@ -138,6 +138,16 @@ neo_status tensor_map_prefill_q(const void* ptr, int32_t total_tokens, int32_t h
   const cuuint64_t strides[3] = {256, static_cast<cuuint64_t>(hq) * 256, 128};
   const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(G), static_cast<cuuint32_t>(128 / G), 1};
   return encode_cached(TmKey{ptr, total_tokens, hq, G, 0, kTmPrefillQ}, 4, dims, strides, box, out);
+}
+
+// Prefill output out[T][Hq][128] for TMA tensor stores: {64 el, Hq, T, 2 halves}
+// with box {64, G, 1, 1} -- one store = one dim-half of the G rows of one token
+// (never past the request's rows), from shared memory in the SW128 layout.
+neo_status tensor_map_prefill_out(void* ptr, int32_t total_tokens, int32_t hq, int32_t G, CUtensorMap* out) {
+  const cuuint64_t dims[4] = {64, static_cast<cuuint64_t>(hq), static_cast<cuuint64_t>(total_tokens), 2};
+  const cuuint64_t strides[3] = {256, static_cast<cuuint64_t>(hq) * 256, 128};
+  const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(G), 1, 1};
+  return encode_cached(TmKey{ptr, total_tokens, hq, G, 0, kTmPrefillOut}, 4, dims, strides, box, out);
 }
 
 namespace {
@@ -533,9 +543,12 @@ NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const vo
   st = neo::tensor_map_prefill_kv(v_pages, page_stride, num_pages, hkv, page_size, &tmv);
   if (st != NEO_OK) return st;
   const char* cap = std::getenv("NEO_PREFILL_CTAS");       // experiment knob: SM budget of the prefill grid
+  CUtensorMap tmo;
+  st = neo::tensor_map_prefill_out(out, total_tokens, hq, G, &tmo);
+  if (st != NEO_OK) return st;
   neo::PrefillLaunch L{out, block_table, seq_lens, q_offsets, batch, hq, hkv, page_size, max_blocks, max_q_len, scale,
                        s, cap ? std::atoi(cap) : 0};
-  return neo::launch_prefill_attn(L, tmq, tmk, tmv);
+  return neo::launch_prefill_attn(L, tmq, tmk, tmv, tmo);
 }
 
 NEO_API neo_status neo_kv_append(void* k_pages, void* v_pages, int64_t page_stride, int64_t num_pages,

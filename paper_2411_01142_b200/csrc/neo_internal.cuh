@@ -67,6 +67,7 @@ neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, i
 neo_status tensor_map_prefill_kv(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,
                                  CUtensorMap* out);
 neo_status tensor_map_prefill_q(const void* ptr, int32_t total_tokens, int32_t hq, int32_t G, CUtensorMap* out);
+neo_status tensor_map_prefill_out(void* ptr, int32_t total_tokens, int32_t hq, int32_t G, CUtensorMap* out);
 
 // ---- prefill attention (neo_prefill.cu)
 struct PrefillLaunch {
@@ -80,7 +81,7 @@ struct PrefillLaunch {
   int32_t max_ctas;   // 0: one CTA per SM
 };
 neo_status launch_prefill_attn(const PrefillLaunch& a, const CUtensorMap& tmq, const CUtensorMap& tmk,
-                               const CUtensorMap& tmv);
+                               const CUtensorMap& tmv, const CUtensorMap& tmo);
 
 // ---- KV append (neo_swap.cu)
 neo_status launch_append(uint16_t* k, uint16_t* v, int64_t page_stride, const int32_t* block_table, int32_t max_blocks,

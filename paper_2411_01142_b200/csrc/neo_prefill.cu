@@ -174,6 +174,9 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 // One work item = (request b, kv-head g, CTA tile ct: 2 x 128 rows).
 struct Item {
   int b, g, q0, q_len, ctx, i0, nt0, nt1;
+  // epilogue through shared memory + TMA stores: tile 0 stages in the last K
+  // stage, tile 1 in the last V stage; both tiles must end on the same key tile
+  __device__ __forceinline__ bool staged() const { return nt1 == 0 || nt0 == nt1; }
 };
 
 // Dense longest-first item list, built per CTA in shared memory by the
@@ -246,7 +249,8 @@ __device__ __forceinline__ void make_item(const PArgs& a, const Sched& sc, int k
 // items, so one item's epilogue overlaps the next item's loads and first S.
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_attn_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
-                        const __grid_constant__ CUtensorMap tmv, const PArgs a) {
+                        const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmo,
+                        const PArgs a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bars[kNumBars];
   __shared__ uint32_t tmem_sh;
@@ -388,7 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         issue_s(1, kc % kStages);
         umma::commit_elect(bar(kBarSFull + 1));
       }
-      umma::commit_elect(bar(kBarKEmpty + kc % kStages));  // K tile consumed once these S complete
+      if (!(nt == 1 && it.staged()))                      // staged: tile 0's epilogue releases K_last
+        umma::commit_elect(bar(kBarKEmpty + kc % kStages));  // K tile consumed once these S complete
       if (nt == 1) umma::commit_elect(bar(kBarQEmpty));    // last S of the item: Q free
       __syncwarp();
       ++kc;
@@ -427,13 +432,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma::fence_after_sync();
           issue_pv(t, st, ksteps, j > 0);
           const bool last_v = t == kTiles - 1 || j >= it.nt1;   // no later tile reads V_j / K_{j+1}
-          if (last_v) umma::commit_elect(bar(kBarVEmpty + st));
+          // staged: tile 1's epilogue releases V_last (and tile 0's K_last, below)
+          if (last_v && !(j == nt - 1 && it.staged() && it.nt1 > 0)) umma::commit_elect(bar(kBarVEmpty + st));
           if (more) {
             issue_s(t, kc % kStages);
             umma::commit_elect(bar(kBarSFull + t));
             if (lane == 0) TRACE(t, (t ? pc1 : pc0) - 1, 6);
             if (last_v) {
-              umma::commit_elect(bar(kBarKEmpty + kc % kStages));
+              if (!(j + 2 == nt && it.staged())) umma::commit_elect(bar(kBarKEmpty + kc % kStages));
               if (j + 2 == nt) umma::commit_elect(bar(kBarQEmpty));   // last S of the item
             }
           } else {
@@ -452,10 +458,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tO = tS + kColO;
     const float sl = a.scale_log2;
     uint32_t sc = 0, oc = 0;                         // S tiles and items consumed so far
+    uint32_t kbase = 0;                              // K/V tiles of earlier items (ring position)
     for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
       Item it;
       make_item(a, sched, k, rows_tok, it);
       const int my_nt = t ? it.nt1 : it.nt0;
+      const int nt_item = max(it.nt0, it.nt1);
+      kbase += nt_item;
       if (my_nt == 0) continue;
       const int i_row = it.i0 + t * rows_tok + r / G;
       const int pos = it.ctx - it.q_len + min(i_row, it.q_len - 1);
@@ -544,6 +553,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (quarter == 0 && lane == 0) TRACE(t, sc - 1, 9);
       const float2 lp = unf2(l2);
       const float inv_l = 1.f / (lp.x + lp.y);
+      if (it.staged()) {
+        // Stage the tile's rows in the freed last K (tile 0) / V (tile 1) stage
+        // in TMA's SW128 layout (conflict-free 16-byte stores), then one TMA
+        // tensor store per token and dim-half; rows past q_len are never written.
+        const int st_last = static_cast<int>((kbase - 1) % kStages);
+        const uint32_t buf = sb + kOffK + st_last * kStageBytes + (t ? 2 * kKVHalf : 0);
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t o[32];
+          umma::ld32(tO + c0, o);
+          umma::wait_ld();
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int ch = c0 / 8 + q4;                // 16-byte chunk 0..15 of the row
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              w[e] = pack_bf16(__uint_as_float(o[8 * q4 + 2 * e]) * inv_l,
+                               __uint_as_float(o[8 * q4 + 2 * e + 1]) * inv_l);
+            sts128(buf + (ch >> 3) * kKVHalf + umma::sw128_off(r, ch & 7), w[0], w[1], w[2], w[3]);
+          }
+        }
+        umma::fence_proxy_async_smem();
+        __syncwarp();
+        const int tpw = 32 / G;                        // tokens of this warp's 32 rows
+        for (int e = lane; e < 2 * tpw; e += 32) {
+          const int kk = e >> 1, h = e & 1;
+          const int tok = it.i0 + t * rows_tok + quarter * tpw + kk;
+          if (tok < it.q_len) {
+            const uint32_t src = buf + h * kKVHalf + (quarter * 32 + kk * G) * 128;
+            asm volatile(
+                "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                    reinterpret_cast<uint64_t>(&tmo)),
+                "r"(0), "r"(it.g * G), "r"(it.q0 + tok), "r"(h), "r"(src)
+                : "memory");
+          }
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // stage read: may be reused
+        // the 4 warps of this tile done -> release the stage to the producer
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+        if (quarter == 0 && lane == 0) mbar_arrive(bar((t ? kBarVEmpty : kBarKEmpty) + st_last));
+      } else {
       // 32-byte stores (full sectors): each thread writes its 256-byte row
       const int tok = it.i0 + t * rows_tok + r / G;
       uint16_t* orow = a.out + (static_cast<int64_t>(it.q0 + min(tok, it.q_len - 1)) * a.hq + it.g * G + r % G) * 128;
@@ -565,10 +617,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      }
       umma::fence_before_sync();
       if (quarter == 0 && lane == 0) TRACE(t, sc - 1, 10);
     }
   }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // output stores complete
   umma::fence_before_sync();
   __syncthreads();
   if (warp == kMmaWarp) umma::tmem_dealloc(tmem, kTmemCols);
@@ -577,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, const CUtensorMap& tmk,
-                               const CUtensorMap& tmv) {
+                               const CUtensorMap& tmv, const CUtensorMap& tmo) {
   static int num_sms = 0;
   if (!num_sms) {
     cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
@@ -613,7 +667,7 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, prefill_attn_kernel, tmq, tmk, tmv, a);
+  cudaLaunchKernelEx(&cfg, prefill_attn_kernel, tmq, tmk, tmv, tmo, a);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? NEO_OK : cuda_fail(e, "prefill attention kernel launch");
 }
