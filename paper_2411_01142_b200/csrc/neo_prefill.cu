@@ -177,6 +177,14 @@ struct Item {
   // epilogue through shared memory + TMA stores: tile 0 stages in the last K
   // stage, tile 1 in the last V stage; both tiles must end on the same key tile
   __device__ __forceinline__ bool staged() const { return nt1 == 0 || nt0 == nt1; }
+  // tile 1 stages in the last V stage only if the MMA warp did not zero a page
+  // tail there (keeps every shared-memory write pair ordered by thread-level
+  // barriers, not only through tcgen05.commit)
+  __device__ __forceinline__ bool staged_v() const {
+    const int nt = nt0 > nt1 ? nt0 : nt1;
+    const int nvalid = min(kBN, ctx - (nt - 1) * kBN);
+    return nt1 > 0 && nt0 == nt1 && (nvalid & 15) == 0;
+  }
 };
 
 // Dense longest-first item list, built per CTA in shared memory by the
@@ -433,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           issue_pv(t, st, ksteps, j > 0);
           const bool last_v = t == kTiles - 1 || j >= it.nt1;   // no later tile reads V_j / K_{j+1}
           // staged: tile 1's epilogue releases V_last (and tile 0's K_last, below)
-          if (last_v && !(j == nt - 1 && it.staged() && it.nt1 > 0)) umma::commit_elect(bar(kBarVEmpty + st));
+          if (last_v && !(j == nt - 1 && it.staged_v())) umma::commit_elect(bar(kBarVEmpty + st));
           if (more) {
             issue_s(t, kc % kStages);
             umma::commit_elect(bar(kBarSFull + t));
@@ -553,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (quarter == 0 && lane == 0) TRACE(t, sc - 1, 9);
       const float2 lp = unf2(l2);
       const float inv_l = 1.f / (lp.x + lp.y);
-      if (it.staged()) {
+      if (t == 0 ? it.staged() : it.staged_v()) {
         // Stage the tile's rows in the freed last K (tile 0) / V (tile 1) stage
         // in TMA's SW128 layout (conflict-free 16-byte stores), then one TMA
         // tensor store per token and dim-half; rows past q_len are never written.
