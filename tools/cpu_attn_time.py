@@ -1,4 +1,7 @@
-"""Time neo_cpu_decode_attn (NEXT-2) on this host: python tools/cpu_attn_time.py [n_req] [ctx] [threads...]"""
+"""Time neo_cpu_decode_attn (NEXT-2) on this host:
+    python tools/cpu_attn_time.py [n_req] [ctx] [threads...]
+NEO_CPU_SEQ=1 lays the request's pages out in order (sequential host block
+table) instead of the random page ids of a fragmented CPU-cache."""
 import math
 import os
 import sys
@@ -16,6 +19,12 @@ threads = [int(x) for x in sys.argv[3:]] or [0]
 hq, hkv, P = 32, 8, 16
 ctx = ni.ctx_uniform(1, B, l)
 table, nh = ni.block_tables(1, ctx, P)
+if os.environ.get("NEO_CPU_SEQ") == "1":       # pages of each request contiguous and in order
+    o = 0
+    for b in range(B):
+        n = (int(ctx[b]) + P - 1) // P
+        table[b, :n] = np.arange(o, o + n)
+        o += n
 host = np.zeros((nh, 1, 2, hkv, P, 128), dtype=np.uint16)
 rng = np.random.default_rng(0)
 host[...] = rng.integers(0x3c00, 0x3f80, size=host.shape, dtype=np.uint16)
