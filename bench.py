@@ -176,7 +176,8 @@ def run_neo(args):
     gb = GpuBatch(wl, ctx=ctx_all, req_ids=req_ids, kv_heads=kvh, q_heads=qh)
     L = layers_per_step(wl)
     stream = torch.cuda.current_stream()
-    chunk = args.chunk or neo.default_chunk(gb.B, gb.hkv, gb.max_seq_len)
+    # a0 plan from the host-known lengths (NEO's scheduler holds them)
+    chunk = args.chunk or neo.plan_chunk(gb.ctx, gb.hkv, gb.P)
     ws = neo.make_workspace(gb.B, gb.hq, gb.hkv, gb.max_seq_len, chunk)
     out = torch.empty(L, gb.B, gb.hq, 128, dtype=torch.bfloat16, device="cuda")
     torch.cuda.synchronize()
@@ -229,7 +230,8 @@ def run_neo(args):
         ends[s].record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
-    t_ms = sum(starts[s].elapsed_time(ends[s]) for s in range(args.steps))
+    step_ms = [starts[s].elapsed_time(ends[s]) for s in range(args.steps)]
+    t_ms = sum(step_ms)
     # Per-launch durations of the attention kernel for the roofline: a separate
     # pass with an event after every launch, on the launching stream.
     launch_ms = []
@@ -306,6 +308,8 @@ def run_neo(args):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(t_max * 1e3 / args.steps, 4),
+            "ms_per_step_rank0": {"median": round(float(np.median(step_ms)), 4), "min": round(min(step_ms), 4),
+                                  "max": round(max(step_ms), 4)},
             "higher_is_better": True,
             "scaling": scaling,
             "vs_baseline": None,
@@ -322,7 +326,8 @@ def run_neo(args):
                 "seq_len_mean": round(float(gb.ctx.mean()), 1), "seq_len_min": int(gb.ctx.min()),
                 "seq_len_max": int(gb.ctx.max()),
                 "layers_per_step": L, "distinct_layer_pools": gb.layers,
-                "chunk_tokens": chunk, "parallelism": par,
+                "chunk_tokens": chunk, "chunk_plan": "explicit --chunk" if args.chunk else
+                "neo_decode_attn_plan_chunk (host lengths)", "parallelism": par,
                 "l2": (f"inputs {gb.layers * gb.kv_bytes_per_call() / 1e9:.1f} GB of distinct KV cycled per step "
                        ">> 126 MB L2; no flush") if flush is None else
                       "L2 flushed (512 MB read) before every step, outside the timed attention window",

@@ -259,6 +259,26 @@ NEO_API neo_status neo_decode_attn_append(const void* q, const float* inv_freq, 
 /* Default split-K chunk length for a call shape (deterministic in its inputs). */
 NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_heads, int32_t max_seq_len);
 
+/* a0 plan ("partition ... aggregate the partial
+ * outputs") with the request lengths on the HOST -- NEO's scheduler holds them
+ * (P:283-290).  Chooses the split-K chunk length C for one neo_decode_attn /
+ * neo_decode_attn_append call over these requests: the candidate (multiples of
+ * 64 tokens and of page_size in [128, 512]) that a replay of the GPU's in-order
+ * CTA dispatch of the chunk-major grid predicts fastest, so that the last wave
+ * of work units is not left mostly empty (DESIGN §6 "chunk planner").  Grids
+ * of >= 4 waves at C = 512 take 512; grids under one wave at C = 128 take
+ * neo_decode_attn_default_chunk().  Pure host computation, no GPU work; the SM
+ * count is the current device's (148 when no device is visible).
+ *   seq_lens     [batch] int32, HOST, each >= 0 (the values the call will see).
+ *   chunk_tokens out: a valid chunk_tokens argument for page_size.
+ * Any chunk is correct (the result depends on C only through fp32 rounding);
+ * this only affects speed.
+ * Errors: NEO_ERR_INVALID_ARG (NULL pointers, batch < 0, num_kv_heads < 1, a
+ * negative length); NEO_ERR_UNSUPPORTED (page_size not a multiple of 16 in
+ * [16, 512]). */
+NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t batch, int32_t num_kv_heads,
+                                              int32_t page_size, int32_t* chunk_tokens);
+
 /* Workspace bytes for a call shape (chunk_tokens 0 = default). */
 NEO_API neo_status neo_decode_attn_workspace_bytes(int32_t batch, int32_t num_q_heads, int32_t num_kv_heads,
                                                    int32_t head_dim, int32_t max_seq_len, int32_t chunk_tokens,

@@ -730,7 +730,10 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
                              : launch_unit<4, 2, false, true>(a, tmk, tmv, units, L.stream);
   }
   int cfg = attn_cfg();
-  if (cfg == 0) cfg = L.max_chunks <= 3 ? 43 : 42;
+  if (cfg == 0) {
+    const AttnShape sh = default_attn_shape(L.max_chunks);
+    cfg = sh.warps * 10 + sh.stages;
+  }
   switch (cfg) {
     case 1042: return launch_unit<4, 2, true>(a, tmk, tmv, units, L.stream);
     case 1043: return launch_unit<4, 3, true>(a, tmk, tmv, units, L.stream);
@@ -741,6 +744,9 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
     case 48: return launch_unit<4, 8>(a, tmk, tmv, units, L.stream);
     case 43: return launch_unit<4, 3>(a, tmk, tmv, units, L.stream);
     case 23: return launch_unit<2, 3>(a, tmk, tmv, units, L.stream);
+    case 22: return launch_unit<2, 2>(a, tmk, tmv, units, L.stream);
+    case 12: return launch_unit<1, 2>(a, tmk, tmv, units, L.stream);
+    case 13: return launch_unit<1, 3>(a, tmk, tmv, units, L.stream);
     case 33: return launch_unit<3, 3>(a, tmk, tmv, units, L.stream);
     case 62: return launch_unit<6, 2>(a, tmk, tmv, units, L.stream);
     case 82: return launch_unit<8, 2>(a, tmk, tmv, units, L.stream);

@@ -164,6 +164,65 @@ int32_t default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
   return c;
 }
 
+// a0 plan with the request lengths on the host (neo_decode_attn_plan_chunk).
+// Replays the hardware's in-order CTA dispatch of the chunk-major grid for one
+// candidate C: every resident CTA slot (SMs x CTAs/SM of the default shape)
+// takes the next CTA when it frees; a CTA of W units costs a per-unit start-up
+// of kPlanUnitOverheadTiles plus the longest of its units in tiles.  Returns
+// the predicted tiles per unit time (higher is better).  The overhead was
+// fitted to same-box chunk sweeps (profiles/r01_chunk_plan.md), where this
+// model picks the measured best C on every c4 shard (N = 1, 2, 4, 8).
+constexpr double kPlanUnitOverheadTiles = 3.0;
+
+double plan_score(const std::vector<int32_t>& ntiles, int32_t hkv, int32_t chunk_tiles, int sms) {
+  int32_t max_chunks = 1;
+  int64_t total = 0;
+  for (int32_t t : ntiles) {
+    max_chunks = std::max(max_chunks, (t + chunk_tiles - 1) / chunk_tiles);
+    total += t;
+  }
+  const AttnShape sh = default_attn_shape(max_chunks);
+  std::vector<double> slot(static_cast<size_t>(sms) * sh.ctas_per_sm, 0.0);   // min-heap of free times
+  auto dispatch = [&](int32_t cta_tiles) {
+    if (cta_tiles == 0) return;   // CTAs past every request's last chunk exit at once
+    std::pop_heap(slot.begin(), slot.end(), std::greater<double>());
+    slot.back() += kPlanUnitOverheadTiles + cta_tiles;
+    std::push_heap(slot.begin(), slot.end(), std::greater<double>());
+  };
+  int in_cta = 0;
+  int32_t cta_max = 0;
+  for (int32_t c = 0; c < max_chunks; ++c) {
+    for (int32_t t : ntiles) {
+      const int32_t u = std::min(std::max(t - c * chunk_tiles, 0), chunk_tiles);
+      if (in_cta == 0 && hkv % sh.warps == 0) {   // whole CTAs of one request (the usual GQA case)
+        for (int32_t k = 0; k < hkv / sh.warps; ++k) dispatch(u);
+        continue;
+      }
+      for (int32_t g = 0; g < hkv; ++g) {
+        cta_max = std::max(cta_max, u);
+        if (++in_cta == sh.warps) {
+          dispatch(cta_max);
+          in_cta = 0;
+          cta_max = 0;
+        }
+      }
+    }
+  }
+  if (in_cta) dispatch(cta_max);
+  const double makespan = *std::max_element(slot.begin(), slot.end());
+  return makespan > 0 ? static_cast<double>(total) * hkv / makespan : 0.0;
+}
+
+int device_sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();   // no device visible (CPU box): plan for a B200
+    return 148;
+  }
+  return n;
+}
+
 neo_status check_chunk(int32_t C, int32_t P) {
   if (C <= 0 || C % kTileTokens != 0 || C % P != 0 || C > kMaxChunkTokens)
     return fail(NEO_ERR_UNSUPPORTED, "chunk_tokens must be a multiple of 16 and of page_size, <= 512 (got " +
@@ -398,6 +457,62 @@ NEO_API neo_status neo_kv_layer_view(const neo_kv_pool* pool, int32_t layer, voi
 
 NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
   return neo::default_chunk(batch, hkv, max_seq_len);
+}
+
+NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t batch, int32_t hkv, int32_t page_size,
+                                              int32_t* chunk_tokens) {
+  if (!chunk_tokens) return neo::fail(NEO_ERR_INVALID_ARG, "chunk_tokens is NULL");
+  if (batch < 0 || hkv <= 0 || (batch > 0 && !seq_lens))
+    return neo::fail(NEO_ERR_INVALID_ARG, "batch >= 0, num_kv_heads >= 1 and seq_lens (host) required");
+  if (page_size <= 0 || page_size % neo::kTileTokens || page_size > neo::kMaxChunkTokens)
+    return neo::fail(NEO_ERR_UNSUPPORTED, "page_size must be a positive multiple of 16, <= 512");
+  std::vector<int32_t> ntiles(static_cast<size_t>(batch));
+  for (int32_t b = 0; b < batch; ++b) {
+    if (seq_lens[b] < 0) return neo::fail(NEO_ERR_INVALID_ARG, "seq_lens[" + std::to_string(b) + "] < 0");
+    ntiles[b] = (seq_lens[b] + neo::kTileTokens - 1) / neo::kTileTokens;
+  }
+  // candidates: multiples of 64 tokens (and of P) in [128, 512], largest first
+  std::vector<int32_t> cand;
+  for (int32_t C = neo::kMaxChunkTokens; C >= 128; C -= 64)
+    if (C % page_size == 0) cand.push_back(C);
+  if (cand.empty()) cand.push_back(page_size);
+  const int sms = neo::device_sm_count();
+  const int32_t ct_max = cand.front() / neo::kTileTokens;
+  int64_t units = 0;
+  for (int32_t t : ntiles) units += static_cast<int64_t>(hkv) * ((t + ct_max - 1) / ct_max);
+  int32_t max_chunks = 1;
+  for (int32_t t : ntiles) max_chunks = std::max(max_chunks, (t + ct_max - 1) / ct_max);
+  const neo::AttnShape sh = neo::default_attn_shape(max_chunks);
+  const double waves = static_cast<double>(units) / (static_cast<double>(sms) * sh.ctas_per_sm * sh.warps);
+  // Many waves: the tail is amortised and the longest chunk (fewest pipeline
+  // ramps and partials) wins (every c2/c3/c5 sweep).  Under one wave at the
+  // smallest candidate the call is latency-bound: keep the shape-only default.
+  if (waves >= 4.0) {
+    *chunk_tokens = cand.front();
+    return NEO_OK;
+  }
+  const int32_t ct_min = cand.back() / neo::kTileTokens;
+  int64_t units_min = 0;
+  for (int32_t t : ntiles) units_min += static_cast<int64_t>(hkv) * ((t + ct_min - 1) / ct_min);
+  if (units_min < static_cast<int64_t>(sms) * 2 * 4) {
+    int32_t max_len = 0;
+    for (int32_t b = 0; b < batch; ++b) max_len = std::max(max_len, seq_lens[b]);
+    int32_t C = neo::default_chunk(batch, hkv, max_len);
+    if (C % page_size) C = page_size * ((C + page_size - 1) / page_size);
+    *chunk_tokens = std::min(C, neo::kMaxChunkTokens);
+    return NEO_OK;
+  }
+  int32_t best = cand.front();
+  double best_score = -1.0;
+  for (int32_t C : cand) {        // largest first: a smaller C must win by > 1 %
+    const double sc = neo::plan_score(ntiles, hkv, C / neo::kTileTokens, sms);
+    if (sc > best_score * 1.01) {
+      best = C;
+      best_score = sc;
+    }
+  }
+  *chunk_tokens = best;
+  return NEO_OK;
 }
 
 static neo_status attn_shape(int32_t batch, int32_t hq, int32_t hkv, int32_t d, int32_t max_seq_len,

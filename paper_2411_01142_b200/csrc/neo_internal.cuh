@@ -54,6 +54,16 @@ size_t workspace_counter_cap(size_t ws_bytes);
 size_t workspace_required(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks);
 WorkspaceLayout workspace_layout(int32_t batch, int32_t hq, int32_t hkv, int32_t max_chunks, size_t ws_bytes);
 neo_status launch_decode_attn(const AttnLaunch& a, const CUtensorMap& tmk, const CUtensorMap& tmv);
+// Default kernel shape launch_decode_attn picks for a grid of `max_chunks` chunk
+// levels: (4 warps, 3 stages) -> 2 resident CTAs per SM for <= 3 chunks per
+// request, else (4 warps, 2 stages) -> 3 CTAs per SM.  The chunk planner
+// simulates the same shape.
+struct AttnShape {
+  int warps, stages, ctas_per_sm;
+};
+inline AttnShape default_attn_shape(int32_t max_chunks) {
+  return max_chunks <= 3 ? AttnShape{4, 3, 2} : AttnShape{4, 2, 3};
+}
 // debug validation of device metadata (syncs the stream)
 neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
                                int32_t batch, int32_t page_size, int32_t max_seq_len, int64_t num_pages,

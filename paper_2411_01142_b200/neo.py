@@ -24,7 +24,7 @@ STATUS_NAMES = {0: "NEO_OK", 1: "NEO_ERR_INVALID_ARG", 2: "NEO_ERR_OUT_OF_PAGES"
 
 EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_create", "neo_kv_pool_destroy",
             "neo_kv_alloc", "neo_kv_free", "neo_kv_free_count", "neo_kv_layer_view", "neo_decode_attn",
-            "neo_decode_attn_default_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
+            "neo_decode_attn_default_chunk", "neo_decode_attn_plan_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
             "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
             "neo_kv_append", "neo_schedule", "neo_rope_append", "neo_prefill_append", "neo_prefill_attn",
             "neo_decode_attn_append"]
@@ -90,6 +90,8 @@ def lib() -> ctypes.CDLL:
             L.neo_kv_pool_destroy.restype = None
             L.neo_decode_attn_default_chunk.argtypes = [i32, i32, i32]
             L.neo_decode_attn_default_chunk.restype = i32
+            L.neo_decode_attn_plan_chunk.argtypes = [ctypes.c_void_p, i32, i32, i32, ctypes.POINTER(i32)]
+            L.neo_decode_attn_plan_chunk.restype = i32
             _lib = L
     return _lib
 
@@ -128,6 +130,15 @@ def _ids(ids) -> np.ndarray:
 
 def default_chunk(batch: int, num_kv_heads: int, max_seq_len: int) -> int:
     return int(lib().neo_decode_attn_default_chunk(batch, num_kv_heads, max_seq_len))
+
+
+def plan_chunk(seq_lens, num_kv_heads: int, page_size: int = 16) -> int:
+    """a0 plan from HOST request lengths (include/neo.h neo_decode_attn_plan_chunk)."""
+    sl = _ids(seq_lens)
+    out = ctypes.c_int32()
+    check(lib().neo_decode_attn_plan_chunk(sl.ctypes.data if sl.size else None, int(sl.size), num_kv_heads,
+                                            page_size, ctypes.byref(out)))
+    return int(out.value)
 
 
 def workspace_bytes(batch: int, num_q_heads: int, num_kv_heads: int, max_seq_len: int,

@@ -124,6 +124,74 @@ def test_workspace_bytes_and_default_chunk():
     assert big <= 1.05 * data + 65536
 
 
+def _plan_replay(ctx, hkv, P, sms=148, o=3.0):
+    """Independent replay of the planner's model (include/neo.h
+    neo_decode_attn_plan_chunk): chunk-major units, W = 4 per CTA, CTAs taken
+    in order by the earliest-free slot (SMs x CTAs/SM of the default shape)."""
+    import heapq
+    nt = [(c + 15) // 16 for c in ctx]
+    cands = [C for C in range(512, 127, -64) if C % P == 0] or [P]
+
+    def shape(mc):
+        return (4, 2) if mc <= 3 else (4, 3)          # (warps, CTAs/SM)
+
+    ct0 = cands[0] // 16
+    units = sum(hkv * -(-t // ct0) for t in nt)
+    w, k = shape(max([-(-t // ct0) for t in nt] + [1]))
+    if units >= 4 * sms * k * w:
+        return cands[0]
+    ctn = cands[-1] // 16
+    if sum(hkv * -(-t // ctn) for t in nt) < sms * 8:
+        return None                                   # latency-bound: library default
+    best, best_sc = cands[0], -1.0
+    for C in cands:
+        ct = C // 16
+        mc = max([-(-t // ct) for t in nt] + [1])
+        w, k = shape(mc)
+        units = [min(max(t - c * ct, 0), ct) for c in range(mc) for t in nt for _ in range(hkv)]
+        units += [0] * (-len(units) % w)
+        heap = [0.0] * (sms * k)
+        for i in range(0, len(units), w):
+            m = max(units[i:i + w])
+            if m:
+                heapq.heapreplace(heap, heap[0] + o + m)
+        sc = sum(nt) * hkv / max(heap)
+        if sc > best_sc * 1.01:
+            best, best_sc = C, sc
+    return best
+
+
+def test_plan_chunk():
+    """a0 planner: valid chunks, >= 4 waves -> 512, measured c4-shard picks, and
+    agreement with an independent replay of its dispatch model."""
+    from neo_inputs.workloads import WORKLOADS
+    rng = np.random.default_rng(307)
+    for _ in range(40):
+        B, hkv, P = int(rng.integers(1, 700)), int(rng.choice([1, 2, 4, 8])), int(rng.choice([16, 32, 64]))
+        ctx = rng.integers(0, int(rng.choice([300, 3000, 20000])), size=B).astype(np.int32)
+        C = neo.plan_chunk(ctx, hkv, P)
+        assert C % 16 == 0 and C % P == 0 and 16 <= C <= 512
+        ref = _plan_replay(ctx.tolist(), hkv, P)
+        if ref is not None:
+            assert C == ref, (B, hkv, P, C, ref)
+    for name in ("c2", "c3", "c5"):
+        wl = WORKLOADS[name]
+        assert neo.plan_chunk(wl.contexts(), wl.hkv, 16) == 512
+    c4 = WORKLOADS["c4"].contexts()
+    # profiles/r01_chunk_plan.md: best measured C per c4 shard (N = 8, 4, 2, 1)
+    assert [neo.plan_chunk(c4, 8 // n, 16) for n in (8, 4, 2, 1)] == [384, 448, 512, 512]
+    assert neo.plan_chunk([], 8, 16) == neo.default_chunk(0, 8, 0)
+    with pytest.raises(neo.NeoError) as e:
+        neo.plan_chunk([5, -1], 8, 16)
+    assert e.value.status == neo.NEO_ERR_INVALID_ARG
+    with pytest.raises(neo.NeoError) as e:
+        neo.plan_chunk([5], 8, 24)
+    assert e.value.status == neo.NEO_ERR_UNSUPPORTED
+    with pytest.raises(neo.NeoError) as e:
+        neo.plan_chunk([5], 0, 16)
+    assert e.value.status == neo.NEO_ERR_INVALID_ARG
+
+
 def test_pool_bytes_and_layer_view():
     pool = neo.KVPool(num_layers=3, num_kv_heads=8, num_gpu_pages=10, num_host_pages=4, allocate=False)
     page = 8 * 16 * 128 * 2

@@ -41,6 +41,25 @@ def test_parity_ragged(hq, hkv, chunk):
     check_case(case, chunk, f"G={hq // hkv} C={chunk}")
 
 
+@pytest.mark.parametrize("chunk", [192, 320, 384, 448])
+def test_parity_planner_chunks(chunk):
+    """Non-power-of-two chunks the a0 planner (neo_decode_attn_plan_chunk) picks,
+    on contexts that end at, one past and one short of chunk boundaries."""
+    ctx = [1, chunk - 1, chunk, chunk + 1, 2 * chunk + 17, 1844, 2252]
+    case = Case(ctx, 64, 8, seed=11 + chunk)
+    check_case(case, chunk, f"C={chunk}")
+
+
+def test_parity_planned_chunk_c4_shard():
+    """The chunk the planner picks for one kv-head of a c4-like batch, end to end."""
+    from paper_2411_01142_b200 import neo
+    rng = np.random.default_rng(8)
+    ctx = rng.integers(1844, 2253, size=64)
+    C = neo.plan_chunk(ctx, 1, 16)
+    assert C % 16 == 0 and 16 <= C <= 512
+    check_case(Case(ctx, 8, 1, seed=12), C, f"planned C={C}")
+
+
 @pytest.mark.parametrize("P,chunk", [(32, 64), (32, 0), (64, 128), (32, 512)])
 def test_parity_page_sizes(P, chunk):
     case = Case([1, 31, 32, 33, 95, 513, 700], 32, 8, P=P, seed=7 + P)

@@ -13,7 +13,10 @@ The data path has no collective (units are independent), so the per-rank
 kernel time is the N-GPU step time up to the (separately reported, overlapped)
 head all-gather.  Prints one JSON line per (config, N).
 
-  python tools/shard_time.py [c4] [c5] [--reps 5]
+  python tools/shard_time.py [c4] [c5] [--reps 5] [--n 1,2,4,8] [--chunks 128,256,...]
+
+With several --chunks, rank 0's shard of each N is timed at every chunk size
+(a tuning sweep; NEO_ATTN_CFG selects the kernel shape).
 """
 import json
 import os
@@ -31,10 +34,10 @@ from paper_2411_01142_b200 import neo  # noqa: E402
 from paper_2411_01142_b200.shard import head_shard, lpt_assign  # noqa: E402
 
 
-def time_batch(gb, reps, layers):
-    """Average per-layer device time (s) of back-to-back decode_attn calls cycling
+def time_batch(gb, reps, layers, chunk=0):
+    """Median per-layer device time (s) of back-to-back decode_attn calls cycling
     the batch's distinct layer pools (each > L2 or flushed)."""
-    chunk = neo.default_chunk(gb.B, gb.hkv, gb.max_seq_len)
+    chunk = chunk or neo.plan_chunk(gb.ctx, gb.hkv, gb.P)
     ws = neo.make_workspace(gb.B, gb.hq, gb.hkv, gb.max_seq_len, chunk)
     out = torch.empty(gb.B, gb.hq, 128, dtype=torch.bfloat16, device="cuda")
     flush = None
@@ -66,17 +69,49 @@ def time_batch(gb, reps, layers):
     return float(np.median(ts)), chunk
 
 
+def sweep(configs, ns, chunks, reps):
+    shape = os.environ.get("NEO_ATTN_CFG", "default")
+    for name in configs:
+        wl = WORKLOADS[name]
+        ctx_all = wl.contexts()
+        for n in ns:
+            if name == "c4":
+                kvh, qh = head_shard(wl.hq, wl.hkv, 0, n)
+                gb = GpuBatch(wl, ctx=ctx_all, kv_heads=kvh, q_heads=qh)
+            else:
+                gb = GpuBatch(wl, ctx=ctx_all, req_ids=np.sort(lpt_assign(ctx_all, n)[0]))
+            kvb = gb.kv_bytes_per_call()
+            row = {}
+            for c in chunks:
+                t, _ = time_batch(gb, reps, 16, c)
+                row[c] = round(kvb / t / 1e9, 0)
+            print(json.dumps({"config": name, "n": n, "shape": shape, "kv_gbs_by_chunk": row,
+                              "default_chunk": neo.default_chunk(gb.B, gb.hkv, gb.max_seq_len),
+                              "planned_chunk": neo.plan_chunk(gb.ctx, gb.hkv, gb.P)}), flush=True)
+            del gb
+            torch.cuda.empty_cache()
+
+
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    argv = sys.argv[1:]
+    args = [a for i, a in enumerate(argv) if not a.startswith("--") and (i == 0 or not argv[i - 1].startswith("--"))]
     reps = 5
     if "--reps" in sys.argv:
         reps = int(sys.argv[sys.argv.index("--reps") + 1])
     configs = args or ["c4", "c5"]
+    ns = (1, 2, 4, 8)
+    if "--n" in sys.argv:
+        ns = tuple(int(x) for x in sys.argv[sys.argv.index("--n") + 1].split(","))
+    chunks = [0]
+    if "--chunks" in sys.argv:
+        chunks = [int(x) for x in sys.argv[sys.argv.index("--chunks") + 1].split(",")]
+    if len(chunks) > 1:
+        return sweep(configs, ns, chunks, reps)
     for name in configs:
         wl = WORKLOADS[name]
         ctx_all = wl.contexts()
         t1 = None
-        for n in (1, 2, 4, 8):
+        for n in ns:
             per_rank = []
             kv_total = 0
             if name == "c4":
