@@ -53,6 +53,8 @@ struct KArgs {
   uint16_t* k_pages;
   uint16_t* v_pages;
   int64_t page_stride;
+  int32_t probe;              // experiment knob (NEO_ATTN_PROBE bits): 1 no epilogue, 2 no tile math,
+                              // 4 no combine, 8 partial stores only (no counter)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -327,6 +329,13 @@ __device__ __forceinline__ void write_zero_row(const KArgs& a, int b, int g, int
   for (int e = lane * 8; e < a.G * kHeadDim; e += 32 * 8) *reinterpret_cast<uint4*>(o + e) = make_uint4(0, 0, 0, 0);
 }
 
+// One 32-byte partial row segment: o[0..7][k] (k selects head / dim half).
+__device__ __forceinline__ void st256(float* dst, const Acc& s, int k) {
+  asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(s.o[0][k]), "f"(s.o[1][k]),
+               "f"(s.o[2][k]), "f"(s.o[3][k]), "f"(s.o[4][k]), "f"(s.o[5][k]), "f"(s.o[6][k]), "f"(s.o[7][k])
+               : "memory");
+}
+
 // End of a unit: single-chunk units write the output (a6 bypass); others write
 // the partial and the last-arriving warp of (b, g) runs the combine (a7).
 __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g, int c, int n_chunks, int lane,
@@ -364,33 +373,32 @@ __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g
   const int bg = b * a.hkv + g;
   const int64_t slot = static_cast<int64_t>(bg) * a.max_chunks + c;
   float* acc = a.ws_acc + slot * G * kHeadDim;
+  // 256-bit stores: each lane writes whole 32-byte sectors (dims 8r..8r+7 and
+  // 64+8r..64+8r+7 of its heads); the workspace acc region is 512-byte aligned
   if (h0 < G) {
-    float4* p = reinterpret_cast<float4*>(acc + h0 * kHeadDim + 8 * r);
-    p[0] = make_float4(s.o[0][0], s.o[1][0], s.o[2][0], s.o[3][0]);
-    p[1] = make_float4(s.o[4][0], s.o[5][0], s.o[6][0], s.o[7][0]);
-    float4* p2 = reinterpret_cast<float4*>(acc + h0 * kHeadDim + 64 + 8 * r);
-    p2[0] = make_float4(s.o[0][2], s.o[1][2], s.o[2][2], s.o[3][2]);
-    p2[1] = make_float4(s.o[4][2], s.o[5][2], s.o[6][2], s.o[7][2]);
+    st256(acc + h0 * kHeadDim + 8 * r, s, 0);
+    st256(acc + h0 * kHeadDim + 64 + 8 * r, s, 2);
     if (r == 0) a.ws_ml[slot * G + h0] = make_float2(s.m0, s.l0);
   }
   if (h1 < G) {
-    float4* p = reinterpret_cast<float4*>(acc + h1 * kHeadDim + 8 * r);
-    p[0] = make_float4(s.o[0][1], s.o[1][1], s.o[2][1], s.o[3][1]);
-    p[1] = make_float4(s.o[4][1], s.o[5][1], s.o[6][1], s.o[7][1]);
-    float4* p2 = reinterpret_cast<float4*>(acc + h1 * kHeadDim + 64 + 8 * r);
-    p2[0] = make_float4(s.o[0][3], s.o[1][3], s.o[2][3], s.o[3][3]);
-    p2[1] = make_float4(s.o[4][3], s.o[5][3], s.o[6][3], s.o[7][3]);
+    st256(acc + h1 * kHeadDim + 8 * r, s, 1);
+    st256(acc + h1 * kHeadDim + 64 + 8 * r, s, 3);
     if (r == 0) a.ws_ml[slot * G + h1] = make_float2(s.m1, s.l1);
   }
   // publish: the warp barrier orders every lane's partial stores before lane 0's
   // acq_rel atomic (release at GPU scope, cumulative); the last arriver's acquire
   // makes all partials of (b, g) visible to the __ldcg reads below
   __syncwarp();
+  if (a.probe & 8) return;
   int prev = 0;
   if (lane == 0)
     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ws_cnt + bg) : "memory");
   prev = __shfl_sync(kFull, prev, 0);
   if (prev != n_chunks - 1) return;
+  if (a.probe & 4) {
+    if (lane == 0) a.ws_cnt[bg] = 0;
+    return;
+  }
   // combine in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c.
   // Latency-parallel: pass 1 spreads the (chunk, head) statistics over the lanes
   // (G divides 32, so lane L only ever sees head L % G); pass 2 walks the chunks in
@@ -601,9 +609,9 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(j + kStages);
     }
-    if (!kStreamOnly) compute_tile(f, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
+      if (!kStreamOnly && !(a.probe & 2)) compute_tile(f, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
   }
-  if (!kStreamOnly) finish_unit(a, acc, b, g, c, n_chunks, lane, r, qd);
+  if (!kStreamOnly && !(a.probe & 1)) finish_unit(a, acc, b, g, c, n_chunks, lane, r, qd);
 }
 
 }  // namespace
@@ -724,6 +732,11 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   a.k_pages = static_cast<uint16_t*>(L.k_pages);
   a.v_pages = static_cast<uint16_t*>(L.v_pages);
   a.page_stride = L.page_stride;
+  static const int probe = [] {
+    const char* v = std::getenv("NEO_ATTN_PROBE");
+    return v ? std::atoi(v) : 0;
+  }();
+  a.probe = probe;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
   if (L.k_new) {   // fused append (+ RoPE): the two default shapes
     return L.max_chunks <= 3 ? launch_unit<4, 3, false, true>(a, tmk, tmv, units, L.stream)
