@@ -329,6 +329,80 @@ __device__ __forceinline__ void write_zero_row(const KArgs& a, int b, int g, int
   for (int e = lane * 8; e < a.G * kHeadDim; e += 32 * 8) *reinterpret_cast<uint4*>(o + e) = make_uint4(0, 0, 0, 0);
 }
 
+// (a7) combine of the n_chunks partials of (b, g), by the last-arriving warp:
+//   out_h = sum_c 2^(m_ch - M_h) acc_ch / sum_c 2^(m_ch - M_h) l_ch,  M_h = max_c m_ch.
+// Latency-parallel for any G: pass 1 gives lane L chunks L, L+32, ... and merges
+// their (m, l) per head, then a butterfly merges the lanes (commutative, so every
+// lane ends with bitwise the same M_h, L_h); pass 2 has each lane accumulate 4 dims
+// of every head over the chunks in chunk order, loading K chunks x G heads of
+// partials per batch before using any of them.
+template <int G>
+__device__ __forceinline__ void combine(const KArgs& a, int b, int g, int bg, int n_chunks, int lane) {
+  const int64_t slot0 = static_cast<int64_t>(bg) * a.max_chunks;
+  const float2* ml = a.ws_ml + slot0 * G;
+  float M[G], L[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) M[h] = -INFINITY, L[h] = 0.f;
+  for (int c = lane; c < n_chunks; c += 32) {
+    float2 t[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) t[h] = __ldcg(&ml[c * G + h]);
+#pragma unroll
+    for (int h = 0; h < G; ++h) {   // chunk m is finite (>= 1 token), so mn is too
+      const float mn = fmaxf(M[h], t[h].x);
+      L[h] = L[h] * ex2(M[h] - mn) + t[h].y * ex2(t[h].x - mn);
+      M[h] = mn;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      const float Mo = __shfl_xor_sync(kFull, M[h], off), Lo = __shfl_xor_sync(kFull, L[h], off);
+      const float mn = fmaxf(M[h], Mo);
+      L[h] = (M[h] == -INFINITY ? 0.f : L[h] * ex2(M[h] - mn)) + (Mo == -INFINITY ? 0.f : Lo * ex2(Mo - mn));
+      M[h] = mn;
+    }
+  }
+  constexpr int K = 16 / G > 1 ? 16 / G : 1;       // chunks per batch (<= 16 partial rows in flight)
+  float4 s4[G];
+#pragma unroll
+  for (int h = 0; h < G; ++h) s4[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* accb = a.ws_acc + slot0 * G * kHeadDim + 4 * lane;
+  for (int c0 = 0; c0 < n_chunks; c0 += K) {
+    float4 v[K][G];
+    float w[K][G];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int cc = c0 + k < n_chunks ? c0 + k : n_chunks - 1;
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        v[k][h] = __ldcg(reinterpret_cast<const float4*>(accb + (static_cast<int64_t>(cc) * G + h) * kHeadDim));
+        w[k][h] = __ldcg(&ml[cc * G + h].x);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        const float wk = c0 + k < n_chunks ? ex2(w[k][h] - M[h]) : 0.f;
+        s4[h].x += wk * v[k][h].x;
+        s4[h].y += wk * v[k][h].y;
+        s4[h].z += wk * v[k][h].z;
+        s4[h].w += wk * v[k][h].w;
+      }
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < G; ++h) {
+    const float inv = 1.f / L[h];
+    uint2 pk;
+    pk.x = pack_bf16(s4[h].x * inv, s4[h].y * inv);
+    pk.y = pack_bf16(s4[h].z * inv, s4[h].w * inv);
+    *reinterpret_cast<uint2*>(a.out + (static_cast<int64_t>(b) * a.hq + g * G + h) * kHeadDim + 4 * lane) = pk;
+  }
+}
+
 // One 32-byte partial row segment: o[0..7][k] (k selects head / dim half).
 __device__ __forceinline__ void st256(float* dst, const Acc& s, int k) {
   asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "f"(s.o[0][k]), "f"(s.o[1][k]),
@@ -399,60 +473,15 @@ __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g
     if (lane == 0) a.ws_cnt[bg] = 0;
     return;
   }
-  // combine in chunk order: out = sum_c 2^(m_c - M) acc_c / sum_c 2^(m_c - M) l_c.
-  // Latency-parallel: pass 1 spreads the (chunk, head) statistics over the lanes
-  // (G divides 32, so lane L only ever sees head L % G); pass 2 walks the chunks in
-  // order with independent loads, four chunks per batch, all heads at once.
-  const int64_t slot0 = static_cast<int64_t>(bg) * a.max_chunks;
-  const float2* ml = a.ws_ml + slot0 * G;
-  const int ne = n_chunks * G;
-  float mloc = -INFINITY;
-  for (int e = lane; e < ne; e += 32) mloc = fmaxf(mloc, __ldcg(&ml[e].x));
-  for (int off = G; off < 32; off <<= 1) mloc = fmaxf(mloc, __shfl_xor_sync(kFull, mloc, off));
-  float lloc = 0.f;
-  for (int e = lane; e < ne; e += 32) {
-    const float2 v = __ldcg(&ml[e]);
-    lloc += v.y * ex2(v.x - mloc);
-  }
-  for (int off = G; off < 32; off <<= 1) lloc += __shfl_xor_sync(kFull, lloc, off);
-  // lane h (< G) now holds M_h in mloc and L_h in lloc
-  float Mh[kMaxGroup], inv[kMaxGroup];
-  float4 s4[kMaxGroup];
-#pragma unroll
-  for (int h = 0; h < kMaxGroup; ++h) {
-    Mh[h] = __shfl_sync(kFull, mloc, h < G ? h : 0);
-    inv[h] = 1.f / __shfl_sync(kFull, lloc, h < G ? h : 0);
-    s4[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const float* accb = a.ws_acc + slot0 * G * kHeadDim + 4 * lane;
-  for (int c0 = 0; c0 < n_chunks; c0 += 4) {
-#pragma unroll
-    for (int h = 0; h < kMaxGroup; ++h) {
-      if (h >= G) break;
-      float4 v[4];
-      float w[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int cc = c0 + k < n_chunks ? c0 + k : n_chunks - 1;
-        v[k] = __ldcg(reinterpret_cast<const float4*>(accb + (static_cast<int64_t>(cc) * G + h) * kHeadDim));
-        w[k] = c0 + k < n_chunks ? ex2(__ldcg(&ml[cc * G + h].x) - Mh[h]) : 0.f;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        s4[h].x += w[k] * v[k].x;
-        s4[h].y += w[k] * v[k].y;
-        s4[h].z += w[k] * v[k].z;
-        s4[h].w += w[k] * v[k].w;
-      }
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < kMaxGroup; ++h) {
-    if (h >= G) break;
-    uint2 pk;
-    pk.x = pack_bf16(s4[h].x * inv[h], s4[h].y * inv[h]);
-    pk.y = pack_bf16(s4[h].z * inv[h], s4[h].w * inv[h]);
-    *reinterpret_cast<uint2*>(a.out + (static_cast<int64_t>(b) * a.hq + g * G + h) * kHeadDim + 4 * lane) = pk;
+  switch (G) {
+    case 1: combine<1>(a, b, g, bg, n_chunks, lane); break;
+    case 2: combine<2>(a, b, g, bg, n_chunks, lane); break;
+    case 3: combine<3>(a, b, g, bg, n_chunks, lane); break;
+    case 4: combine<4>(a, b, g, bg, n_chunks, lane); break;
+    case 5: combine<5>(a, b, g, bg, n_chunks, lane); break;
+    case 6: combine<6>(a, b, g, bg, n_chunks, lane); break;
+    case 7: combine<7>(a, b, g, bg, n_chunks, lane); break;
+    default: combine<8>(a, b, g, bg, n_chunks, lane); break;
   }
   if (lane == 0) a.ws_cnt[bg] = 0;  // leave the workspace re-usable
 }

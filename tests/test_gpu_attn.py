@@ -41,6 +41,15 @@ def test_parity_ragged(hq, hkv, chunk):
     check_case(case, chunk, f"G={hq // hkv} C={chunk}")
 
 
+@pytest.mark.parametrize("hq,hkv", [(24, 8), (40, 8), (48, 8), (28, 4), (7, 1)])
+@pytest.mark.parametrize("chunk", [16, 64, 512])
+def test_parity_group_sizes_not_dividing_32(hq, hkv, chunk):
+    """G in {3, 5, 6, 7} (e.g. 28 q / 4 kv heads): the combine's per-head
+    statistics must not assume G divides the warp size."""
+    ctx = [1, 16, 17, 129, 600, 1000, 2049]
+    check_case(Case(ctx, hq, hkv, seed=13 + hq + chunk), chunk, f"G={hq // hkv} C={chunk}")
+
+
 @pytest.mark.parametrize("chunk", [192, 320, 384, 448])
 def test_parity_planner_chunks(chunk):
     """Non-power-of-two chunks the a0 planner (neo_decode_attn_plan_chunk) picks,
