@@ -60,7 +60,7 @@ class HostCase:
         return worst
 
 
-@pytest.mark.parametrize("hq,hkv", [(32, 8), (64, 8), (32, 32), (8, 1), (16, 8)])
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (64, 8), (32, 32), (8, 1), (16, 8), (28, 4), (24, 8)])
 @pytest.mark.parametrize("threads", [1, 3, 8])
 @pytest.mark.parametrize("path", ["2", "1", "0"])      # AVX-512 BF16 / AVX-512F / portable
 def test_cpu_attn_parity(hq, hkv, threads, path, monkeypatch):
