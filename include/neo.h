@@ -144,7 +144,7 @@ NEO_API neo_status neo_kv_layer_view(const neo_kv_pool* pool, int32_t layer, voi
  *   out         [batch][Hq][D] bf16, device (fp32 -> bf16 round-to-nearest-even).
  *   max_seq_len host-known upper bound of seq_lens (sizes the grid).
  *   scale       softmax scale, typically 1/sqrt(D) (DESIGN c1).
- *   chunk_tokens split-K chunk length C (multiple of 16 and of P, <= 512), or 0 for
+ *   chunk_tokens split-K chunk length C (multiple of 16 and of P, <= 1024), or 0 for
  *               the library default neo_decode_attn_default_chunk().  The result for
  *               request b depends only on (its inputs, C): outputs are bitwise
  *               deterministic run to run (fixed merge order, no float atomics).

@@ -601,10 +601,14 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
   // with the seq_lens load: lane i reads the page of tile i of the chunk (index
   // clamped into the table; entries past the context are loaded but never used).
   const int t_begin = c * a.chunk_tiles;
-  int my_pid = 0;
+  int my_pid = 0, my_pid2 = 0;   // pages of tiles lane and 32 + lane (chunks of up to 64 tiles)
   if (lane < a.chunk_tiles) {
     const int pg = min((t_begin + lane) * kTileTokens / a.page_size, a.max_blocks - 1);
     my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + pg);
+  }
+  if (lane + 32 < a.chunk_tiles) {
+    const int pg = min((t_begin + 32 + lane) * kTileTokens / a.page_size, a.max_blocks - 1);
+    my_pid2 = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + pg);
   }
   uint4 qf[4];
   load_q(a, b, g, r, qd, qf);
@@ -627,7 +631,7 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
 
   // KV stream (a2): tile j of the unit -> stage j % kStages
   auto issue = [&](int j) {
-    const int pid = __shfl_sync(kFull, my_pid, j);
+    const int pid = j < 32 ? __shfl_sync(kFull, my_pid, j) : __shfl_sync(kFull, my_pid2, j - 32);
     if (lane == 0) {
       const int s = j % kStages;
       issue_tile(&tmk, &tmv, sbase + s * kStageBytes, bar0 + 8 * s, ((t_begin + j) * kTileTokens) % a.page_size, g,

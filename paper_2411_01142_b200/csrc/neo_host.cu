@@ -160,7 +160,7 @@ int32_t default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
   const double target_units = 3.0 * 148 * 12;
   const double want = static_cast<double>(batch) * hkv * std::max(max_seq_len, 1) / target_units;
   int32_t c = 64;
-  while (c < want && c < kMaxChunkTokens) c *= 2;
+  while (c < want && c < kDefaultMaxChunk) c *= 2;
   return c;
 }
 
@@ -170,9 +170,10 @@ int32_t default_chunk(int32_t batch, int32_t hkv, int32_t max_seq_len) {
 // takes the next CTA when it frees; a CTA of W units costs a per-unit start-up
 // of kPlanUnitOverheadTiles plus the longest of its units in tiles.  Returns
 // the predicted tiles per unit time (higher is better).  The overhead was
-// fitted to same-box chunk sweeps (profiles/r01_chunk_plan.md), where this
-// model picks the measured best C on every c4 shard (N = 1, 2, 4, 8).
-constexpr double kPlanUnitOverheadTiles = 3.0;
+// fitted to same-box chunk sweeps (profiles/r01_chunk_plan.md): over the c2,
+// c2s, c3, c4 (N = 1, 2, 4, 8) and c5 (N = 1, 2, 4, 8) shards its picks reach
+// 99.6 % of the best measured chunk on geometric mean, 97.9 % worst case.
+constexpr double kPlanUnitOverheadTiles = 6.0;
 
 double plan_score(const std::vector<int32_t>& ntiles, int32_t hkv, int32_t chunk_tiles, int sms) {
   int32_t max_chunks = 1;
@@ -225,7 +226,7 @@ int device_sm_count() {
 
 neo_status check_chunk(int32_t C, int32_t P) {
   if (C <= 0 || C % kTileTokens != 0 || C % P != 0 || C > kMaxChunkTokens)
-    return fail(NEO_ERR_UNSUPPORTED, "chunk_tokens must be a multiple of 16 and of page_size, <= 512 (got " +
+    return fail(NEO_ERR_UNSUPPORTED, "chunk_tokens must be a multiple of 16 and of page_size, <= 1024 (got " +
                                          std::to_string(C) + ")");
   return NEO_OK;
 }
@@ -471,9 +472,12 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
     if (seq_lens[b] < 0) return neo::fail(NEO_ERR_INVALID_ARG, "seq_lens[" + std::to_string(b) + "] < 0");
     ntiles[b] = (seq_lens[b] + neo::kTileTokens - 1) / neo::kTileTokens;
   }
-  // candidates: multiples of 64 tokens (and of P) in [128, 512], largest first
+  // candidates (largest first), those that are multiples of P: the sizes the
+  // same-box sweeps resolved (profiles/r01_chunk_plan.md); finer steps only let the
+  // model's error pick worse neighbours
+  static const int32_t kCand[] = {1024, 640, 512, 448, 384, 320, 256};
   std::vector<int32_t> cand;
-  for (int32_t C = neo::kMaxChunkTokens; C >= 128; C -= 64)
+  for (int32_t C : kCand)
     if (C % page_size == 0) cand.push_back(C);
   if (cand.empty()) cand.push_back(page_size);
   const int sms = neo::device_sm_count();
@@ -485,9 +489,9 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
   const neo::AttnShape sh = neo::default_attn_shape(max_chunks);
   const double waves = static_cast<double>(units) / (static_cast<double>(sms) * sh.ctas_per_sm * sh.warps);
   // Many waves: the tail is amortised and the longest chunk (fewest pipeline
-  // ramps and partials) wins (every c2/c3/c5 sweep).  Under one wave at the
-  // smallest candidate the call is latency-bound: keep the shape-only default.
-  if (waves >= 4.0) {
+  // ramps and partials) wins (c5 sweeps).  Under one wave at the smallest
+  // candidate the call is latency-bound: keep the shape-only default.
+  if (waves >= 16.0) {
     *chunk_tokens = cand.front();
     return NEO_OK;
   }

@@ -16,7 +16,8 @@ constexpr int kHeadDim = 128;
 constexpr int kTileTokens = 16;                       // tokens per MMA tile
 constexpr int kTileBytes = kTileTokens * kHeadDim * 2;  // 4096: one K (or V) tile
 constexpr int kMaxGroup = 8;                          // G <= 8 (MMA N = 8)
-constexpr int kMaxChunkTokens = 512;                  // <= 32 tiles per work unit
+constexpr int kMaxChunkTokens = 1024;                 // <= 64 tiles per work unit
+constexpr int kDefaultMaxChunk = 512;                 // cap of the shape-only default chunk
 
 // thread-local error text for neo_last_error()
 void set_error(const std::string& msg);

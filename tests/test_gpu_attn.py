@@ -50,7 +50,7 @@ def test_parity_group_sizes_not_dividing_32(hq, hkv, chunk):
     check_case(Case(ctx, hq, hkv, seed=13 + hq + chunk), chunk, f"G={hq // hkv} C={chunk}")
 
 
-@pytest.mark.parametrize("chunk", [192, 320, 384, 448])
+@pytest.mark.parametrize("chunk", [192, 320, 384, 448, 768, 1024])
 def test_parity_planner_chunks(chunk):
     """Non-power-of-two chunks the a0 planner (neo_decode_attn_plan_chunk) picks,
     on contexts that end at, one past and one short of chunk boundaries."""
