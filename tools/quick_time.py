@@ -16,7 +16,7 @@ from paper_2411_01142_b200 import neo  # noqa: E402
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "c2"
-    chunks = [int(x) for x in sys.argv[2:]] or [0]
+    chunks = [int(x) for x in sys.argv[2:]] or [-1]      # -1: the a0 planner's chunk (as bench.py)
     wl = WORKLOADS[name]
     t0 = time.time()
     gb = GpuBatch(wl)
@@ -26,6 +26,8 @@ def main():
     kvb = gb.kv_bytes_per_call()
     out = torch.empty(gb.B, wl.hq, 128, dtype=torch.bfloat16, device="cuda")
     for C in chunks:
+        if C < 0:
+            C = neo.plan_chunk(gb.ctx, gb.hkv, gb.P)
         ws = neo.make_workspace(gb.B, wl.hq, wl.hkv, gb.max_seq_len, C)
         L = max(gb.layers, 8)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(L + 1)]
