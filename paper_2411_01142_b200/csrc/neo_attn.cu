@@ -583,6 +583,16 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
   // previous kernel (which may have produced q, the KV pages, the block table or
   // seq_lens) to complete before touching any input.  No-ops without PDL.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // Input-free setup overlaps the previous kernel's tail: the tensor-map
+  // prefetch (kernel parameters) and this warp's stage barriers (shared memory).
+  if (lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+  }
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
+  const uint32_t bar0 = smem_u32(&bars[warp][0]);
+  init_ring(bar0, kStages, lane);
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int64_t unit = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
@@ -593,10 +603,6 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
   const int b = bg / a.hkv;
   const int g = bg - b * a.hkv;
 
-  if (lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
-  }
   // Issue the block-table walk (a1) and the q loads speculatively, in parallel
   // with the seq_lens load: lane i reads the page of tile i of the chunk (index
   // clamped into the table; entries past the context are loaded but never used).
@@ -623,10 +629,6 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
   if (c >= n_chunks) return;
   const int nt = min(a.chunk_tiles, ntile_total - t_begin);
 
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
-  const uint32_t bar0 = smem_u32(&bars[warp][0]);
-  init_ring(bar0, kStages, lane);
   const uint64_t policy = evict_first_policy();
 
   // KV stream (a2): tile j of the unit -> stage j % kStages
