@@ -1,6 +1,6 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times (library-default chunk, device-generated inputs, scattered block
-tables): sampled requests of sampled layers are checked one by one against the
+times (the a0 planner's chunk from the host lengths, device-generated inputs,
+scattered block tables), and at the library-default chunk: sampled requests of sampled layers are checked one by one against the
 fp64 oracle, and every output row is checked to be finite.  Head-sharded (c4)
 and request-sharded (c5) shards are checked the same way on their slice."""
 import math
@@ -22,7 +22,7 @@ def gpu():
     build.build()
 
 
-def run_and_sample(wl, layers, n_samples, rng, **kw):
+def run_and_sample(wl, layers, n_samples, rng, planned=True, **kw):
     import torch
 
     import oracle
@@ -30,10 +30,11 @@ def run_and_sample(wl, layers, n_samples, rng, **kw):
     from neo_inputs.gpu import GpuBatch
     from paper_2411_01142_b200 import neo
     gb = GpuBatch(wl, layers=max(layers) + 1, **kw)
+    C = neo.plan_chunk(gb.ctx, gb.hkv, gb.P) if planned else 0
     worst = 0.0
     for layer in layers:
         k, v = gb.layer(layer)
-        out = neo.decode_attn(gb.q[layer], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len)
+        out = neo.decode_attn(gb.q[layer], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, chunk_tokens=C)
         torch.cuda.synchronize()
         assert torch.isfinite(out.float()).all()
         picks = set(rng.choice(gb.B, size=min(n_samples, gb.B), replace=False).tolist())
@@ -57,6 +58,13 @@ def test_fullsize_sampled(name, layers, n):
     rng = np.random.default_rng(hash(name) % 1000)
     w = run_and_sample(WORKLOADS[name], layers, n, rng)
     print(f"{name}: worst err/tol {w:.3f}")
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_fullsize_sampled_default_chunk(name):
+    from neo_inputs.workloads import WORKLOADS
+    rng = np.random.default_rng(7 + hash(name) % 1000)
+    run_and_sample(WORKLOADS[name], [2], 8, rng, planned=False)
 
 
 @pytest.mark.parametrize("world", [2, 8])
