@@ -251,7 +251,11 @@ def run_neo(args):
     kv_local = gb.kv_bytes_per_call() * L * args.steps
     tok_local = int(gb.ctx.astype(np.int64).sum()) * L * args.steps
     tot = torch.tensor([kv_local, tok_local], dtype=torch.float64, device="cuda")
+    per_rank = None
     if world > 1:
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = [float(x.item()) / args.steps for x in allt]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if scaling == "strong" and wl.name == "c4":
             # head sharding: each (request, token, layer) is attended once over all ranks
@@ -337,6 +341,8 @@ def run_neo(args):
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                          "kernel": "decode_attn_kernel", "avg_launch_us": round(avg_launch * 1e6, 2),
                          "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
+            "per_rank_ms_per_step": None if per_rank is None else [round(x, 4) for x in per_rank],
+            "rank_imbalance": None if per_rank is None else round(max(per_rank) / (sum(per_rank) / world), 4),
             "gpu_launches": L * args.steps,
             "clocks": clk,
             "e2e": e2e,
@@ -509,7 +515,7 @@ def run_reassembly(args, gb, L, step, stream, world, dist):
     full = torch.empty((L, gb.B, gb.hq * world, 128), dtype=torch.bfloat16, device="cuda")
     gbuf = torch.empty((L, world, gb.B, gb.hq, 128), dtype=torch.bfloat16, device="cuda")
     outl = torch.empty((L, gb.B, gb.hq, 128), dtype=torch.bfloat16, device="cuda")
-    chunk = neo.default_chunk(gb.B, gb.hkv, gb.max_seq_len)
+    chunk = neo.plan_chunk(gb.ctx, gb.hkv, gb.P)
     ws = neo.make_workspace(gb.B, gb.hq, gb.hkv, gb.max_seq_len, chunk)
     evs = [torch.cuda.Event() for _ in range(L)]
 
@@ -687,7 +693,11 @@ def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
     kv = torch.tensor([float(gb.kv_bytes_per_call() * L * args.steps)], dtype=torch.float64, device="cuda")
+    per_rank = None
     if world > 1:
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = [float(x.item()) / args.steps for x in allt]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(kv, op=dist.ReduceOp.SUM)
     h2d = q_host.numel() * 2 + bt_host.numel() * 4 + sl_host.numel() * 4
