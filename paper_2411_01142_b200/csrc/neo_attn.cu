@@ -600,8 +600,12 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
   const int c = static_cast<int>(unit / BH);
   if (c >= a.max_chunks) return;
   const int bg = static_cast<int>(unit - static_cast<int64_t>(c) * BH);
-  const int b = bg / a.hkv;
-  const int g = bg - b * a.hkv;
+  int b = bg / a.hkv;
+  int g = bg - b * a.hkv;
+  if (a.probe & 64) {   // probe: head-major unit order (a CTA's warps read different requests)
+    g = bg / a.batch;
+    b = bg - g * a.batch;
+  }
 
   // Issue the block-table walk (a1) and the q loads speculatively, in parallel
   // with the seq_lens load: lane i reads the page of tile i of the chunk (index
@@ -663,6 +667,194 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
   if (!kStreamOnly && !(a.probe & 1)) finish_unit(a, acc, b, g, c, n_chunks, lane, r, qd);
 }
 
+
+// ------------------------------------------ kernel 2: one CTA per (b, g) group
+//
+// Grouped split-K: CTA (q, b, g) covers group q of request b's tiles for KV head
+// g -- the tiles split into n_groups = ceil(ntiles / 256) equal groups, and each
+// group into 4 equal per-warp ranges (<= 64 tiles, so one TMA ring and two
+// page-id registers per lane as in kernel 1).  The split depends only on the
+// request's own length, so results stay a function of (its inputs) alone.
+// The 4 warps merge their (m, l, acc) through shared memory (their own, drained
+// stage rings); a single-group request writes its bf16 output right there -- no
+// partial rows, no counter -- and only requests longer than 4096 tokens write one
+// merged partial per group and run the split-K combine (a7) across groups.
+constexpr int kGroupWarps = 4;
+constexpr int kMaxWarpTiles = kGroupTiles / kGroupWarps;
+
+template <int G>
+__device__ __forceinline__ void group_merge(const KArgs& a, const uint8_t* base, int stage_bytes, int warp, int lane,
+                                            int b, int g, int bg, int q, int n_groups) {
+  for (int h = warp; h < G; h += kGroupWarps) {
+    float mc[kGroupWarps], lc[kGroupWarps];
+    float M = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < kGroupWarps; ++c) {
+      const float2 t = reinterpret_cast<const float2*>(base + c * stage_bytes + G * kHeadDim * 4)[h];
+      mc[c] = t.x;
+      lc[c] = t.y;
+      M = fmaxf(M, t.x);
+    }
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < kGroupWarps; ++c) {   // warps without tiles have m = -inf, l = 0
+      const float w = mc[c] == -INFINITY ? 0.f : ex2(mc[c] - M);
+      L += w * lc[c];
+      const float4 v = reinterpret_cast<const float4*>(base + c * stage_bytes)[h * (kHeadDim / 4) + lane];
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
+    }
+    if (n_groups == 1) {
+      const float inv = 1.f / L;
+      uint2 pk;
+      pk.x = pack_bf16(acc.x * inv, acc.y * inv);
+      pk.y = pack_bf16(acc.z * inv, acc.w * inv);
+      *reinterpret_cast<uint2*>(a.out + (static_cast<int64_t>(b) * a.hq + g * G + h) * kHeadDim + 4 * lane) = pk;
+    } else {
+      const int64_t slot = static_cast<int64_t>(bg) * a.max_chunks + q;
+      reinterpret_cast<float4*>(a.ws_acc + (slot * G + h) * kHeadDim)[lane] = acc;
+      if (lane == 0) a.ws_ml[slot * G + h] = make_float2(M, L);
+    }
+  }
+}
+
+template <int kStages>
+__global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kStages>())
+    decode_attn_group_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
+                             const KArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[kGroupWarps][kStages];
+  __shared__ int last_flag;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2;
+  const int qd = lane & 3;
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+  }
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
+  const uint32_t bar0 = smem_u32(&bars[warp][0]);
+  init_ring(bar0, kStages, lane);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
+  const int q = static_cast<int>(blockIdx.x / BH);
+  const int bg = static_cast<int>(blockIdx.x - static_cast<int64_t>(q) * BH);
+  const int b = bg / a.hkv;
+  const int g = bg - b * a.hkv;
+  uint4 qf[4];
+  load_q(a, b, g, r, qd, qf);
+  const int ctx = __ldg(a.seq_lens + b);
+  if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
+    if (q == 0 && warp == 0) write_zero_row(a, b, g, lane);
+    return;
+  }
+  const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
+  const int n_groups = (ntile_total + kGroupWarps * kMaxWarpTiles - 1) / (kGroupWarps * kMaxWarpTiles);
+  if (q >= n_groups) return;                       // uniform over the CTA (same b, q)
+  const int tg = (ntile_total + n_groups - 1) / n_groups;
+  const int g0 = q * tg, g1 = min(g0 + tg, ntile_total);
+  const int tw = (g1 - g0 + kGroupWarps - 1) / kGroupWarps;
+  const int t_begin = g0 + warp * tw;
+  const int nt = max(0, min(t_begin + tw, g1) - t_begin);
+
+  int my_pid = 0, my_pid2 = 0;
+  if (lane < nt) my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks +
+                                (t_begin + lane) * kTileTokens / a.page_size);
+  if (lane + 32 < nt) my_pid2 = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks +
+                                      (t_begin + 32 + lane) * kTileTokens / a.page_size);
+  const uint64_t policy = evict_first_policy();
+  auto issue = [&](int j) {
+    const int pid = j < 32 ? __shfl_sync(kFull, my_pid, j) : __shfl_sync(kFull, my_pid2, j - 32);
+    if (lane == 0) {
+      const int s = j % kStages;
+      issue_tile(&tmk, &tmv, sbase + s * kStageBytes, bar0 + 8 * s, ((t_begin + j) * kTileTokens) % a.page_size, g,
+                 pid, policy);
+    }
+  };
+  const int npro = nt < kStages ? nt : kStages;
+  for (int j = 0; j < npro; ++j) issue(j);
+
+  Acc acc;
+  acc_reset(acc);
+  for (int j = 0; j < nt; ++j) {
+    const int s = j % kStages;
+    mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
+    Frags f;
+    load_frags(sbase + s * kStageBytes, r, qd, f);
+    __syncwarp();
+    if (j + kStages < nt) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(j + kStages);
+    }
+    compute_tile(f, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
+  }
+
+  // (a6/a7 in the CTA) this warp's (acc, m, l) into its drained stage ring
+#pragma unroll
+  for (int off = 4; off < 32; off <<= 1) {
+    acc.l0 += __shfl_xor_sync(kFull, acc.l0, off);
+    acc.l1 += __shfl_xor_sync(kFull, acc.l1, off);
+  }
+  const int G = a.G;
+  const int h0 = 2 * qd, h1 = 2 * qd + 1;
+  float* sp = reinterpret_cast<float*>(base + warp * (kStages * kStageBytes));
+  if (h0 < G) {
+    *reinterpret_cast<float4*>(sp + h0 * kHeadDim + 8 * r) = make_float4(acc.o[0][0], acc.o[1][0], acc.o[2][0], acc.o[3][0]);
+    *reinterpret_cast<float4*>(sp + h0 * kHeadDim + 8 * r + 4) = make_float4(acc.o[4][0], acc.o[5][0], acc.o[6][0], acc.o[7][0]);
+    *reinterpret_cast<float4*>(sp + h0 * kHeadDim + 64 + 8 * r) = make_float4(acc.o[0][2], acc.o[1][2], acc.o[2][2], acc.o[3][2]);
+    *reinterpret_cast<float4*>(sp + h0 * kHeadDim + 68 + 8 * r) = make_float4(acc.o[4][2], acc.o[5][2], acc.o[6][2], acc.o[7][2]);
+    if (r == 0) reinterpret_cast<float2*>(sp + G * kHeadDim)[h0] = make_float2(acc.m0, acc.l0);
+  }
+  if (h1 < G) {
+    *reinterpret_cast<float4*>(sp + h1 * kHeadDim + 8 * r) = make_float4(acc.o[0][1], acc.o[1][1], acc.o[2][1], acc.o[3][1]);
+    *reinterpret_cast<float4*>(sp + h1 * kHeadDim + 8 * r + 4) = make_float4(acc.o[4][1], acc.o[5][1], acc.o[6][1], acc.o[7][1]);
+    *reinterpret_cast<float4*>(sp + h1 * kHeadDim + 64 + 8 * r) = make_float4(acc.o[0][3], acc.o[1][3], acc.o[2][3], acc.o[3][3]);
+    *reinterpret_cast<float4*>(sp + h1 * kHeadDim + 68 + 8 * r) = make_float4(acc.o[4][3], acc.o[5][3], acc.o[6][3], acc.o[7][3]);
+    if (r == 0) reinterpret_cast<float2*>(sp + G * kHeadDim)[h1] = make_float2(acc.m1, acc.l1);
+  }
+  __syncthreads();
+  const int sb = kStages * kStageBytes;
+  switch (G) {
+    case 1: group_merge<1>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+    case 2: group_merge<2>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+    case 3: group_merge<3>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+    case 4: group_merge<4>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+    case 5: group_merge<5>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+    case 6: group_merge<6>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+    case 7: group_merge<7>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+    default: group_merge<8>(a, base, sb, warp, lane, b, g, bg, q, n_groups); break;
+  }
+  if (n_groups == 1) return;
+  // publish this group's merged partial; the last-arriving group runs the combine
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int prev;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ws_cnt + bg) : "memory");
+    last_flag = prev == n_groups - 1;
+  }
+  __syncthreads();
+  if (!last_flag || warp != 0) return;
+  switch (G) {
+    case 1: combine<1>(a, b, g, bg, n_groups, lane); break;
+    case 2: combine<2>(a, b, g, bg, n_groups, lane); break;
+    case 3: combine<3>(a, b, g, bg, n_groups, lane); break;
+    case 4: combine<4>(a, b, g, bg, n_groups, lane); break;
+    case 5: combine<5>(a, b, g, bg, n_groups, lane); break;
+    case 6: combine<6>(a, b, g, bg, n_groups, lane); break;
+    case 7: combine<7>(a, b, g, bg, n_groups, lane); break;
+    default: combine<8>(a, b, g, bg, n_groups, lane); break;
+  }
+  if (lane == 0) a.ws_cnt[bg] = 0;  // leave the workspace re-usable
+}
 }  // namespace
 
 size_t workspace_counter_cap(size_t ws_bytes) { return (ws_bytes / 64) & ~size_t(255); }
@@ -737,6 +929,33 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
   return NEO_OK;
 }
 
+template <int S>
+static neo_status launch_group(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t ctas,
+                               cudaStream_t stream) {
+  static bool configured = false;
+  constexpr int smem = kGroupWarps * S * kStageBytes + 1024;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(decode_attn_group_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_group_kernel)");
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+  cfg.blockDim = dim3(kGroupWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, decode_attn_group_kernel<S>, tmk, tmv, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "decode_attn_group_kernel launch");
+  return NEO_OK;
+}
+
 // Kernel shape: kWarps independent warps per CTA x kStages TMA stages per warp.
 // Default, from same-box sweeps (profiles/r01_sweep.md): (4, 3) -- 97 KiB of
 // stages, 2 CTAs/SM -- when every request spans <= 3 chunks (c2: +2 % over
@@ -787,6 +1006,10 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   }();
   a.probe = probe;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
+  if (L.grouped) {   // NEO_CHUNK_GROUPED: kernel 2, max_chunks = groups per request
+    const int64_t ctas = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
+    return launch_group<2>(a, tmk, tmv, ctas, L.stream);
+  }
   if (L.k_new) {   // fused append (+ RoPE): the two default shapes
     return L.max_chunks <= 3 ? launch_unit<4, 3, false, true>(a, tmk, tmv, units, L.stream)
                              : launch_unit<4, 2, false, true>(a, tmk, tmv, units, L.stream);

@@ -468,9 +468,21 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
   if (page_size <= 0 || page_size % neo::kTileTokens || page_size > neo::kMaxChunkTokens)
     return neo::fail(NEO_ERR_UNSUPPORTED, "page_size must be a positive multiple of 16, <= 512");
   std::vector<int32_t> ntiles(static_cast<size_t>(batch));
+  int32_t lmin = INT32_MAX, lmax = 0;
   for (int32_t b = 0; b < batch; ++b) {
     if (seq_lens[b] < 0) return neo::fail(NEO_ERR_INVALID_ARG, "seq_lens[" + std::to_string(b) + "] < 0");
     ntiles[b] = (seq_lens[b] + neo::kTileTokens - 1) / neo::kTileTokens;
+    if (seq_lens[b] > 0) lmin = std::min(lmin, seq_lens[b]), lmax = std::max(lmax, seq_lens[b]);
+  }
+  const int sms = neo::device_sm_count();
+  // Grouped kernel: every request one CTA-group (<= 4096 tokens), lengths within
+  // 1.5x (equal CTAs) and >= 4 waves of (4-warp, 3-per-SM) CTAs -- the regime
+  // where it measured faster than every split chunk (c2 +1.8 %, c4 at N = 1 / 2
+  // +3.5 %); skewed, long or few-CTA batches measured slower there.
+  if (lmax > 0 && lmax <= neo::kGroupTiles * neo::kTileTokens && 2 * static_cast<int64_t>(lmax) <= 3 * static_cast<int64_t>(lmin) &&
+      static_cast<int64_t>(batch) * hkv >= static_cast<int64_t>(4) * sms * 3) {
+    *chunk_tokens = NEO_CHUNK_GROUPED;
+    return NEO_OK;
   }
   // candidates (largest first), those that are multiples of P: the sizes the
   // same-box sweeps resolved (profiles/r01_chunk_plan.md); finer steps only let the
@@ -480,7 +492,6 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
   for (int32_t C : kCand)
     if (C % page_size == 0) cand.push_back(C);
   if (cand.empty()) cand.push_back(page_size);
-  const int sms = neo::device_sm_count();
   const int32_t ct_max = cand.front() / neo::kTileTokens;
   int64_t units = 0;
   for (int32_t t : ntiles) units += static_cast<int64_t>(hkv) * ((t + ct_max - 1) / ct_max);
@@ -526,6 +537,7 @@ static neo_status attn_shape(int32_t batch, int32_t hq, int32_t hkv, int32_t d, 
   if (hq % hkv != 0) return fail(NEO_ERR_INVALID_ARG, "num_q_heads must be a multiple of num_kv_heads");
   if (d != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
   if (hq / hkv > neo::kMaxGroup) return fail(NEO_ERR_UNSUPPORTED, "GQA group size G = Hq/Hkv must be <= 8");
+  if (*chunk_tokens == NEO_CHUNK_GROUPED) return NEO_OK;
   if (*chunk_tokens == 0) {
     *chunk_tokens = neo::default_chunk(batch, hkv, max_seq_len);
     if (page_size > 0 && *chunk_tokens % page_size) *chunk_tokens = page_size * ((*chunk_tokens + page_size - 1) / page_size);
@@ -538,7 +550,8 @@ NEO_API neo_status neo_decode_attn_workspace_bytes(int32_t batch, int32_t hq, in
   if (!bytes) return fail(NEO_ERR_INVALID_ARG, "bytes is NULL");
   neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, 16);
   if (st != NEO_OK) return st;
-  const int32_t max_chunks = std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
+  const int32_t max_chunks = chunk_tokens == NEO_CHUNK_GROUPED ? neo::max_groups_for(max_seq_len)
+                                                              : std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
   *bytes = neo::workspace_required(batch, hq, hkv, max_chunks);
   return NEO_OK;
 }
@@ -556,6 +569,7 @@ static neo_status decode_attn_impl(const void* q, const void* k_pages, const voi
                                    int32_t chunk_tokens, void* workspace, size_t workspace_bytes, void* stream,
                                    const float* inv_freq, const void* k_new, const void* v_new) {
   if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
+  if (k_new && chunk_tokens == NEO_CHUNK_GROUPED) chunk_tokens = 0;   // the fused append runs split-K
   neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, page_size);
   if (st != NEO_OK) return st;
   if (batch == 0) return NEO_OK;
@@ -570,7 +584,9 @@ static neo_status decode_attn_impl(const void* q, const void* k_pages, const voi
   if (max_blocks < 1 || static_cast<int64_t>(max_seq_len) > static_cast<int64_t>(max_blocks) * page_size)
     return fail(NEO_ERR_INVALID_ARG, "max_seq_len exceeds max_blocks * page_size");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(NEO_ERR_INVALID_ARG, "scale must be finite and > 0");
-  const int32_t max_chunks = std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
+  const bool grouped = chunk_tokens == NEO_CHUNK_GROUPED;
+  const int32_t max_chunks = grouped ? neo::max_groups_for(max_seq_len)
+                                     : std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
   if (!neo::workspace_layout(batch, hq, hkv, max_chunks, workspace_bytes).fits)
     return fail(NEO_ERR_INVALID_ARG, "workspace too small: need " +
                                          std::to_string(neo::workspace_required(batch, hq, hkv, max_chunks)) + " bytes");
@@ -586,6 +602,7 @@ static neo_status decode_attn_impl(const void* q, const void* k_pages, const voi
   if (st != NEO_OK) return st;
   neo::AttnLaunch L{q, out, block_table, seq_lens, workspace, workspace_bytes, batch, hq, hkv, page_size,
                     max_blocks, chunk_tokens, max_chunks, scale, s};
+  L.grouped = grouped;
   if (k_new) {
     L.inv_freq = inv_freq;
     L.k_new = k_new;

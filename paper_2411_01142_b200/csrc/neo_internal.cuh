@@ -42,7 +42,13 @@ struct AttnLaunch {
   void* k_pages = nullptr;
   void* v_pages = nullptr;
   int64_t page_stride = 0;
+  bool grouped = false;        // NEO_CHUNK_GROUPED: max_chunks holds the group count
 };
+constexpr int kGroupTiles = 4 * 64;                   // tiles per group of the grouped kernel
+inline int32_t max_groups_for(int32_t max_seq_len) {
+  const int32_t tiles = (max_seq_len + kTileTokens - 1) / kTileTokens;
+  return tiles > 0 ? (tiles + kGroupTiles - 1) / kGroupTiles : 1;
+}
 // Byte layout of a workspace of `ws_bytes` bytes for a call shape.  The
 // completion counters occupy [0, counter_cap(ws_bytes)) -- a region fixed by the
 // workspace size alone, so calls of different shapes sharing one workspace

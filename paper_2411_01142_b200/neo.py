@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("NEO_LIB") or os.path.join(_HERE, "libneo.so")   # NEO
 
 NEO_OK, NEO_ERR_INVALID_ARG, NEO_ERR_OUT_OF_PAGES, NEO_ERR_UNSUPPORTED, NEO_ERR_CUDA, NEO_ERR_INTERNAL = range(6)
 NEO_GPU, NEO_HOST = 0, 1
+NEO_CHUNK_GROUPED = -1          # chunk_tokens selecting the grouped split-K kernel (include/neo.h)
 STATUS_NAMES = {0: "NEO_OK", 1: "NEO_ERR_INVALID_ARG", 2: "NEO_ERR_OUT_OF_PAGES", 3: "NEO_ERR_UNSUPPORTED",
                 4: "NEO_ERR_CUDA", 5: "NEO_ERR_INTERNAL"}
 

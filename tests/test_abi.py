@@ -135,6 +135,9 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0):
     def shape(mc):
         return (4, 2) if mc <= 3 else (4, 3)          # (warps, CTAs/SM)
 
+    pos = [c for c in ctx if c > 0]
+    if pos and max(pos) <= 4096 and 2 * max(pos) <= 3 * min(pos) and len(ctx) * hkv >= 4 * sms * 3:
+        return -1                                     # NEO_CHUNK_GROUPED
     ct0 = cands[0] // 16
     units = sum(hkv * -(-t // ct0) for t in nt)
     w, k = shape(max([-(-t // ct0) for t in nt] + [1]))
@@ -170,16 +173,18 @@ def test_plan_chunk():
         B, hkv, P = int(rng.integers(1, 700)), int(rng.choice([1, 2, 4, 8])), int(rng.choice([16, 32, 64]))
         ctx = rng.integers(0, int(rng.choice([300, 3000, 20000])), size=B).astype(np.int32)
         C = neo.plan_chunk(ctx, hkv, P)
-        assert C % 16 == 0 and C % P == 0 and 16 <= C <= 1024
+        assert C == neo.NEO_CHUNK_GROUPED or (C % 16 == 0 and C % P == 0 and 16 <= C <= 1024)
         ref = _plan_replay(ctx.tolist(), hkv, P)
         if ref is not None:
             assert C == ref, (B, hkv, P, C, ref)
     c5 = WORKLOADS["c5"].contexts()
     assert neo.plan_chunk(c5, 8, 16) == 1024                  # many waves: the longest chunk
     c4 = WORKLOADS["c4"].contexts()
-    # profiles/r01_chunk_plan.md: the measured best C of the c4 shards at N = 8 and 4
-    # (384, 640) and within 1 % of it at N = 2 and 1 (640)
-    assert [neo.plan_chunk(c4, 8 // n, 16) for n in (8, 4, 2, 1)] == [384, 640, 640, 640]
+    # profiles/r01_chunk_plan.md: the measured best split C of the c4 shards at N = 8
+    # and 4 (384, 640); N = 2 and 1 are uniform, many-CTA batches -> grouped kernel
+    assert [neo.plan_chunk(c4, 8 // n, 16) for n in (8, 4, 2, 1)] == [384, 640, -1, -1]
+    # uniform ~1K batches of 2048 (request, kv-head) pairs take the grouped kernel (c2)
+    assert neo.plan_chunk(WORKLOADS["c2"].contexts(), 8, 16) == neo.NEO_CHUNK_GROUPED
     assert neo.plan_chunk([], 8, 16) == neo.default_chunk(0, 8, 0)
     with pytest.raises(neo.NeoError) as e:
         neo.plan_chunk([5, -1], 8, 16)
@@ -190,6 +195,20 @@ def test_plan_chunk():
     with pytest.raises(neo.NeoError) as e:
         neo.plan_chunk([5], 0, 16)
     assert e.value.status == neo.NEO_ERR_INVALID_ARG
+
+
+def test_grouped_workspace_and_chunk_validation():
+    """NEO_CHUNK_GROUPED: requests <= 4096 tokens need no partials (counters only);
+    longer ones one partial row set per 4096-token group.  Other negatives are invalid."""
+    one = neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=neo.NEO_CHUNK_GROUPED)
+    three = neo.workspace_bytes(256, 32, 8, 9000, chunk_tokens=neo.NEO_CHUNK_GROUPED)
+    assert one < 256 * 8 * 4 * 64 * 2                      # counter region only
+    units = 256 * 8 * 3
+    assert three >= units * 4 * 8 + units * 4 * 128 * 4
+    with pytest.raises(neo.NeoError) as e:
+        neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=-2)
+    assert e.value.status == neo.NEO_ERR_UNSUPPORTED
+    assert _attn(C=-1) != neo.NEO_ERR_UNSUPPORTED           # accepted (fails later only on fake pointers)
 
 
 def test_pool_bytes_and_layer_view():

@@ -162,7 +162,7 @@ def test_relocation_and_poison_bitwise():
     a = Case(ctx, 32, 8, seed=9, table_seed=1, tail="zero", fill_unused="zero", extra_pages=0)
     b = Case(ctx, 32, 8, seed=9, table_seed=2, tail="nan", fill_unused="nan", extra_pages=40)
     assert not np.array_equal(a.table, b.table)
-    for chunk in (0, 16, 64):
+    for chunk in (0, 16, 64, -1):
         import torch
         oa = a.run(chunk_tokens=chunk)
         ob = b.run(chunk_tokens=chunk)
@@ -410,3 +410,52 @@ def test_decode_attn_append_rope_vs_oracle(chunk, P):
         ref = oracle.decode_attention(qr, kreq, case.v_req[b], np.float32(case.scale))
         ok, ratio = within_tol(got[b], ref)
         assert ok, (b, n, ratio)
+
+
+# ---- grouped split-K kernel (chunk_tokens = NEO_CHUNK_GROUPED = -1)
+
+GROUPED = -1
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (64, 8), (32, 32), (28, 4), (24, 8), (8, 1), (40, 8)])
+def test_parity_grouped(hq, hkv):
+    """One CTA per group of <= 256 tiles, 4 per-warp ranges merged in shared memory;
+    > 4096 tokens run several groups and the cross-group combine."""
+    ctx = [1, 15, 16, 17, 63, 65, 255, 256, 257, 1000, 4095, 4096, 4097, 4111, 8192, 9000]
+    check_case(Case(ctx, hq, hkv, seed=21 + hq + hkv), GROUPED, f"grouped G={hq // hkv}")
+
+
+@pytest.mark.parametrize("P", [32, 64])
+def test_parity_grouped_page_sizes(P):
+    check_case(Case([1, 31, 32, 33, 700, 5000], 32, 8, P=P, seed=22 + P), GROUPED, f"grouped P={P}")
+
+
+@pytest.mark.parametrize("variant", [ni.VARIANT_PEAKED, ni.VARIANT_SINK, ni.VARIANT_PEAKED | ni.VARIANT_SINK])
+def test_parity_grouped_variants(variant):
+    check_case(Case([3, 500, 1100, 4500], 64, 8, seed=23, variant=variant), GROUPED, f"grouped variant={variant}")
+
+
+def test_grouped_empty_determinism_and_batch_independence():
+    """Empty contexts give zero rows; outputs are bitwise run to run and a request's
+    row does not depend on the other requests of the batch (the split is a function
+    of its own length)."""
+    import torch
+    full = Case([0, 5, 0, 300, 4200, 1000], 32, 8, seed=24)
+    outs = [full.run(chunk_tokens=GROUPED).clone() for _ in range(3)]
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int16), outs[0].view(torch.int16))
+    got = full.out_f64(outs[0])
+    assert (got[0] == 0).all() and (got[2] == 0).all()
+    for b in (1, 3, 4, 5):
+        assert within_tol(got[b], full.oracle(b))[0]
+
+
+def test_grouped_under_cuda_graph_and_workspace_reuse():
+    import torch
+
+    from paper_2411_01142_b200 import neo
+    case = Case([100, 4500, 9000, 33], 32, 8, seed=25)
+    ws = neo.make_workspace(case.B, 32, 8, case.max_seq_len, GROUPED)
+    eager = case.run(chunk_tokens=GROUPED, workspace=ws).clone()
+    again = case.run(chunk_tokens=GROUPED, workspace=ws).clone()
+    assert torch.equal(eager.view(torch.int16), again.view(torch.int16))
