@@ -275,9 +275,9 @@ NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_head
  * CTA dispatch of the chunk-major grid predicts fastest, so that the last wave
  * of work units is not left mostly empty (DESIGN §6 "chunk planner").  Grids
  * of >= 4 waves at C = 512 take 512; grids under one wave at C = 128 take
- * neo_decode_attn_default_chunk(); a batch whose requests all fit one group
- * (<= 4096 tokens), within a 1.5x length spread and with >= 4 waves of CTAs,
- * takes NEO_CHUNK_GROUPED.  Pure host computation, no GPU work; the SM
+ * neo_decode_attn_default_chunk(); the grouped kernel, replayed the same way,
+ * is taken (NEO_CHUNK_GROUPED) when it beats the best split chunk by > 1 %.
+ * Pure host computation, no GPU work; the SM
  * count is the current device's (148 when no device is visible).
  *   seq_lens     [batch] int32, HOST, each >= 0 (the values the call will see).
  *   chunk_tokens out: a valid chunk_tokens argument for page_size (possibly

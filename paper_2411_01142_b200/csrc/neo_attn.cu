@@ -929,6 +929,16 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
   return NEO_OK;
 }
 
+// Stages per warp of the grouped kernel: 2 (3 CTAs/SM); NEO_ATTN_GROUP_STAGES=3
+// (2 CTAs/SM) is an experiment knob.
+static int group_stages() {
+  static const int k = [] {
+    const char* v = std::getenv("NEO_ATTN_GROUP_STAGES");
+    return v ? std::atoi(v) : 2;
+  }();
+  return k;
+}
+
 template <int S>
 static neo_status launch_group(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t ctas,
                                cudaStream_t stream) {
@@ -1008,7 +1018,8 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
   if (L.grouped) {   // NEO_CHUNK_GROUPED: kernel 2, max_chunks = groups per request
     const int64_t ctas = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
-    return launch_group<2>(a, tmk, tmv, ctas, L.stream);
+    return group_stages() == 3 ? launch_group<3>(a, tmk, tmv, ctas, L.stream)
+                               : launch_group<2>(a, tmk, tmv, ctas, L.stream);
   }
   if (L.k_new) {   // fused append (+ RoPE): the two default shapes
     return L.max_chunks <= 3 ? launch_unit<4, 3, false, true>(a, tmk, tmv, units, L.stream)

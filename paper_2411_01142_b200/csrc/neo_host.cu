@@ -214,6 +214,37 @@ double plan_score(const std::vector<int32_t>& ntiles, int32_t hkv, int32_t chunk
   return makespan > 0 ? static_cast<double>(total) * hkv / makespan : 0.0;
 }
 
+// The grouped kernel in the same replay: CTA (q, b, g) in group-major order,
+// 3 CTAs per SM, cost = kPlanGroupOverheadTiles + its per-warp tile range
+// (fitted on the same sweeps: profiles/r01_grouped_sweep.txt).
+constexpr double kPlanGroupOverheadTiles = 3.0;
+
+double plan_score_grouped(const std::vector<int32_t>& ntiles, int32_t hkv, int sms) {
+  int32_t max_groups = 1;
+  int64_t total = 0;
+  for (int32_t t : ntiles) {
+    max_groups = std::max(max_groups, (t + kGroupTiles - 1) / kGroupTiles);
+    total += t;
+  }
+  std::vector<double> slot(static_cast<size_t>(sms) * 3, 0.0);
+  for (int32_t q = 0; q < max_groups; ++q) {
+    for (int32_t t : ntiles) {
+      const int32_t ng = (t + kGroupTiles - 1) / kGroupTiles;
+      if (q >= ng) continue;
+      const int32_t tg = (t + ng - 1) / ng;
+      const int32_t g0 = q * tg, g1 = std::min(g0 + tg, t);
+      const int32_t tw = (g1 - g0 + 3) / 4;
+      for (int32_t g = 0; g < hkv; ++g) {
+        std::pop_heap(slot.begin(), slot.end(), std::greater<double>());
+        slot.back() += kPlanGroupOverheadTiles + tw;
+        std::push_heap(slot.begin(), slot.end(), std::greater<double>());
+      }
+    }
+  }
+  const double makespan = *std::max_element(slot.begin(), slot.end());
+  return makespan > 0 ? static_cast<double>(total) * hkv / makespan : 0.0;
+}
+
 int device_sm_count() {
   int dev = 0, n = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -468,22 +499,11 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
   if (page_size <= 0 || page_size % neo::kTileTokens || page_size > neo::kMaxChunkTokens)
     return neo::fail(NEO_ERR_UNSUPPORTED, "page_size must be a positive multiple of 16, <= 512");
   std::vector<int32_t> ntiles(static_cast<size_t>(batch));
-  int32_t lmin = INT32_MAX, lmax = 0;
   for (int32_t b = 0; b < batch; ++b) {
     if (seq_lens[b] < 0) return neo::fail(NEO_ERR_INVALID_ARG, "seq_lens[" + std::to_string(b) + "] < 0");
     ntiles[b] = (seq_lens[b] + neo::kTileTokens - 1) / neo::kTileTokens;
-    if (seq_lens[b] > 0) lmin = std::min(lmin, seq_lens[b]), lmax = std::max(lmax, seq_lens[b]);
   }
   const int sms = neo::device_sm_count();
-  // Grouped kernel: every request one CTA-group (<= 4096 tokens), lengths within
-  // 1.5x (equal CTAs) and >= 4 waves of (4-warp, 3-per-SM) CTAs -- the regime
-  // where it measured faster than every split chunk (c2 +1.8 %, c4 at N = 1 / 2
-  // +3.5 %); skewed, long or few-CTA batches measured slower there.
-  if (lmax > 0 && lmax <= neo::kGroupTiles * neo::kTileTokens && 2 * static_cast<int64_t>(lmax) <= 3 * static_cast<int64_t>(lmin) &&
-      static_cast<int64_t>(batch) * hkv >= static_cast<int64_t>(4) * sms * 3) {
-    *chunk_tokens = NEO_CHUNK_GROUPED;
-    return NEO_OK;
-  }
   // candidates (largest first), those that are multiples of P: the sizes the
   // same-box sweeps resolved (profiles/r01_chunk_plan.md); finer steps only let the
   // model's error pick worse neighbours
@@ -492,20 +512,8 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
   for (int32_t C : kCand)
     if (C % page_size == 0) cand.push_back(C);
   if (cand.empty()) cand.push_back(page_size);
-  const int32_t ct_max = cand.front() / neo::kTileTokens;
-  int64_t units = 0;
-  for (int32_t t : ntiles) units += static_cast<int64_t>(hkv) * ((t + ct_max - 1) / ct_max);
-  int32_t max_chunks = 1;
-  for (int32_t t : ntiles) max_chunks = std::max(max_chunks, (t + ct_max - 1) / ct_max);
-  const neo::AttnShape sh = neo::default_attn_shape(max_chunks);
-  const double waves = static_cast<double>(units) / (static_cast<double>(sms) * sh.ctas_per_sm * sh.warps);
-  // Many waves: the tail is amortised and the longest chunk (fewest pipeline
-  // ramps and partials) wins (c5 sweeps).  Under one wave at the smallest
-  // candidate the call is latency-bound: keep the shape-only default.
-  if (waves >= 16.0) {
-    *chunk_tokens = cand.front();
-    return NEO_OK;
-  }
+  // Under one wave at the smallest candidate the call is latency-bound: keep the
+  // shape-only default.
   const int32_t ct_min = cand.back() / neo::kTileTokens;
   int64_t units_min = 0;
   for (int32_t t : ntiles) units_min += static_cast<int64_t>(hkv) * ((t + ct_min - 1) / ct_min);
@@ -517,16 +525,30 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
     *chunk_tokens = std::min(C, neo::kMaxChunkTokens);
     return NEO_OK;
   }
+  const int32_t ct_max = cand.front() / neo::kTileTokens;
+  int64_t units = 0;
+  int32_t max_chunks = 1;
+  for (int32_t t : ntiles) {
+    units += static_cast<int64_t>(hkv) * ((t + ct_max - 1) / ct_max);
+    max_chunks = std::max(max_chunks, (t + ct_max - 1) / ct_max);
+  }
+  const neo::AttnShape sh = neo::default_attn_shape(max_chunks);
+  const double waves = static_cast<double>(units) / (static_cast<double>(sms) * sh.ctas_per_sm * sh.warps);
   int32_t best = cand.front();
   double best_score = -1.0;
-  for (int32_t C : cand) {        // largest first: a smaller C must win by > 1 %
-    const double sc = neo::plan_score(ntiles, hkv, C / neo::kTileTokens, sms);
-    if (sc > best_score * 1.01) {
-      best = C;
-      best_score = sc;
+  if (waves >= 16.0) {   // many waves: the tail is amortised and the longest chunk wins (c5 sweeps)
+    best_score = neo::plan_score(ntiles, hkv, ct_max, sms);
+  } else {
+    for (int32_t C : cand) {        // largest first: a smaller C must win by > 1 %
+      const double sc = neo::plan_score(ntiles, hkv, C / neo::kTileTokens, sms);
+      if (sc > best_score * 1.01) {
+        best = C;
+        best_score = sc;
+      }
     }
   }
-  *chunk_tokens = best;
+  // the grouped kernel must beat the best split chunk by > 1 % in the same model
+  *chunk_tokens = neo::plan_score_grouped(ntiles, hkv, sms) > best_score * 1.01 ? NEO_CHUNK_GROUPED : best;
   return NEO_OK;
 }
 

@@ -124,10 +124,12 @@ def test_workspace_bytes_and_default_chunk():
     assert big <= 1.05 * data + 65536
 
 
-def _plan_replay(ctx, hkv, P, sms=148, o=6.0):
+def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=3.0):
     """Independent replay of the planner's model (include/neo.h
-    neo_decode_attn_plan_chunk): chunk-major units, W = 4 per CTA, CTAs taken
-    in order by the earliest-free slot (SMs x CTAs/SM of the default shape)."""
+    neo_decode_attn_plan_chunk): split-K units in chunk-major order, W = 4 per CTA,
+    CTAs taken in order by the earliest-free slot (SMs x CTAs/SM of the default
+    shape); the grouped kernel's CTAs likewise at 3 per SM.  None = latency-bound
+    (library default)."""
     import heapq
     nt = [(c + 15) // 16 for c in ctx]
     cands = [C for C in (1024, 640, 512, 448, 384, 320, 256) if C % P == 0] or [P]
@@ -135,19 +137,7 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0):
     def shape(mc):
         return (4, 2) if mc <= 3 else (4, 3)          # (warps, CTAs/SM)
 
-    pos = [c for c in ctx if c > 0]
-    if pos and max(pos) <= 4096 and 2 * max(pos) <= 3 * min(pos) and len(ctx) * hkv >= 4 * sms * 3:
-        return -1                                     # NEO_CHUNK_GROUPED
-    ct0 = cands[0] // 16
-    units = sum(hkv * -(-t // ct0) for t in nt)
-    w, k = shape(max([-(-t // ct0) for t in nt] + [1]))
-    if units >= 16 * sms * k * w:
-        return cands[0]
-    ctn = cands[-1] // 16
-    if sum(hkv * -(-t // ctn) for t in nt) < sms * 8:
-        return None                                   # latency-bound: library default
-    best, best_sc = cands[0], -1.0
-    for C in cands:
+    def split_score(C):
         ct = C // 16
         mc = max([-(-t // ct) for t in nt] + [1])
         w, k = shape(mc)
@@ -158,10 +148,37 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0):
             m = max(units[i:i + w])
             if m:
                 heapq.heapreplace(heap, heap[0] + o + m)
-        sc = sum(nt) * hkv / max(heap)
-        if sc > best_sc * 1.01:
-            best, best_sc = C, sc
-    return best
+        return sum(nt) * hkv / max(heap)
+
+    def grouped_score():
+        heap = [0.0] * (sms * 3)
+        mg = max([-(-t // 256) for t in nt] + [1])
+        for q in range(mg):
+            for t in nt:
+                ng = -(-t // 256)
+                if q >= ng:
+                    continue
+                tg = -(-t // ng)
+                g0, g1 = q * tg, min(q * tg + tg, t)
+                for _ in range(hkv):
+                    heapq.heapreplace(heap, heap[0] + og + -(-(g1 - g0) // 4))
+        return sum(nt) * hkv / max(heap)
+
+    ctn = cands[-1] // 16
+    if sum(hkv * -(-t // ctn) for t in nt) < sms * 8:
+        return None
+    ct0 = cands[0] // 16
+    units = sum(hkv * -(-t // ct0) for t in nt)
+    w, k = shape(max([-(-t // ct0) for t in nt] + [1]))
+    if units >= 16 * sms * k * w:
+        best, best_sc = cands[0], split_score(cands[0])
+    else:
+        best, best_sc = cands[0], -1.0
+        for C in cands:
+            sc = split_score(C)
+            if sc > best_sc * 1.01:
+                best, best_sc = C, sc
+    return -1 if grouped_score() > best_sc * 1.01 else best
 
 
 def test_plan_chunk():
@@ -178,7 +195,7 @@ def test_plan_chunk():
         if ref is not None:
             assert C == ref, (B, hkv, P, C, ref)
     c5 = WORKLOADS["c5"].contexts()
-    assert neo.plan_chunk(c5, 8, 16) == 1024                  # many waves: the longest chunk
+    assert neo.plan_chunk(c5, 8, 16) == neo.NEO_CHUNK_GROUPED    # profiles/r01_grouped_sweep.txt: +3.3 %
     c4 = WORKLOADS["c4"].contexts()
     # profiles/r01_chunk_plan.md: the measured best split C of the c4 shards at N = 8
     # and 4 (384, 640); N = 2 and 1 are uniform, many-CTA batches -> grouped kernel
