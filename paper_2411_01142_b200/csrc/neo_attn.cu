@@ -721,7 +721,7 @@ __device__ __forceinline__ void group_merge(const KArgs& a, const uint8_t* base,
   }
 }
 
-template <int kStages>
+template <int kStages, bool kFuse = false>
 __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kStages>())
     decode_attn_group_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                              const KArgs a) {
@@ -756,6 +756,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
     if (q == 0 && warp == 0) write_zero_row(a, b, g, lane);
     return;
   }
+  if (kFuse && a.inv_freq && r < a.G) rope_q(qf, qd, ctx - 1, a.inv_freq);
   const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
   const int n_groups = (ntile_total + kGroupWarps * kMaxWarpTiles - 1) / (kGroupWarps * kMaxWarpTiles);
   if (q >= n_groups) return;                       // uniform over the CTA (same b, q)
@@ -787,6 +788,9 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   for (int j = 0; j < nt; ++j) {
     const int s = j % kStages;
     mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
+    // fused append: the warp whose range ends the request holds the new token
+    if (kFuse && t_begin + nt == ntile_total && j == nt - 1)
+      patch_new_token(a, sbase + s * kStageBytes, b, g, ctx, lane);
     Frags f;
     load_frags(sbase + s * kStageBytes, r, qd, f);
     __syncwarp();
@@ -939,14 +943,14 @@ static int group_stages() {
   return k;
 }
 
-template <int S>
+template <int S, bool kFuse>
 static neo_status launch_group(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t ctas,
                                cudaStream_t stream) {
   static bool configured = false;
   constexpr int smem = kGroupWarps * S * kStageBytes + 1024;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(decode_attn_group_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(decode_attn_group_kernel<S, kFuse>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_group_kernel)");
     configured = true;
   }
@@ -960,7 +964,7 @@ static neo_status launch_group(const KArgs& a, const CUtensorMap& tmk, const CUt
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, decode_attn_group_kernel<S>, tmk, tmv, a);
+  cudaLaunchKernelEx(&cfg, decode_attn_group_kernel<S, kFuse>, tmk, tmv, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_attn_group_kernel launch");
   return NEO_OK;
@@ -1018,8 +1022,9 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
   if (L.grouped) {   // NEO_CHUNK_GROUPED: kernel 2, max_chunks = groups per request
     const int64_t ctas = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
-    return group_stages() == 3 ? launch_group<3>(a, tmk, tmv, ctas, L.stream)
-                               : launch_group<2>(a, tmk, tmv, ctas, L.stream);
+    if (L.k_new) return launch_group<2, true>(a, tmk, tmv, ctas, L.stream);
+    return group_stages() == 3 ? launch_group<3, false>(a, tmk, tmv, ctas, L.stream)
+                               : launch_group<2, false>(a, tmk, tmv, ctas, L.stream);
   }
   if (L.k_new) {   // fused append (+ RoPE): the two default shapes
     return L.max_chunks <= 3 ? launch_unit<4, 3, false, true>(a, tmk, tmv, units, L.stream)

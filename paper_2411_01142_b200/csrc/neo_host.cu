@@ -591,7 +591,6 @@ static neo_status decode_attn_impl(const void* q, const void* k_pages, const voi
                                    int32_t chunk_tokens, void* workspace, size_t workspace_bytes, void* stream,
                                    const float* inv_freq, const void* k_new, const void* v_new) {
   if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
-  if (k_new && chunk_tokens == NEO_CHUNK_GROUPED) chunk_tokens = 0;   // the fused append runs split-K
   neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, page_size);
   if (st != NEO_OK) return st;
   if (batch == 0) return NEO_OK;

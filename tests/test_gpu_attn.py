@@ -344,13 +344,13 @@ def test_rope_append_then_attend():
         assert within_tol(got[b], ref)[0]
 
 
-@pytest.mark.parametrize("chunk", [0, 64])
+@pytest.mark.parametrize("chunk", [0, 64, -1])
 def test_decode_attn_append_plain_equals_separate(chunk):
     """neo_decode_attn_append without RoPE == neo_kv_append + neo_decode_attn, bit
     for bit (output and the appended page slots), the new slots poisoned first."""
     import torch
     from paper_2411_01142_b200 import neo
-    ctx_new = [1, 16, 17, 300, 1025, 2048]
+    ctx_new = [1, 16, 17, 300, 1025, 2048, 4097, 5000]
     a = Case(ctx_new, 32, 8, seed=81)
     b = Case(ctx_new, 32, 8, seed=81)
     k_new = np.stack([a.k_req[i][n - 1] for i, n in enumerate(ctx_new)])
@@ -375,7 +375,7 @@ def test_decode_attn_append_plain_equals_separate(chunk):
                                pb[b.table[i, t // b.P], :, t % b.P].view(torch.int16))
 
 
-@pytest.mark.parametrize("chunk,P", [(0, 16), (64, 16), (0, 32)])
+@pytest.mark.parametrize("chunk,P", [(0, 16), (64, 16), (0, 32), (-1, 16), (-1, 32)])
 def test_decode_attn_append_rope_vs_oracle(chunk, P):
     """The one-launch decode step with RoPE: output within tolerance of the oracle
     over the fp64-rotated q and k (bf16-rounded), the page slot's k within
@@ -384,7 +384,7 @@ def test_decode_attn_append_rope_vs_oracle(chunk, P):
     from oracle import rope as orope
     import oracle
     from paper_2411_01142_b200 import neo
-    ctx_new = [1, 17, 300, 4096, 700]
+    ctx_new = [1, 17, 300, 4096, 700, 4097, 6000]
     case = Case(ctx_new, 32, 8, P=P, seed=91 + P)
     f = orope.llama_inv_freq()
     k_new = np.stack([case.k_req[b][n - 1] for b, n in enumerate(ctx_new)])

@@ -19,7 +19,8 @@ from paper_2411_01142_b200 import neo  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 gb = GpuBatch(WORKLOADS[cfg], layers=1)
 k, v = gb.layer(0)
-ws = neo.make_workspace(gb.B, gb.hq, gb.hkv, gb.max_seq_len)
+C = int(sys.argv[2]) if len(sys.argv) > 2 else neo.plan_chunk(gb.ctx, gb.hkv, gb.P)   # the a0 planner's choice
+ws = neo.make_workspace(gb.B, gb.hq, gb.hkv, gb.max_seq_len, C)
 out = torch.empty(gb.B, gb.hq, 128, dtype=torch.bfloat16, device="cuda")
 kn = torch.randn(gb.B, gb.hkv, 128, dtype=torch.bfloat16, device="cuda")
 vn = torch.randn(gb.B, gb.hkv, 128, dtype=torch.bfloat16, device="cuda")
@@ -29,7 +30,7 @@ flush = torch.ones(128 << 20, dtype=torch.int32, device="cuda")
 
 
 def attn():
-    neo.decode_attn(q, k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=out, workspace=ws)
+    neo.decode_attn(q, k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=out, workspace=ws, chunk_tokens=C)
 
 
 def separate():
@@ -39,7 +40,7 @@ def separate():
 
 def fused():
     neo.decode_attn_append(q, k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, kn, vn, inv_freq=inv, out=out,
-                           workspace=ws)
+                           workspace=ws, chunk_tokens=C)
 
 
 def timed(fn, reps=20):
@@ -59,4 +60,4 @@ def timed(fn, reps=20):
 kvb = gb.kv_bytes_per_call()
 for name, fn in (("attention only", attn), ("rope_append + attention", separate), ("fused (one launch)", fused)):
     t = timed(fn)
-    print(f"{cfg} {name:26s} {t:8.1f} us   {kvb / t / 1e3:7.1f} GB/s of KV")
+    print(f"{cfg} C={C} {name:26s} {t:8.1f} us   {kvb / t / 1e3:7.1f} GB/s of KV")
