@@ -271,27 +271,29 @@ def test_kv_append_then_attend(P):
     check_case(case, 64, f"append P={P}")
 
 
-def test_cuda_graph_capture_matches_eager():
-    """decode_attn launches (PDL attribute, fused combine counters) captured in a
-    CUDA graph and replayed give the eager results bit for bit, replay after replay."""
+@pytest.mark.parametrize("C", [64, -1])
+def test_cuda_graph_capture_matches_eager(C):
+    """decode_attn launches (PDL attribute, fused combine counters; split and
+    grouped kernels) captured in a CUDA graph and replayed give the eager results
+    bit for bit, replay after replay."""
     import torch
     from paper_2411_01142_b200 import neo
-    cases = [Case([5, 300, 1100, 40], 32, 8, seed=60 + i) for i in range(3)]
-    ws = neo.make_workspace(4, 32, 8, 1100, chunk_tokens=64)
-    eager = [c.run(chunk_tokens=64, workspace=ws).clone() for c in cases]
+    cases = [Case([5, 300, 1100, 40, 5000], 32, 8, seed=60 + i) for i in range(3)]
+    ws = neo.make_workspace(5, 32, 8, 5000, chunk_tokens=C)
+    eager = [c.run(chunk_tokens=C, workspace=ws).clone() for c in cases]
     outs = [torch.empty_like(e) for e in eager]
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):                                  # warm-up on the capture stream
         for c, o in zip(cases, outs):
-            neo.decode_attn(c.q_dev, c.k_dev, c.v_dev, c.bt_dev, c.sl_dev, c.max_seq_len, out=o, chunk_tokens=64,
+            neo.decode_attn(c.q_dev, c.k_dev, c.v_dev, c.bt_dev, c.sl_dev, c.max_seq_len, out=o, chunk_tokens=C,
                             workspace=ws)
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         for c, o in zip(cases, outs):
-            neo.decode_attn(c.q_dev, c.k_dev, c.v_dev, c.bt_dev, c.sl_dev, c.max_seq_len, out=o, chunk_tokens=64,
+            neo.decode_attn(c.q_dev, c.k_dev, c.v_dev, c.bt_dev, c.sl_dev, c.max_seq_len, out=o, chunk_tokens=C,
                             workspace=ws)
     for rep in range(3):
         for o in outs:
@@ -450,7 +452,9 @@ def test_grouped_empty_determinism_and_batch_independence():
         assert within_tol(got[b], full.oracle(b))[0]
 
 
-def test_grouped_under_cuda_graph_and_workspace_reuse():
+def test_grouped_workspace_reuse():
+    """The multi-group combine leaves its counters at zero: a reused workspace
+    gives bitwise the same output (graph capture: test_cuda_graph_capture_matches_eager)."""
     import torch
 
     from paper_2411_01142_b200 import neo
