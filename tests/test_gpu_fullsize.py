@@ -88,8 +88,9 @@ def test_fullsize_request_shard_c5():
     run_and_sample(wl, [0], 6, rng, ctx=ctx, req_ids=parts[3])
 
 
+@pytest.mark.parametrize("C", [256, -1])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_head_shards_reassemble_bitwise(world):
+def test_head_shards_reassemble_bitwise(world, C):
     """KV-head shards (each rank's own heads, own pool),
     reassembled along heads, equal the unsharded output bit for bit at the same C."""
     import torch
@@ -100,7 +101,6 @@ def test_head_shards_reassemble_bitwise(world):
     from paper_2411_01142_b200.shard import head_shard
     wl = WORKLOADS["c4"]
     ctx = wl.contexts()[:96]
-    C = 256
     full = GpuBatch(wl, ctx=ctx, layers=1)
     k, v = full.layer(0)
     ref = neo.decode_attn(full.q[0], k, v, full.block_table, full.seq_lens, full.max_seq_len, chunk_tokens=C)
@@ -116,9 +116,11 @@ def test_head_shards_reassemble_bitwise(world):
     assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
 
 
-def test_request_shards_reassemble_bitwise():
+@pytest.mark.parametrize("C", [128, -1])
+def test_request_shards_reassemble_bitwise(C):
     """Request (LPT) shards in their own pools and batches equal the unsharded
-    output bit for bit: a request's result depends only on its inputs and C."""
+    output bit for bit: a request's result depends only on its inputs and C
+    (for the grouped kernel, C = -1: on its own length)."""
     import torch
 
     from neo_inputs.gpu import GpuBatch
@@ -127,7 +129,6 @@ def test_request_shards_reassemble_bitwise():
     from paper_2411_01142_b200.shard import lpt_assign
     wl = WORKLOADS["c5"]
     ctx = wl.contexts()[:200]
-    C = 128
     full = GpuBatch(wl, ctx=ctx, layers=1)
     k, v = full.layer(0)
     ref = neo.decode_attn(full.q[0], k, v, full.block_table, full.seq_lens, full.max_seq_len, chunk_tokens=C)
