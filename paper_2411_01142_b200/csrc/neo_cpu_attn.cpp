@@ -271,7 +271,42 @@ NEO_BF16_TARGET void task_avx512bf16(const Job& jb, int b, int g, int j0, int j1
         m2[h] = mn;
         _mm512_store_ps(pw[h], p);
       }
-      // (a5) P.V: two heads at a time with their accumulators in registers
+      // (a5) P.V.  G a multiple of 4: four heads at a time over one half of the
+      // dims per pass (16 accumulators in registers), so each V row is widened
+      // once per head quad instead of once per head pair.
+      if (kG > 0 && kG % 4 == 0) {
+#pragma GCC unroll 2
+        for (int h = 0; h < G; h += 4) {
+#pragma GCC unroll 2
+          for (int half = 0; half < 2; ++half) {
+            const int c0 = 4 * half;
+            __m512 a[4][4];
+#pragma GCC unroll 4
+            for (int i = 0; i < 4; ++i) {
+              const __m512 al = _mm512_set1_ps(alpha[h + i]);
+#pragma GCC unroll 4
+              for (int c = 0; c < 4; ++c) a[i][c] = _mm512_mul_ps(_mm512_loadu_ps(&out.acc[h + i][16 * (c0 + c)]), al);
+            }
+            for (int t = 0; t < nt; ++t) {
+              __m512 v[4];
+#pragma GCC unroll 4
+              for (int c = 0; c < 4; ++c) v[c] = load_bf16x16(V + t * kD + 16 * (c0 + c));
+#pragma GCC unroll 4
+              for (int i = 0; i < 4; ++i) {
+                const __m512 p = _mm512_set1_ps(pw[h + i][t]);
+#pragma GCC unroll 4
+                for (int c = 0; c < 4; ++c) a[i][c] = _mm512_fmadd_ps(p, v[c], a[i][c]);
+              }
+            }
+#pragma GCC unroll 4
+            for (int i = 0; i < 4; ++i)
+#pragma GCC unroll 4
+              for (int c = 0; c < 4; ++c) _mm512_storeu_ps(&out.acc[h + i][16 * (c0 + c)], a[i][c]);
+          }
+        }
+        continue;
+      }
+      // otherwise two heads at a time with their accumulators in registers
 #pragma GCC unroll 4
       for (int h = 0; h < G; h += 2) {
         const bool two = h + 1 < G;
