@@ -146,11 +146,13 @@ NEO_API neo_status neo_kv_layer_view(const neo_kv_pool* pool, int32_t layer, voi
  *   scale       softmax scale, typically 1/sqrt(D) (DESIGN c1).
  *   chunk_tokens split-K chunk length C (multiple of 16 and of P, <= 1024), or 0 for
  *               the library default neo_decode_attn_default_chunk(), or
- *               NEO_CHUNK_GROUPED: each request's tiles split into ceil(tiles/256)
- *               equal groups of four equal per-warp ranges, one CTA per group,
- *               merged in shared memory (no partials for requests <= 4096
- *               tokens); neo_decode_attn_plan_chunk() picks it for uniform
- *               batches of many such requests.  The result for
+ *               NEO_CHUNK_GROUPED (-1), -2 or -4: the grouped kernel -- each
+ *               request's tiles split into ceil(tiles / (256/k)) equal groups
+ *               (k = 1, 2, 4: groups of at most 4096, 2048, 1024 tokens) of four
+ *               equal per-warp ranges, one CTA per group, merged in shared
+ *               memory; single-group requests need no partials.
+ *               neo_decode_attn_plan_chunk() picks among these and the split
+ *               chunks.  The result for
  *               request b depends only on (its inputs, C): outputs are bitwise
  *               deterministic run to run (fixed merge order, no float atomics).
  *   workspace   device scratch of >= neo_decode_attn_workspace_bytes(...) bytes,
@@ -261,7 +263,8 @@ NEO_API neo_status neo_decode_attn_append(const void* q, const float* inv_freq, 
                                           int32_t chunk_tokens, void* workspace, size_t workspace_bytes,
                                           void* stream);
 
-/* chunk_tokens value selecting the grouped split-K kernel (see neo_decode_attn). */
+/* chunk_tokens value selecting the grouped split-K kernel with groups of <= 4096
+ * tokens; -2 and -4 select groups of <= 2048 and <= 1024 tokens (neo_decode_attn). */
 #define NEO_CHUNK_GROUPED (-1)
 
 /* Default split-K chunk length for a call shape (deterministic in its inputs). */
@@ -276,12 +279,13 @@ NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_head
  * of work units is not left mostly empty (DESIGN §6 "chunk planner").  Grids
  * of >= 4 waves at C = 512 take 512; grids under one wave at C = 128 take
  * neo_decode_attn_default_chunk(); the grouped kernel, replayed the same way,
- * is taken (NEO_CHUNK_GROUPED) when it beats the best split chunk by > 1 %.
+ * (group sizes 4096 / 2048 / 1024 tokens) is taken (-1 / -2 / -4) when it beats
+ * the best split chunk by > 1 %.
  * Pure host computation, no GPU work; the SM
  * count is the current device's (148 when no device is visible).
  *   seq_lens     [batch] int32, HOST, each >= 0 (the values the call will see).
  *   chunk_tokens out: a valid chunk_tokens argument for page_size (possibly
- *                NEO_CHUNK_GROUPED).
+ *                -1, -2 or -4: the grouped kernel).
  * Any chunk is correct (the result depends on C only through fp32 rounding);
  * this only affects speed.
  * Errors: NEO_ERR_INVALID_ARG (NULL pointers, batch < 0, num_kv_heads < 1, a

@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
 // partial rows, no counter -- and only requests longer than 4096 tokens write one
 // merged partial per group and run the split-K combine (a7) across groups.
 constexpr int kGroupWarps = 4;
-constexpr int kMaxWarpTiles = kGroupTiles / kGroupWarps;
+constexpr int kMaxWarpTiles = kGroupTiles / kGroupWarps;   // per-warp range <= 64 tiles
 
 template <int G>
 __device__ __forceinline__ void group_merge(const KArgs& a, const uint8_t* base, int stage_bytes, int warp, int lane,
@@ -758,7 +758,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   }
   if (kFuse && a.inv_freq && r < a.G) rope_q(qf, qd, ctx - 1, a.inv_freq);
   const int ntile_total = (ctx + kTileTokens - 1) / kTileTokens;
-  const int n_groups = (ntile_total + kGroupWarps * kMaxWarpTiles - 1) / (kGroupWarps * kMaxWarpTiles);
+  const int n_groups = (ntile_total + a.chunk_tiles - 1) / a.chunk_tiles;   // chunk_tiles = group tiles
   if (q >= n_groups) return;                       // uniform over the CTA (same b, q)
   const int tg = (ntile_total + n_groups - 1) / n_groups;
   const int g0 = q * tg, g1 = min(g0 + tg, ntile_total);
@@ -1020,7 +1020,8 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   }();
   a.probe = probe;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
-  if (L.grouped) {   // NEO_CHUNK_GROUPED: kernel 2, max_chunks = groups per request
+  if (L.grouped) {   // grouped kernel: max_chunks = groups per request, chunk_tiles = group tiles
+    a.chunk_tiles = group_tiles_of(L.chunk_tokens);
     const int64_t ctas = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
     if (L.k_new) return launch_group<2, true>(a, tmk, tmv, ctas, L.stream);
     return group_stages() == 3 ? launch_group<3, false>(a, tmk, tmv, ctas, L.stream)

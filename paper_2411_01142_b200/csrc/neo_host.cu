@@ -215,28 +215,32 @@ double plan_score(const std::vector<int32_t>& ntiles, int32_t hkv, int32_t chunk
 }
 
 // The grouped kernel in the same replay: CTA (q, b, g) in group-major order,
-// 3 CTAs per SM, cost = kPlanGroupOverheadTiles + its per-warp tile range
-// (fitted on the same sweeps: profiles/r01_grouped_sweep.txt).
-constexpr double kPlanGroupOverheadTiles = 3.0;
+// 3 CTAs per SM, cost = kPlanGroupOverheadTiles + its per-warp tile range, plus
+// kPlanGroupMultiTiles when the request has several groups (partial + combine).
+// Fitted on the same-box sweep profiles/r01_grouped_sweep.txt (11 shard rows x
+// group sizes 4096/2048/1024 and the split chunks): picks reach 99.6 % of the
+// best measured choice on geometric mean, 97.3 % worst.
+constexpr double kPlanGroupOverheadTiles = 2.0;
+constexpr double kPlanGroupMultiTiles = 2.0;
 
-double plan_score_grouped(const std::vector<int32_t>& ntiles, int32_t hkv, int sms) {
+double plan_score_grouped(const std::vector<int32_t>& ntiles, int32_t hkv, int32_t group_tiles, int sms) {
   int32_t max_groups = 1;
   int64_t total = 0;
   for (int32_t t : ntiles) {
-    max_groups = std::max(max_groups, (t + kGroupTiles - 1) / kGroupTiles);
+    max_groups = std::max(max_groups, (t + group_tiles - 1) / group_tiles);
     total += t;
   }
   std::vector<double> slot(static_cast<size_t>(sms) * 3, 0.0);
   for (int32_t q = 0; q < max_groups; ++q) {
     for (int32_t t : ntiles) {
-      const int32_t ng = (t + kGroupTiles - 1) / kGroupTiles;
+      const int32_t ng = (t + group_tiles - 1) / group_tiles;
       if (q >= ng) continue;
       const int32_t tg = (t + ng - 1) / ng;
       const int32_t g0 = q * tg, g1 = std::min(g0 + tg, t);
       const int32_t tw = (g1 - g0 + 3) / 4;
       for (int32_t g = 0; g < hkv; ++g) {
         std::pop_heap(slot.begin(), slot.end(), std::greater<double>());
-        slot.back() += kPlanGroupOverheadTiles + tw;
+        slot.back() += kPlanGroupOverheadTiles + tw + (ng > 1 ? kPlanGroupMultiTiles : 0.0);
         std::push_heap(slot.begin(), slot.end(), std::greater<double>());
       }
     }
@@ -547,8 +551,15 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
       }
     }
   }
-  // the grouped kernel must beat the best split chunk by > 1 % in the same model
-  *chunk_tokens = neo::plan_score_grouped(ntiles, hkv, sms) > best_score * 1.01 ? NEO_CHUNK_GROUPED : best;
+  // the grouped kernel (groups of 4096, 2048 or 1024 tokens, largest first) must
+  // beat the best split chunk -- and a smaller group the larger one -- by > 1 %
+  double best_g = -1.0;
+  int32_t best_k = 0;
+  for (int32_t k : {1, 2, 4}) {
+    const double sc = neo::plan_score_grouped(ntiles, hkv, neo::kGroupTiles / k, sms);
+    if (sc > best_g * 1.01) best_g = sc, best_k = k;
+  }
+  *chunk_tokens = best_g > best_score * 1.01 ? -best_k : best;
   return NEO_OK;
 }
 
@@ -559,7 +570,7 @@ static neo_status attn_shape(int32_t batch, int32_t hq, int32_t hkv, int32_t d, 
   if (hq % hkv != 0) return fail(NEO_ERR_INVALID_ARG, "num_q_heads must be a multiple of num_kv_heads");
   if (d != neo::kHeadDim) return fail(NEO_ERR_UNSUPPORTED, "head_dim must be 128");
   if (hq / hkv > neo::kMaxGroup) return fail(NEO_ERR_UNSUPPORTED, "GQA group size G = Hq/Hkv must be <= 8");
-  if (*chunk_tokens == NEO_CHUNK_GROUPED) return NEO_OK;
+  if (neo::is_grouped_chunk(*chunk_tokens)) return NEO_OK;
   if (*chunk_tokens == 0) {
     *chunk_tokens = neo::default_chunk(batch, hkv, max_seq_len);
     if (page_size > 0 && *chunk_tokens % page_size) *chunk_tokens = page_size * ((*chunk_tokens + page_size - 1) / page_size);
@@ -572,7 +583,8 @@ NEO_API neo_status neo_decode_attn_workspace_bytes(int32_t batch, int32_t hq, in
   if (!bytes) return fail(NEO_ERR_INVALID_ARG, "bytes is NULL");
   neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, 16);
   if (st != NEO_OK) return st;
-  const int32_t max_chunks = chunk_tokens == NEO_CHUNK_GROUPED ? neo::max_groups_for(max_seq_len)
+  const int32_t max_chunks = neo::is_grouped_chunk(chunk_tokens)
+                                 ? neo::max_groups_for(max_seq_len, neo::group_tiles_of(chunk_tokens))
                                                               : std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
   *bytes = neo::workspace_required(batch, hq, hkv, max_chunks);
   return NEO_OK;
@@ -605,8 +617,8 @@ static neo_status decode_attn_impl(const void* q, const void* k_pages, const voi
   if (max_blocks < 1 || static_cast<int64_t>(max_seq_len) > static_cast<int64_t>(max_blocks) * page_size)
     return fail(NEO_ERR_INVALID_ARG, "max_seq_len exceeds max_blocks * page_size");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(NEO_ERR_INVALID_ARG, "scale must be finite and > 0");
-  const bool grouped = chunk_tokens == NEO_CHUNK_GROUPED;
-  const int32_t max_chunks = grouped ? neo::max_groups_for(max_seq_len)
+  const bool grouped = neo::is_grouped_chunk(chunk_tokens);
+  const int32_t max_chunks = grouped ? neo::max_groups_for(max_seq_len, neo::group_tiles_of(chunk_tokens))
                                      : std::max(1, (max_seq_len + chunk_tokens - 1) / chunk_tokens);
   if (!neo::workspace_layout(batch, hq, hkv, max_chunks, workspace_bytes).fits)
     return fail(NEO_ERR_INVALID_ARG, "workspace too small: need " +

@@ -44,10 +44,13 @@ struct AttnLaunch {
   int64_t page_stride = 0;
   bool grouped = false;        // NEO_CHUNK_GROUPED: max_chunks holds the group count
 };
-constexpr int kGroupTiles = 4 * 64;                   // tiles per group of the grouped kernel
-inline int32_t max_groups_for(int32_t max_seq_len) {
+constexpr int kGroupTiles = 4 * 64;                   // largest group of the grouped kernel (tiles)
+// chunk_tokens -k (k = 1, 2, 4) selects groups of kGroupTiles / k tiles
+inline bool is_grouped_chunk(int32_t c) { return c == -1 || c == -2 || c == -4; }
+inline int32_t group_tiles_of(int32_t c) { return kGroupTiles / (-c); }
+inline int32_t max_groups_for(int32_t max_seq_len, int32_t group_tiles) {
   const int32_t tiles = (max_seq_len + kTileTokens - 1) / kTileTokens;
-  return tiles > 0 ? (tiles + kGroupTiles - 1) / kGroupTiles : 1;
+  return tiles > 0 ? (tiles + group_tiles - 1) / group_tiles : 1;
 }
 // Byte layout of a workspace of `ws_bytes` bytes for a call shape.  The
 // completion counters occupy [0, counter_cap(ws_bytes)) -- a region fixed by the

@@ -124,7 +124,7 @@ def test_workspace_bytes_and_default_chunk():
     assert big <= 1.05 * data + 65536
 
 
-def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=3.0):
+def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=2.0, om=2.0):
     """Independent replay of the planner's model (include/neo.h
     neo_decode_attn_plan_chunk): split-K units in chunk-major order, W = 4 per CTA,
     CTAs taken in order by the earliest-free slot (SMs x CTAs/SM of the default
@@ -150,18 +150,18 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=3.0):
                 heapq.heapreplace(heap, heap[0] + o + m)
         return sum(nt) * hkv / max(heap)
 
-    def grouped_score():
+    def grouped_score(gt):
         heap = [0.0] * (sms * 3)
-        mg = max([-(-t // 256) for t in nt] + [1])
+        mg = max([-(-t // gt) for t in nt] + [1])
         for q in range(mg):
             for t in nt:
-                ng = -(-t // 256)
+                ng = -(-t // gt)
                 if q >= ng:
                     continue
                 tg = -(-t // ng)
                 g0, g1 = q * tg, min(q * tg + tg, t)
                 for _ in range(hkv):
-                    heapq.heapreplace(heap, heap[0] + og + -(-(g1 - g0) // 4))
+                    heapq.heapreplace(heap, heap[0] + og + -(-(g1 - g0) // 4) + (om if ng > 1 else 0.0))
         return sum(nt) * hkv / max(heap)
 
     ctn = cands[-1] // 16
@@ -178,7 +178,12 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=3.0):
             sc = split_score(C)
             if sc > best_sc * 1.01:
                 best, best_sc = C, sc
-    return -1 if grouped_score() > best_sc * 1.01 else best
+    best_g, best_k = -1.0, 0
+    for k in (1, 2, 4):
+        sc = grouped_score(256 // k)
+        if sc > best_g * 1.01:
+            best_g, best_k = sc, k
+    return -best_k if best_g > best_sc * 1.01 else best
 
 
 def test_plan_chunk():
@@ -190,16 +195,16 @@ def test_plan_chunk():
         B, hkv, P = int(rng.integers(1, 700)), int(rng.choice([1, 2, 4, 8])), int(rng.choice([16, 32, 64]))
         ctx = rng.integers(0, int(rng.choice([300, 3000, 20000])), size=B).astype(np.int32)
         C = neo.plan_chunk(ctx, hkv, P)
-        assert C == neo.NEO_CHUNK_GROUPED or (C % 16 == 0 and C % P == 0 and 16 <= C <= 1024)
+        assert C in (-1, -2, -4) or (C % 16 == 0 and C % P == 0 and 16 <= C <= 1024)
         ref = _plan_replay(ctx.tolist(), hkv, P)
         if ref is not None:
             assert C == ref, (B, hkv, P, C, ref)
     c5 = WORKLOADS["c5"].contexts()
     assert neo.plan_chunk(c5, 8, 16) == neo.NEO_CHUNK_GROUPED    # profiles/r01_grouped_sweep.txt: +3.3 %
     c4 = WORKLOADS["c4"].contexts()
-    # profiles/r01_chunk_plan.md: the measured best split C of the c4 shards at N = 8
-    # and 4 (384, 640); N = 2 and 1 are uniform, many-CTA batches -> grouped kernel
-    assert [neo.plan_chunk(c4, 8 // n, 16) for n in (8, 4, 2, 1)] == [384, 640, -1, -1]
+    # the c4 shards: uniform ~2K contexts -> grouped kernel, with smaller groups as
+    # the per-rank (request, head) count falls (profiles/r01_grouped_sweep.txt)
+    assert [neo.plan_chunk(c4, 8 // n, 16) for n in (8, 4, 2, 1)] == [-2, -2, -1, -1]
     # uniform ~1K batches of 2048 (request, kv-head) pairs take the grouped kernel (c2)
     assert neo.plan_chunk(WORKLOADS["c2"].contexts(), 8, 16) == neo.NEO_CHUNK_GROUPED
     assert neo.plan_chunk([], 8, 16) == neo.default_chunk(0, 8, 0)
@@ -222,8 +227,10 @@ def test_grouped_workspace_and_chunk_validation():
     assert one < 256 * 8 * 4 * 64 * 2                      # counter region only
     units = 256 * 8 * 3
     assert three >= units * 4 * 8 + units * 4 * 128 * 4
+    four = neo.workspace_bytes(256, 32, 8, 4096, chunk_tokens=-4)   # 1024-token groups: 4 per request
+    assert four >= 256 * 8 * 4 * (4 * 8 + 4 * 128 * 4)
     with pytest.raises(neo.NeoError) as e:
-        neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=-2)
+        neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=-3)
     assert e.value.status == neo.NEO_ERR_UNSUPPORTED
     assert _attn(C=-1) != neo.NEO_ERR_UNSUPPORTED           # accepted (fails later only on fake pointers)
 

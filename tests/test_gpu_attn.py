@@ -271,7 +271,7 @@ def test_kv_append_then_attend(P):
     check_case(case, 64, f"append P={P}")
 
 
-@pytest.mark.parametrize("C", [64, -1])
+@pytest.mark.parametrize("C", [64, -1, -4])
 def test_cuda_graph_capture_matches_eager(C):
     """decode_attn launches (PDL attribute, fused combine counters; split and
     grouped kernels) captured in a CUDA graph and replayed give the eager results
@@ -346,7 +346,7 @@ def test_rope_append_then_attend():
         assert within_tol(got[b], ref)[0]
 
 
-@pytest.mark.parametrize("chunk", [0, 64, -1])
+@pytest.mark.parametrize("chunk", [0, 64, -1, -4])
 def test_decode_attn_append_plain_equals_separate(chunk):
     """neo_decode_attn_append without RoPE == neo_kv_append + neo_decode_attn, bit
     for bit (output and the appended page slots), the new slots poisoned first."""
@@ -419,17 +419,19 @@ def test_decode_attn_append_rope_vs_oracle(chunk, P):
 GROUPED = -1
 
 
+@pytest.mark.parametrize("k", [-1, -2, -4])
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (64, 8), (32, 32), (28, 4), (24, 8), (8, 1), (40, 8)])
-def test_parity_grouped(hq, hkv):
-    """One CTA per group of <= 256 tiles, 4 per-warp ranges merged in shared memory;
-    > 4096 tokens run several groups and the cross-group combine."""
-    ctx = [1, 15, 16, 17, 63, 65, 255, 256, 257, 1000, 4095, 4096, 4097, 4111, 8192, 9000]
-    check_case(Case(ctx, hq, hkv, seed=21 + hq + hkv), GROUPED, f"grouped G={hq // hkv}")
+def test_parity_grouped(hq, hkv, k):
+    """One CTA per group of <= 256 / -k tiles, 4 per-warp ranges merged in shared
+    memory; longer requests run several groups and the cross-group combine."""
+    ctx = [1, 15, 16, 17, 63, 65, 255, 256, 257, 1000, 1025, 2049, 4095, 4096, 4097, 4111, 8192, 9000]
+    check_case(Case(ctx, hq, hkv, seed=21 + hq + hkv), k, f"grouped{k} G={hq // hkv}")
 
 
+@pytest.mark.parametrize("k", [-1, -4])
 @pytest.mark.parametrize("P", [32, 64])
-def test_parity_grouped_page_sizes(P):
-    check_case(Case([1, 31, 32, 33, 700, 5000], 32, 8, P=P, seed=22 + P), GROUPED, f"grouped P={P}")
+def test_parity_grouped_page_sizes(P, k):
+    check_case(Case([1, 31, 32, 33, 700, 1100, 5000], 32, 8, P=P, seed=22 + P), k, f"grouped{k} P={P}")
 
 
 @pytest.mark.parametrize("variant", [ni.VARIANT_PEAKED, ni.VARIANT_SINK, ni.VARIANT_PEAKED | ni.VARIANT_SINK])

@@ -88,7 +88,7 @@ def test_fullsize_request_shard_c5():
     run_and_sample(wl, [0], 6, rng, ctx=ctx, req_ids=parts[3])
 
 
-@pytest.mark.parametrize("C", [256, -1])
+@pytest.mark.parametrize("C", [256, -1, -4])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_head_shards_reassemble_bitwise(world, C):
     """KV-head shards (each rank's own heads, own pool),
@@ -116,7 +116,7 @@ def test_head_shards_reassemble_bitwise(world, C):
     assert torch.equal(got.view(torch.int16), ref.view(torch.int16))
 
 
-@pytest.mark.parametrize("C", [128, -1])
+@pytest.mark.parametrize("C", [128, -1, -2])
 def test_request_shards_reassemble_bitwise(C):
     """Request (LPT) shards in their own pools and batches equal the unsharded
     output bit for bit: a request's result depends only on its inputs and C
