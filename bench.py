@@ -695,11 +695,7 @@ def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
     kv = torch.tensor([float(gb.kv_bytes_per_call() * L * args.steps)], dtype=torch.float64, device="cuda")
-    per_rank = None
     if world > 1:
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(allt, t)
-        per_rank = [float(x.item()) / args.steps for x in allt]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(kv, op=dist.ReduceOp.SUM)
     h2d = q_host.numel() * 2 + bt_host.numel() * 4 + sl_host.numel() * 4
