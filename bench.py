@@ -330,7 +330,7 @@ def run_neo(args):
                 "seq_len_mean": round(float(gb.ctx.mean()), 1), "seq_len_min": int(gb.ctx.min()),
                 "seq_len_max": int(gb.ctx.max()),
                 "layers_per_step": L, "distinct_layer_pools": gb.layers,
-                "chunk_tokens": chunk, "chunk_mode": "grouped" if chunk == neo.NEO_CHUNK_GROUPED else "split",
+                "chunk_tokens": chunk, "chunk_mode": f"grouped (groups <= {4096 // -chunk} tokens)" if chunk < 0 else "split",
                 "chunk_plan": "explicit --chunk" if args.chunk else
                 "neo_decode_attn_plan_chunk (host lengths)", "parallelism": par,
                 "l2": (f"inputs {gb.layers * gb.kv_bytes_per_call() / 1e9:.1f} GB of distinct KV cycled per step "
@@ -340,7 +340,7 @@ def run_neo(args):
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                         "kernel": "decode_attn_group_kernel" if chunk == neo.NEO_CHUNK_GROUPED else
+                         "kernel": "decode_attn_group_kernel" if chunk < 0 else
                          "decode_attn_kernel", "avg_launch_us": round(avg_launch * 1e6, 2),
                          "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
             "per_rank_ms_per_step": None if per_rank is None else [round(x, 4) for x in per_rank],
