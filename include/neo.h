@@ -272,25 +272,27 @@ NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_head
 
 /* a0 plan ("partition ... aggregate the partial
  * outputs") with the request lengths on the HOST -- NEO's scheduler holds them
- * (P:283-290).  Chooses the split-K chunk length C for one neo_decode_attn /
- * neo_decode_attn_append call over these requests: the candidate (multiples of
- * 64 tokens and of page_size in [128, 512]) that a replay of the GPU's in-order
- * CTA dispatch of the chunk-major grid predicts fastest, so that the last wave
- * of work units is not left mostly empty (DESIGN §6 "chunk planner").  Grids
- * of >= 4 waves at C = 512 take 512; grids under one wave at C = 128 take
- * neo_decode_attn_default_chunk(); the grouped kernel, replayed the same way,
- * (group sizes 4096 / 2048 / 1024 tokens) is taken (-1 / -2 / -4) when it beats
- * the best split chunk by > 1 %.
- * Pure host computation, no GPU work; the SM
- * count is the current device's (148 when no device is visible).
+ * (P:283-290).  Chooses chunk_tokens for one neo_decode_attn /
+ * neo_decode_attn_append call over these requests (DESIGN §6 "chunk planner"):
+ *  - a replay of the GPU's in-order CTA dispatch scores the split kernel at
+ *    C in {1024, 640, 512, 448, 384, 320, 256} (multiples of page_size) and the
+ *    grouped kernel at groups of 4096 / 2048 / 1024 tokens (-1 / -2 / -4);
+ *    a smaller C, a smaller group, and the grouped kernel over the split one
+ *    must each win by > 1 %;
+ *  - grids of >= 16 waves at C = 1024 score only that split chunk;
+ *  - grids under one wave at the smallest C are latency-bound: the grouped
+ *    kernel (-1) when every request fits one 4096-token group, else
+ *    neo_decode_attn_default_chunk().
+ * Pure host computation, no GPU work; the SM count is the current device's
+ * (148 when no device is visible).
  *   seq_lens     [batch] int32, HOST, each >= 0 (the values the call will see).
  *   chunk_tokens out: a valid chunk_tokens argument for page_size (possibly
  *                -1, -2 or -4: the grouped kernel).
- * Any chunk is correct (the result depends on C only through fp32 rounding);
+ * Any choice is correct (the result depends on it only through fp32 rounding);
  * this only affects speed.
  * Errors: NEO_ERR_INVALID_ARG (NULL pointers, batch < 0, num_kv_heads < 1, a
  * negative length); NEO_ERR_UNSUPPORTED (page_size not a multiple of 16 in
- * [16, 512]). */
+ * [16, 1024]). */
 NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t batch, int32_t num_kv_heads,
                                               int32_t page_size, int32_t* chunk_tokens);
 

@@ -501,7 +501,7 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
   if (batch < 0 || hkv <= 0 || (batch > 0 && !seq_lens))
     return neo::fail(NEO_ERR_INVALID_ARG, "batch >= 0, num_kv_heads >= 1 and seq_lens (host) required");
   if (page_size <= 0 || page_size % neo::kTileTokens || page_size > neo::kMaxChunkTokens)
-    return neo::fail(NEO_ERR_UNSUPPORTED, "page_size must be a positive multiple of 16, <= 512");
+    return neo::fail(NEO_ERR_UNSUPPORTED, "page_size must be a positive multiple of 16, <= 1024");
   std::vector<int32_t> ntiles(static_cast<size_t>(batch));
   for (int32_t b = 0; b < batch; ++b) {
     if (seq_lens[b] < 0) return neo::fail(NEO_ERR_INVALID_ARG, "seq_lens[" + std::to_string(b) + "] < 0");
@@ -516,14 +516,19 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
   for (int32_t C : kCand)
     if (C % page_size == 0) cand.push_back(C);
   if (cand.empty()) cand.push_back(page_size);
-  // Under one wave at the smallest candidate the call is latency-bound: keep the
-  // shape-only default.
+  // Under one wave at the smallest candidate the call is latency-bound: requests
+  // that fit one 4096-token group take the grouped kernel (no partials, no
+  // combine round trips: c1 12.6 -> 10.2 us); otherwise the shape-only default.
   const int32_t ct_min = cand.back() / neo::kTileTokens;
   int64_t units_min = 0;
   for (int32_t t : ntiles) units_min += static_cast<int64_t>(hkv) * ((t + ct_min - 1) / ct_min);
   if (units_min < static_cast<int64_t>(sms) * 2 * 4) {
     int32_t max_len = 0;
     for (int32_t b = 0; b < batch; ++b) max_len = std::max(max_len, seq_lens[b]);
+    if (max_len > 0 && max_len <= neo::kGroupTiles * neo::kTileTokens) {
+      *chunk_tokens = NEO_CHUNK_GROUPED;
+      return NEO_OK;
+    }
     int32_t C = neo::default_chunk(batch, hkv, max_len);
     if (C % page_size) C = page_size * ((C + page_size - 1) / page_size);
     *chunk_tokens = std::min(C, neo::kMaxChunkTokens);

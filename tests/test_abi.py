@@ -166,7 +166,7 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=2.0, om=2.0):
 
     ctn = cands[-1] // 16
     if sum(hkv * -(-t // ctn) for t in nt) < sms * 8:
-        return None
+        return -1 if 0 < max(ctx) <= 4096 else None   # latency-bound: grouped, else library default
     ct0 = cands[0] // 16
     units = sum(hkv * -(-t // ct0) for t in nt)
     w, k = shape(max([-(-t // ct0) for t in nt] + [1]))
@@ -208,6 +208,7 @@ def test_plan_chunk():
     # uniform ~1K batches of 2048 (request, kv-head) pairs take the grouped kernel (c2)
     assert neo.plan_chunk(WORKLOADS["c2"].contexts(), 8, 16) == neo.NEO_CHUNK_GROUPED
     assert neo.plan_chunk([], 8, 16) == neo.default_chunk(0, 8, 0)
+    assert neo.plan_chunk(WORKLOADS["c1"].contexts(), 32, 16) == neo.NEO_CHUNK_GROUPED   # latency-bound c1
     with pytest.raises(neo.NeoError) as e:
         neo.plan_chunk([5, -1], 8, 16)
     assert e.value.status == neo.NEO_ERR_INVALID_ARG
