@@ -641,8 +641,9 @@ def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
     inputs (q of every layer, block table, seq_lens) host->device from pinned
     memory, runs the L attention calls and copies every layer's output back to
     pinned host memory.  Copies run on two copy streams, pipelined per layer with
-    the attention launches (q[l+1] uploads and out[l-1] downloads while layer l
-    computes); the step ends when its last output has reached the host."""
+    the attention launches, into two device buffer sets used by alternate steps
+    (the next step's uploads and this step's downloads overlap compute); the
+    timed region ends when the last step's outputs have reached the host."""
     import torch
 
     from paper_2411_01142_b200 import neo
@@ -652,38 +653,53 @@ def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
     bt_host = gb.block_table.cpu().pin_memory()
     sl_host = gb.seq_lens.cpu().pin_memory()
     out_host = torch.empty((L, gb.B, gb.hq, 128), dtype=torch.bfloat16).pin_memory()
-    q_dev = torch.empty_like(q_host, device="cuda")
-    bt_dev = torch.empty_like(bt_host, device="cuda")
-    sl_dev = torch.empty_like(sl_host, device="cuda")
-    out_dev = torch.empty_like(out_host, device="cuda")
+    # two device buffer sets, alternating by step: step s+1 uploads while step s
+    # computes, and step s's outputs download while step s+1 computes
+    q_dev = [torch.empty_like(q_host, device="cuda") for _ in range(2)]
+    bt_dev = [torch.empty_like(bt_host, device="cuda") for _ in range(2)]
+    sl_dev = [torch.empty_like(sl_host, device="cuda") for _ in range(2)]
+    out_dev = [torch.empty_like(out_host, device="cuda") for _ in range(2)]
     h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(L)]
-    ev_att = [torch.cuda.Event() for _ in range(L)]
-    ev_done = torch.cuda.Event()
+    ev_in = [[torch.cuda.Event() for _ in range(L)] for _ in range(2)]
+    ev_att = [[torch.cuda.Event() for _ in range(L)] for _ in range(2)]
+    ev_used = [torch.cuda.Event() for _ in range(2)]      # compute finished reading set i
+    ev_down = [torch.cuda.Event() for _ in range(2)]      # outputs of set i reached the host
+    for i in range(2):
+        ev_used[i].record(stream)
+        ev_down[i].record(stream)
+    counter = [0]
 
     def step():
-        h2d_s.wait_stream(stream)                  # previous step finished with the buffers
+        i = counter[0] % 2
+        counter[0] += 1
+        h2d_s.wait_event(ev_used[i])               # the step two back finished with set i
         with torch.cuda.stream(h2d_s):
-            bt_dev.copy_(bt_host, non_blocking=True)
-            sl_dev.copy_(sl_host, non_blocking=True)
+            bt_dev[i].copy_(bt_host, non_blocking=True)
+            sl_dev[i].copy_(sl_host, non_blocking=True)
             for l in range(L):
-                q_dev[l].copy_(q_host[l], non_blocking=True)
-                ev_in[l].record(h2d_s)
+                q_dev[i][l].copy_(q_host[l], non_blocking=True)
+                ev_in[i][l].record(h2d_s)
+        stream.wait_event(ev_down[i])              # its outputs were downloaded before overwriting
         for l in range(L):
-            stream.wait_event(ev_in[l])
+            stream.wait_event(ev_in[i][l])
             k, v = gb.layer(l)
-            neo.decode_attn(q_dev[l], k, v, bt_dev, sl_dev, gb.max_seq_len, out=out_dev[l], chunk_tokens=chunk,
-                            workspace=ws, stream=stream)
-            ev_att[l].record(stream)
+            neo.decode_attn(q_dev[i][l], k, v, bt_dev[i], sl_dev[i], gb.max_seq_len, out=out_dev[i][l],
+                            chunk_tokens=chunk, workspace=ws, stream=stream)
+            ev_att[i][l].record(stream)
+        ev_used[i].record(stream)
         with torch.cuda.stream(d2h_s):
             for l in range(L):
-                d2h_s.wait_event(ev_att[l])
-                out_host[l].copy_(out_dev[l], non_blocking=True)
-            ev_done.record(d2h_s)
-        stream.wait_event(ev_done)
+                d2h_s.wait_event(ev_att[i][l])
+                out_host[l].copy_(out_dev[i][l], non_blocking=True)
+            ev_down[i].record(d2h_s)
+
+    def drain():
+        for i in range(2):
+            stream.wait_event(ev_down[i])
 
     for _ in range(max(1, args.warmup)):
         step()
+    drain()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -691,6 +707,7 @@ def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
     e0.record(stream)
     for _ in range(args.steps):
         step()
+    drain()                                        # every step's outputs are on the host
     e1.record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
