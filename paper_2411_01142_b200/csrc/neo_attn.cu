@@ -671,9 +671,9 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
 // ------------------------------------------ kernel 2: one CTA per (b, g) group
 //
 // Grouped split-K: CTA (q, b, g) covers group q of request b's tiles for KV head
-// g -- the tiles split into n_groups = ceil(ntiles / 256) equal groups, and each
-// group into 4 equal per-warp ranges (<= 64 tiles, so one TMA ring and two
-// page-id registers per lane as in kernel 1).  The split depends only on the
+// g -- the tiles split into n_groups = ceil(ntiles / T) equal groups (T = 256,
+// 128 or 64), each group's tiles dealt round-robin to the 4 warps (<= 64 tiles
+// per warp, so one TMA ring and two page-id registers per lane as in kernel 1).  The split depends only on the
 // request's own length, so results stay a function of (its inputs) alone.
 // The 4 warps merge their (m, l, acc) through shared memory (their own, drained
 // stage rings); a single-group request writes its bf16 output right there -- no
@@ -751,6 +751,16 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   const int g = bg - b * a.hkv;
   uint4 qf[4];
   load_q(a, b, g, r, qd, qf);
+  // Warp w takes tiles g0 + w, g0 + w + 4, ... of its group (interleaved), so for
+  // the first group (g0 = 0, every single-group request) lane i's page ids --
+  // tiles w + 4i and w + 4(i + 32) -- are known before seq_lens arrives: issue
+  // them with it (entries past the context are clamped into the row, never used).
+  const int32_t* bt_row = a.block_table + static_cast<int64_t>(b) * a.max_blocks;
+  int my_pid = 0, my_pid2 = 0;
+  if (q == 0) {
+    my_pid = __ldg(bt_row + min((warp + 4 * lane) * kTileTokens / a.page_size, a.max_blocks - 1));
+    my_pid2 = __ldg(bt_row + min((warp + 4 * (lane + 32)) * kTileTokens / a.page_size, a.max_blocks - 1));
+  }
   const int ctx = __ldg(a.seq_lens + b);
   if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
     if (q == 0 && warp == 0) write_zero_row(a, b, g, lane);
@@ -762,22 +772,19 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   if (q >= n_groups) return;                       // uniform over the CTA (same b, q)
   const int tg = (ntile_total + n_groups - 1) / n_groups;
   const int g0 = q * tg, g1 = min(g0 + tg, ntile_total);
-  const int tw = (g1 - g0 + kGroupWarps - 1) / kGroupWarps;
-  const int t_begin = g0 + warp * tw;
-  const int nt = max(0, min(t_begin + tw, g1) - t_begin);
-
-  int my_pid = 0, my_pid2 = 0;
-  if (lane < nt) my_pid = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks +
-                                (t_begin + lane) * kTileTokens / a.page_size);
-  if (lane + 32 < nt) my_pid2 = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks +
-                                      (t_begin + 32 + lane) * kTileTokens / a.page_size);
+  const int first = g0 + warp;                              // tiles first, first + 4, ... < g1
+  const int nt = first < g1 ? (g1 - first + kGroupWarps - 1) / kGroupWarps : 0;
+  if (q > 0) {
+    if (lane < nt) my_pid = __ldg(bt_row + (first + kGroupWarps * lane) * kTileTokens / a.page_size);
+    if (lane + 32 < nt) my_pid2 = __ldg(bt_row + (first + kGroupWarps * (lane + 32)) * kTileTokens / a.page_size);
+  }
   const uint64_t policy = evict_first_policy();
   auto issue = [&](int j) {
     const int pid = j < 32 ? __shfl_sync(kFull, my_pid, j) : __shfl_sync(kFull, my_pid2, j - 32);
     if (lane == 0) {
       const int s = j % kStages;
-      issue_tile(&tmk, &tmv, sbase + s * kStageBytes, bar0 + 8 * s, ((t_begin + j) * kTileTokens) % a.page_size, g,
-                 pid, policy);
+      issue_tile(&tmk, &tmv, sbase + s * kStageBytes, bar0 + 8 * s,
+                 ((first + kGroupWarps * j) * kTileTokens) % a.page_size, g, pid, policy);
     }
   };
   const int npro = nt < kStages ? nt : kStages;
@@ -789,7 +796,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
     const int s = j % kStages;
     mbar_wait(bar0 + 8 * s, static_cast<uint32_t>((j / kStages) & 1));
     // fused append: the warp whose range ends the request holds the new token
-    if (kFuse && t_begin + nt == ntile_total && j == nt - 1)
+    if (kFuse && first + kGroupWarps * j == ntile_total - 1)
       patch_new_token(a, sbase + s * kStageBytes, b, g, ctx, lane);
     Frags f;
     load_frags(sbase + s * kStageBytes, r, qd, f);
@@ -798,7 +805,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(j + kStages);
     }
-    compute_tile(f, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
+    compute_tile(f, qf, ctx - (first + kGroupWarps * j) * kTileTokens, a.scale_log2, r, qd, acc);
   }
 
   // (a6/a7 in the CTA) this warp's (acc, m, l) into its drained stage ring
