@@ -4,7 +4,8 @@ profiles/cost_profile_b200_llama8b.json:
 
   lin   linear stage per layer (QKV, O, gate/up, down GEMMs: library cuBLAS via
         torch.matmul -- a cost-table measurement, not part of the hot path)
-  gdec  GPU decode attention per layer: our neo_decode_attn over batches of ~1K contexts
+  gdec  GPU decode attention per layer: our neo_decode_attn (at the planner's chunk)
+        over batches of ~1K contexts
   gpre  prefill attention per layer: our neo_prefill_attn (paged, causal, one
         whole prompt of t tokens), fitted to a t^2 + b t
   cdec  CPU decode attention per layer: our neo_cpu_decode_attn on the host cores
@@ -66,10 +67,11 @@ def gdec_table():
         wl = Workload("p", "LLaMa-3.1-8B", HQ, HKV, B, 1, 1, "uniform", (1024,), index=50)
         gb = GpuBatch(wl, layers=1)
         k, v = gb.layer(0)
-        ws = neo.make_workspace(gb.B, HQ, HKV, gb.max_seq_len)
+        C = neo.plan_chunk(gb.ctx, HKV, gb.P)           # the a0 planner's choice, as bench.py
+        ws = neo.make_workspace(gb.B, HQ, HKV, gb.max_seq_len, C)
         o = torch.empty(gb.B, HQ, D, dtype=torch.bfloat16, device="cuda")
         t = gpu_time(lambda: neo.decode_attn(gb.q[0], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=o,
-                                             workspace=ws))
+                                             workspace=ws, chunk_tokens=C))
         out.append((int(gb.ctx.astype(np.int64).sum() + gb.B), t))
         del gb
         torch.cuda.empty_cache()
