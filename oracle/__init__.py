@@ -17,8 +17,10 @@ CUDA library; the CUDA path never imports it.
   for a layer range, written as numpy indexing.
 
 Pinned against closed forms, brute force and invariants in
-``tests/test_oracle_pins.py``.  Every oracle function is pinned (DESIGN.md
-"Oracle pins").
+``tests/test_oracle_pins.py`` (the batch driver against fp64 torch SDPA and
+bitwise against the single-request call; the softmax weights against fp64
+torch.softmax and Decimal brute force).  Every exported function is pinned
+(DESIGN.md §3).
 """
 from __future__ import annotations
 

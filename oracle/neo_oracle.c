@@ -185,14 +185,17 @@ int oracle_decode_attention_batch(const uint16_t* q, const uint16_t* k, const ui
   pthread_t th[256];
   job_t jobs[256];
   int rc = 0;
-  /* interleave requests by index so ragged lengths spread over threads */
+  /* contiguous runs of ceil(batch / nthreads) requests per thread */
   int64_t per = (batch + nthreads - 1) / nthreads;
   int started = 0;
   for (int i = 0; i < nthreads; ++i) {
     int64_t b0 = i * per, b1 = b0 + per < batch ? b0 + per : batch;
     if (b0 >= b1) break;
     jobs[i] = (job_t){q, k, v, offsets, b0, b1, hq, hkv, d, scale, out, 0};
-    if (pthread_create(&th[i], NULL, run_job, &jobs[i]) != 0) return -3;
+    if (pthread_create(&th[i], NULL, run_job, &jobs[i]) != 0) {
+      rc = -3;
+      break;
+    }
     ++started;
   }
   for (int i = 0; i < started; ++i) {
@@ -237,7 +240,10 @@ int oracle_prefill_attention(const uint16_t* q, const uint16_t* k, const uint16_
   int rc = 0, started = 0;
   for (int i = 0; i < nthreads; ++i) {
     jobs[i] = (prefill_job_t){q, k, v, n, n_q, hq, hkv, d, i, nthreads, scale, out, 0};
-    if (pthread_create(&th[i], NULL, run_prefill, &jobs[i]) != 0) return -3;
+    if (pthread_create(&th[i], NULL, run_prefill, &jobs[i]) != 0) {
+      rc = -3;
+      break;
+    }
     ++started;
   }
   for (int i = 0; i < started; ++i) {

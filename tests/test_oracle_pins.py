@@ -337,3 +337,127 @@ def test_prefill_brute_force_decimal(trial):
         p = n - n_q + i + 1
         ref = _decimal_attention(widen(q[i]), widen(k[:p]), widen(v[:p]), scale, G)
         np.testing.assert_allclose(got[i], ref, rtol=1e-13, atol=1e-15)
+
+
+# ---- batch driver (oracle_decode_attention_batch): it produces every cpu_baseline
+# and --impl reference number, so it is pinned on its own: against fp64 torch SDPA
+# request by request (a library routine), and bit for bit against the single-request
+# definition over ragged offsets and any thread count (an offset or stride bug in the
+# packing shows up as a wrong request, a thread-split bug as a missing one).
+def _ragged_batch(rng, lens, hq, hkv, scale_q=2.0):
+    q = rand_bits(rng, (len(lens), hq, 128), scale_q)
+    ks = [rand_bits(rng, (n, hkv, 128)) for n in lens]
+    vs = [rand_bits(rng, (n, hkv, 128)) for n in lens]
+    return q, ks, vs
+
+
+@pytest.mark.parametrize("nthreads", [1, 3, 16])
+def test_batch_equals_single_request_bitwise(nthreads):
+    rng = np.random.default_rng(400 + nthreads)
+    lens = [1, 17, 300, 2, 129, 16, 1000, 5, 64, 33, 7]
+    q, ks, vs = _ragged_batch(rng, lens, 32, 8)
+    scale = 1 / math.sqrt(128)
+    got = oracle.decode_attention_batch(q, ks, vs, scale, nthreads=nthreads)
+    assert got.shape == (len(lens), 32, 128)
+    for b in range(len(lens)):
+        assert np.array_equal(got[b], oracle.decode_attention(q[b], ks[b], vs[b], scale)), b
+
+
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (64, 8), (8, 8)])
+def test_batch_against_torch_sdpa_fp64(hq, hkv):
+    rng = np.random.default_rng(hq + 7 * hkv)
+    lens = [3, 250, 1, 97, 512]
+    q, ks, vs = _ragged_batch(rng, lens, hq, hkv)
+    scale = 1 / math.sqrt(128)
+    got = oracle.decode_attention_batch(q, ks, vs, scale, nthreads=4)
+    G = hq // hkv
+    for b, n in enumerate(lens):
+        tq = torch.from_numpy(widen(q[b]))[:, None, :]
+        tk = torch.from_numpy(widen(ks[b])).permute(1, 0, 2).repeat_interleave(G, 0)
+        tv = torch.from_numpy(widen(vs[b])).permute(1, 0, 2).repeat_interleave(G, 0)
+        ref = torch.nn.functional.scaled_dot_product_attention(tq, tk, tv, scale=scale)[:, 0].numpy()
+        np.testing.assert_allclose(got[b], ref, rtol=1e-12, atol=1e-13)
+
+
+def test_batch_more_threads_than_requests():
+    rng = np.random.default_rng(410)
+    q, ks, vs = _ragged_batch(rng, [40, 9], 8, 2)
+    got = oracle.decode_attention_batch(q, ks, vs, 0.1, nthreads=64)
+    for b in range(2):
+        assert np.array_equal(got[b], oracle.decode_attention(q[b], ks[b], vs[b], 0.1))
+
+
+# ---- softmax weights (oracle_softmax_weights), beyond "sum to 1": a wrong scale,
+# a wrong GQA group or a token offset each change the weights themselves.
+@pytest.mark.parametrize("hq,hkv,n", [(32, 8, 300), (8, 1, 77), (16, 16, 5), (64, 8, 1)])
+def test_softmax_weights_against_torch_softmax_fp64(hq, hkv, n):
+    rng = np.random.default_rng(500 + n)
+    q = rand_bits(rng, (hq, 128), 3.0)
+    k = rand_bits(rng, (n, hkv, 128))
+    scale = float(np.float32(1 / math.sqrt(128)))
+    w = oracle.softmax_weights(q, k, scale)
+    G = hq // hkv
+    tq = torch.from_numpy(widen(q))                                                    # [Hq][D]
+    tk = torch.from_numpy(widen(k)).permute(1, 0, 2).repeat_interleave(G, 0)          # [Hq][n][D]
+    ref = torch.softmax(scale * torch.einsum("hd,htd->ht", tq, tk), dim=-1).numpy()
+    np.testing.assert_allclose(w, ref, rtol=1e-12, atol=1e-15)
+
+
+def test_softmax_weights_times_v_is_decode_attention():
+    rng = np.random.default_rng(510)
+    hq, hkv, n = 32, 8, 700
+    q = rand_bits(rng, (hq, 128), 4.0)
+    k = rand_bits(rng, (n, hkv, 128))
+    v = rand_bits(rng, (n, hkv, 128))
+    scale = 1 / math.sqrt(128)
+    w = oracle.softmax_weights(q, k, scale)
+    out = oracle.decode_attention(q, k, v, scale)
+    G = hq // hkv
+    vv = widen(v)
+    for h in range(hq):
+        np.testing.assert_allclose(w[h] @ vv[:, h // G], out[h], rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_softmax_weights_brute_force_decimal(trial):
+    getcontext().prec = 50
+    rng = np.random.default_rng(520 + trial)
+    n, d = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+    hkv, G = int(rng.integers(1, 3)), int(rng.choice([1, 2, 4]))
+    q = rand_bits(rng, (hkv * G, d), 2.0)
+    k = rand_bits(rng, (n, hkv, d), 2.0)
+    scale = float(np.float32(1 / math.sqrt(d)))
+    w = oracle.softmax_weights(q, k, scale)
+    qf, kf = widen(q), widen(k)
+    for h in range(hkv * G):
+        e = [(Decimal(scale) * sum(Decimal(float(qf[h, i])) * Decimal(float(kf[t, h // G, i]))
+                                   for i in range(d))).exp() for t in range(n)]
+        den = sum(e)
+        np.testing.assert_allclose(w[h], [float(x / den) for x in e], rtol=1e-13, atol=1e-16)
+
+
+# ---- flash-decoding task statistics (oracle_partial) written out with torch fp64 ops
+def test_partial_statistics_against_torch_fp64():
+    rng = np.random.default_rng(530)
+    hq, hkv, n = 16, 4, 900
+    q = rand_bits(rng, (hq, 128), 3.0)
+    k = rand_bits(rng, (n, hkv, 128))
+    v = rand_bits(rng, (n, hkv, 128))
+    scale = float(np.float32(1 / math.sqrt(128)))
+    G = hq // hkv
+    for h, t0, t1 in ((0, 0, n), (5, 100, 101), (11, 333, 777), (15, 899, 900)):
+        m, l, acc = oracle.partial(q, k, v, h, t0, t1, scale)
+        s = scale * (torch.from_numpy(widen(k[t0:t1, h // G])) @ torch.from_numpy(widen(q[h])))
+        e = torch.exp(s - s.max())
+        assert m == pytest.approx(float(s.max()), rel=1e-14, abs=1e-14)
+        assert l == pytest.approx(float(e.sum()), rel=1e-13)
+        np.testing.assert_allclose(acc, (e[:, None] * torch.from_numpy(widen(v[t0:t1, h // G]))).sum(0).numpy(),
+                                   rtol=1e-12, atol=1e-12)
+
+
+def test_merge_closed_form_two_parts():
+    """Two partials with m_1 = m_2 + ln 2 and equal l, acc: the first counts twice
+    as much, so out = (2 a_1 + a_2) / (2 l + l)."""
+    a1, a2 = np.arange(4.0), np.array([1.0, -1.0, 0.5, 3.0])
+    out = oracle.merge([0.5 + math.log(2.0), 0.5], [3.0, 3.0], np.stack([a1, a2]))
+    np.testing.assert_allclose(out, (2 * a1 + a2) / 9.0, rtol=1e-15, atol=1e-16)
