@@ -41,7 +41,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c2", help="c1..c5 (BASELINE.json configs), c2s = skewed c2")
+    p.add_argument("--config", default="c3", help="c1..c5 (BASELINE.json configs), c2s = skewed c2; default c3 "
+                   "(batch 128, 4K-8K contexts, the north star's regime, with the swap leg)")
     p.add_argument("--impl", default="neo", choices=["neo", "reference"])
     p.add_argument("--chunk", type=int, default=0, help="split-K chunk tokens (0 = library default)")
     p.add_argument("--fraction", type=float, default=1.0, help="c5: GPU-resident fraction f")
@@ -152,6 +153,87 @@ def layers_per_step(wl):
     return 1 if wl.name == "c1" else wl.num_layers
 
 
+# ------------------------------------------------------- multi-rank harness
+
+
+def aggregate_ranks(t_local_s, kv_local, tok_local, steps, world, head_sharded, dist=None, device="cpu"):
+    """Combine per-rank results: time = MAX over ranks, KV bytes =
+    SUM; attended tokens SUM for request sharding, but with KV-head sharding
+    every rank serves every (request, token, layer) for its own heads, so the
+    tokens are counted once (the rank-local count, equal on all ranks).
+    Returns (t_max_s, kv_total, tok_total, per_rank_ms_per_step or None)."""
+    import torch
+    t = torch.tensor([float(t_local_s)], dtype=torch.float64, device=device)
+    kv = torch.tensor([float(kv_local)], dtype=torch.float64, device=device)
+    tok = torch.tensor([float(tok_local)], dtype=torch.float64, device=device)
+    per_rank = None
+    if world > 1:
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = [float(x.item()) * 1e3 / steps for x in allt]
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(kv, op=dist.ReduceOp.SUM)
+        if not head_sharded:
+            dist.all_reduce(tok, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(kv.item()), float(tok.item()), per_rank
+
+
+def rank_imbalance(per_rank):
+    """Slowest rank over the mean rank (1.0 = balanced)."""
+    return round(max(per_rank) / (sum(per_rank) / len(per_rank)), 4)
+
+
+def reassemble_heads_into(full_l, gathered_l):
+    """a9: ``gathered_l`` [world][B][Hq/N][D] (all_gather_into_tensor of the
+    head shards, rank-major) -> ``full_l`` [B][Hq][D]: rank r's q heads are
+    [r·Hq/N, (r+1)·Hq/N) (shard.head_shard)."""
+    world, B, hl, D = gathered_l.shape
+    full_l.view(B, world, hl, D).copy_(gathered_l.permute(1, 0, 2, 3))
+    return full_l
+
+
+READBW_SO = os.path.join(ROOT, "tools", "libreadbw.so")
+
+
+def build_readbw():
+    """Compile the HBM read-ceiling probe (a measurement tool, not the product)."""
+    src = os.path.join(ROOT, "tools", "readbw.cu")
+    if not os.path.exists(READBW_SO) or os.path.getmtime(READBW_SO) < os.path.getmtime(src):
+        tmp = READBW_SO + f".tmp{os.getpid()}"
+        subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "--shared",
+                               "-Xcompiler", "-fPIC", "-o", tmp, src])
+        os.replace(tmp, READBW_SO)
+    return READBW_SO
+
+
+def measure_read_ceiling(gb, stream):
+    """This box's HBM read ceiling, measured in the run: a pure streaming read of
+    4 GiB of the KV pool (best of 5) -- the denominator a read-only kernel can
+    actually reach, reported beside the copy peak of MEASURED_PEAKS.json."""
+    import ctypes
+
+    import torch
+    try:
+        lib = ctypes.CDLL(build_readbw())
+    except Exception:
+        return None
+    lib.readbw.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                           ctypes.c_int, ctypes.c_void_p]
+    flat = gb.pool.view(-1)
+    nbytes = min(4 << 30, flat.numel() * flat.element_size()) // 16 * 16
+    sink = torch.zeros(4096, dtype=torch.int32, device="cuda")
+    best = 0.0
+    for rep in range(7):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lib.readbw(flat.data_ptr(), nbytes, sink.data_ptr(), 1184, 512, 8, stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if rep >= 2:
+            best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return round(best, 1) if best > 0 else None
+
+
 # --------------------------------------------------------------------- neo arm
 
 
@@ -182,11 +264,14 @@ def run_neo(args):
     out = torch.empty(L, gb.B, gb.hq, 128, dtype=torch.bfloat16, device="cuda")
     torch.cuda.synchronize()
 
+    def attn_layer(l):
+        k, v = gb.layer(l)
+        neo.decode_attn(gb.q[l % gb.layers], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=out[l],
+                        chunk_tokens=chunk, workspace=ws, stream=stream)
+
     def step(events=None):
         for l in range(L):
-            k, v = gb.layer(l)
-            neo.decode_attn(gb.q[l % gb.layers], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=out[l],
-                            chunk_tokens=chunk, workspace=ws, stream=stream)
+            attn_layer(l)
             if events is not None:
                 events[l].record(stream)
 
@@ -247,28 +332,20 @@ def run_neo(args):
         for l in range(L):
             launch_ms.append(prev.elapsed_time(per[l]))
             prev = per[l]
-    t = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
     kv_local = gb.kv_bytes_per_call() * L * args.steps
     tok_local = int(gb.ctx.astype(np.int64).sum()) * L * args.steps
-    tot = torch.tensor([kv_local, tok_local], dtype=torch.float64, device="cuda")
-    per_rank = None
-    if world > 1:
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(allt, t)
-        per_rank = [float(x.item()) / args.steps for x in allt]
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        if scaling == "strong" and wl.name == "c4":
-            # head sharding: each (request, token, layer) is attended once over all ranks
-            tok = torch.tensor([float(tok_local)], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tot[:1], op=dist.ReduceOp.SUM)
-            tot[1] = tok[0]
-        else:
-            dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-    t_max = float(t.item()) / 1e3
-    kv_total, tok_total = float(tot[0].item()), float(tot[1].item())
+    t_max, kv_total, tok_total, per_rank = aggregate_ranks(t_ms / 1e3, kv_local, tok_local, args.steps, world,
+                                                           head_sharded=(wl.name == "c4"), dist=dist,
+                                                           device="cuda")
     value = kv_total / t_max / 1e9
-    avg_launch = float(np.mean(launch_ms)) / 1e3
+    # The step is exactly L back-to-back launches of the decode kernel and nothing
+    # else on the stream (profiles/r02_launches_c3.md: 100 % of the timed
+    # kernels), so its average launch duration is the rank's step time / L --
+    # timed with programmatic dependent launch intact.  The event-per-launch pass
+    # above breaks that overlap; it is reported only as `isolated_launch_us`.
+    avg_launch = t_ms / 1e3 / (L * args.steps)
     hbm_peak, peak_src = peaks()
+    read_ceiling = measure_read_ceiling(gb, stream)
     algo = gb.kv_bytes_per_call() + gb.other_bytes_per_call()
     achieved = algo / avg_launch / 1e9
     traffic = None
@@ -293,7 +370,7 @@ def run_neo(args):
 
     swap = None
     if wl.swap_requests and not args.no_swap:
-        swap = run_swap(args, gb, L, step, stream)
+        swap = run_swap(args, gb, L, step, attn_layer, stream)
 
     prefill = None
     if rank == 0 and not args.no_prefill:
@@ -342,9 +419,16 @@ def run_neo(args):
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                          "kernel": "decode_attn_group_kernel" if chunk < 0 else
                          "decode_attn_kernel", "avg_launch_us": round(avg_launch * 1e6, 2),
-                         "algorithmic_bytes_per_launch": algo, "peak_source": peak_src},
+                         "avg_launch_source": "rank-0 timed step / launches per step (PDL intact)",
+                         "isolated_launch_us": round(float(np.mean(launch_ms)) * 1e3, 2),
+                         "algorithmic_bytes_per_launch": algo, "peak_source": peak_src,
+                         "read_ceiling_gbs": read_ceiling,
+                         "frac_of_read_ceiling": round(achieved / read_ceiling, 4) if read_ceiling else None,
+                         "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
+                         "read_ceiling_source": "measured in this run: 16-byte non-allocating loads over 4 GiB of "
+                                                "the KV pool, 1184 CTAs x 512 threads, best of 5 (tools/readbw.cu)"},
             "per_rank_ms_per_step": None if per_rank is None else [round(x, 4) for x in per_rank],
-            "rank_imbalance": None if per_rank is None else round(max(per_rank) / (sum(per_rank) / world), 4),
+            "rank_imbalance": None if per_rank is None else rank_imbalance(per_rank),
             "gpu_launches": L * args.steps,
             "clocks": clk,
             "e2e": e2e,
@@ -530,7 +614,7 @@ def run_reassembly(args, gb, L, step, stream, world, dist):
             comm.wait_event(evs[l])
             with torch.cuda.stream(comm):
                 dist.all_gather_into_tensor(gbuf[l].view(-1), outl[l].view(-1))
-                full[l].view(gb.B, world, gb.hq, 128).copy_(gbuf[l].permute(1, 0, 2, 3))
+                reassemble_heads_into(full[l], gbuf[l])
         stream.wait_stream(comm)
 
     for _ in range(2):
@@ -550,7 +634,7 @@ def run_reassembly(args, gb, L, step, stream, world, dist):
             "overlap": "all_gather of layer l on a comm stream while layer l+1 computes"}
 
 
-def run_swap(args, gb, L, step, stream):
+def run_swap(args, gb, L, step, attn_layer, stream):
     """c3's a8 row: swap the last `swap_requests` requests (LIFO victims)
     out to pinned host through neo_kv_swap_out on a side stream (gather kernel +
     cudaMemcpy2DAsync over PCIe), alone and concurrently with attention steps;
@@ -623,6 +707,35 @@ def run_swap(args, gb, L, step, stream):
     t_att = s0.elapsed_time(s1) / 1e3
     pool.swap_in(host_ids, gpu_ids, staging, stream=side)              # restore
     torch.cuda.synchronize()
+    # NEXT-1 layer-wise pipeline ("start PCIe transmission immediately
+    # after each layer's KV value is computed"): in one decode step, right after
+    # layer l's attention the victims' layer-l pages go out on the side stream
+    # (neo_kv_swap_out_ex + NEO_SWAP_DEFER_JOIN, so the library overlaps layer
+    # l+1's gather with layer l's D2H through the two staging halves); one
+    # neo_kv_swap_join ends the step's swap.
+    def layerwise():
+        ev = [torch.cuda.Event() for _ in range(L)]
+        e_st, e_att = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_sw0, e_sw1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_st.record(stream)
+        for l in range(L):
+            attn_layer(l)
+            ev[l].record(stream)
+            side.wait_event(ev[l])
+            if l == 0:
+                e_sw0.record(side)
+            pool.swap_out(gpu_ids, host_ids, staging, l % gb.layers, l % gb.layers + 1, stream=side,
+                          defer_join=True)
+        e_att.record(stream)
+        pool.swap_join(stream=side)
+        e_sw1.record(side)
+        torch.cuda.synchronize()
+        return e_st.elapsed_time(e_att) / 1e3, e_sw0.elapsed_time(e_sw1) / 1e3, e_st.elapsed_time(e_sw1) / 1e3
+
+    layerwise()                                                        # warm-up
+    lw = [layerwise() for _ in range(2)]
+    lw_att, lw_swap, lw_total = (float(np.mean([x[i] for x in lw])) for i in range(3))
+    lw_bytes = nbytes * L // gb.layers
     pool.close()
     return {"requests": int(wl.swap_requests), "pages": int(n), "layers": int(gb.layers), "bytes": int(nbytes),
             "swap_out_gbs": round(nbytes / t_out / 1e9, 2), "swap_in_gbs": round(nbytes / t_in / 1e9, 2),
@@ -633,7 +746,17 @@ def run_swap(args, gb, L, step, stream):
             "zero_copy_swap_in_gbs": round(nbytes / t_zc_in / 1e9, 2),
             "attention_gbs_during_swap": round(gb.kv_bytes_per_call() * L * steps / t_att / 1e9, 2),
             "attention_steps_during_swap": steps, "staging_bytes": int(staging.numel()),
-            "swap_outlasted_attention": bool(sa.elapsed_time(s1) < sa.elapsed_time(sb))}
+            "swap_outlasted_attention": bool(sa.elapsed_time(s1) < sa.elapsed_time(sb)),
+            "layerwise_pipeline": {
+                "what": "per decode step: attention(l) on the main stream, then swap-out of the 16 victims' "
+                        "layer-l pages on a side stream (neo_kv_swap_out_ex, NEO_SWAP_DEFER_JOIN; staging split "
+                        "in two halves by the library), one neo_kv_swap_join per step",
+                "bytes": int(lw_bytes), "calls_per_step": int(L),
+                "attention_gbs": round(gb.kv_bytes_per_call() * L / lw_att / 1e9, 2),
+                "swap_gbs": round(lw_bytes / lw_swap / 1e9, 2),
+                "swap_frac_of_memcpy": round((lw_bytes / lw_swap) / (nbytes / t_d2h), 4),
+                "step_ms_incl_swap": round(lw_total * 1e3, 3), "attention_ms": round(lw_att * 1e3, 3),
+                "swap_ms_from_first_layer": round(lw_swap * 1e3, 3)}}
 
 
 def run_e2e(args, gb, L, chunk, ws, stream, world, dist):

@@ -18,7 +18,9 @@
  *   - Every call returns neo_status.  NEO_OK = 0.  neo_last_error() returns a
  *     thread-local human-readable message for the last failing call.
  *   - All-or-nothing: a non-OK return has enqueued no GPU work and changed no
- *     pool state (mirrors S:262, S:292 atomicity).
+ *     pool state (mirrors S:262, S:292 atomicity).  Every argument is validated
+ *     before the first enqueue; the one exception is NEO_ERR_CUDA raised by an
+ *     enqueue itself (a failing CUDA context), see the swap section.
  *   - Ownership: the CALLER allocates and owns every device buffer (pool, q,
  *     out, workspace, staging) and the pinned host pool; the library never
  *     allocates or frees device memory.  Pointers must stay valid until the
@@ -329,6 +331,41 @@ NEO_API neo_status neo_kv_swap_out(neo_kv_pool* pool, int32_t n_pages, const int
 NEO_API neo_status neo_kv_swap_in(neo_kv_pool* pool, int32_t n_pages, const int32_t* host_page_ids,
                                   const int32_t* gpu_page_ids, int32_t layer_begin, int32_t layer_end,
                                   void* staging, size_t staging_bytes, void* stream);
+
+/* Pipelining ("start PCIe transmission immediately after
+ * each layer's KV value is computed").  When the staging holds at least two
+ * pages' layer ranges (2 * neo_kv_swap_staging_bytes(pool, 1, ...)) and `stream`
+ * is not being captured into a CUDA graph, a staged swap splits the staging
+ * into two halves: gather/scatter kernels run on `stream`, the PCIe copies on a
+ * copy stream the pool creates on first use (destroyed by
+ * neo_kv_pool_destroy), and events order each half's producer and consumer.
+ * The halves alternate across calls too, so a swap issued per layer overlaps
+ * layer l+1's gather with layer l's D2H.  Otherwise (one-page staging, or graph
+ * capture) the chunks run serially on `stream` with one buffer (after any
+ * copy of an earlier pipelined call still reading the staging; under capture,
+ * call neo_kv_swap_join and synchronise before capturing).  In both cases,
+ * when `stream` passes the point where neo_kv_swap_out/in returned, the swap is
+ * complete.
+ *
+ * neo_kv_swap_out_ex with flags = NEO_SWAP_DEFER_JOIN: on return `stream` is
+ * ordered after the GATHER only -- the GPU pages may be freed or overwritten
+ * once `stream` passes that point -- while the D2H copies may still be in
+ * flight.  The host pages are complete once `stream` (or any stream) passes a
+ * later neo_kv_swap_join(pool, stream), which makes `stream` wait for every
+ * copy the pool's swaps have enqueued so far.  flags = 0 is neo_kv_swap_out.
+ * Errors: NEO_ERR_INVALID_ARG for unknown flags or DEFER on a swap-in, or when
+ * staged swaps of one pool are issued from two devices.
+ *
+ * Atomicity: every argument (ids, ranges, staging size and memory type, pinned
+ * CPU-cache, a pending CUDA error) is validated before the first enqueue, so a
+ * validation failure enqueues nothing.  NEO_ERR_CUDA from an enqueue itself
+ * (after validation) means the CUDA context is failing; earlier chunks of that
+ * call may have been enqueued. */
+#define NEO_SWAP_DEFER_JOIN 1u
+NEO_API neo_status neo_kv_swap_out_ex(neo_kv_pool* pool, int32_t n_pages, const int32_t* gpu_page_ids,
+                                      const int32_t* host_page_ids, int32_t layer_begin, int32_t layer_end,
+                                      void* staging, size_t staging_bytes, uint32_t flags, void* stream);
+NEO_API neo_status neo_kv_swap_join(neo_kv_pool* pool, void* stream);
 
 /* ------------------------------------------------------ CPU attention (NEXT-2)
  * Decode attention of CPU-requests over the CPU-cache -- NEO's PACPU:

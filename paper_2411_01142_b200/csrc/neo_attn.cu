@@ -483,6 +483,9 @@ __device__ __forceinline__ void finish_unit(const KArgs& a, Acc& s, int b, int g
     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(a.ws_cnt + bg) : "memory");
   prev = __shfl_sync(kFull, prev, 0);
   if (prev != n_chunks - 1) return;
+  // shfl only moves the value; the warp barrier extends lane 0's acquire to the
+  // lanes whose __ldcg reads of the other chunks' partials follow
+  __syncwarp();
   if (a.probe & 4) {
     if (lane == 0) a.ws_cnt[bg] = 0;
     return;
@@ -914,15 +917,15 @@ static bool pdl_enabled() {
 template <int W, int S, bool kStreamOnly = false, bool kFuse = false>
 static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t units,
                               cudaStream_t stream) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   constexpr int smem = W * S * kStageBytes + 1024;
-  if (!configured) {
+  neo_status st = once_per_device(configured, [](int) {
     cudaError_t e =
         cudaFuncSetAttribute(decode_attn_kernel<W, S, kStreamOnly, kFuse>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_kernel)");
-    configured = true;
-  }
+    return e == cudaSuccess ? NEO_OK : cuda_fail(e, "cudaFuncSetAttribute(decode_attn_kernel)");
+  });
+  if (st != NEO_OK) return st;
   const int64_t grid = (units + W - 1) / W;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
@@ -953,14 +956,14 @@ static int group_stages() {
 template <int S, bool kFuse>
 static neo_status launch_group(const KArgs& a, const CUtensorMap& tmk, const CUtensorMap& tmv, int64_t ctas,
                                cudaStream_t stream) {
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   constexpr int smem = kGroupWarps * S * kStageBytes + 1024;
-  if (!configured) {
+  neo_status st = once_per_device(configured, [](int) {
     cudaError_t e =
         cudaFuncSetAttribute(decode_attn_group_kernel<S, kFuse>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(decode_attn_group_kernel)");
-    configured = true;
-  }
+    return e == cudaSuccess ? NEO_OK : cuda_fail(e, "cudaFuncSetAttribute(decode_attn_group_kernel)");
+  });
+  if (st != NEO_OK) return st;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(ctas));
   cfg.blockDim = dim3(kGroupWarps * 32);

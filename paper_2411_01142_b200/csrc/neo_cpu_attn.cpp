@@ -12,11 +12,17 @@
 // FMAs against the group's q, online softmax per page, contiguous page reads.
 #include <immintrin.h>
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -35,6 +41,98 @@ const uint8_t* pool_host_base(const neo_kv_pool* p);
 }  // namespace neo
 
 namespace {
+
+// Persistent host worker pool: neo_cpu_decode_attn runs once per layer per
+// iteration (T_ca), so creating and joining threads per call would
+// add ~0.1 ms of fixed cost to every CPU sub-batch.  Workers are created on
+// first use (grown on demand), spin briefly and then sleep on a condition
+// variable between parallel regions; run() hands out task indices through one
+// atomic counter (the caller takes tasks too) and returns when all completed.
+// One parallel region at a time (region_mu_).  A forked child does not inherit
+// the threads, so the pool restarts when the pid changes.
+class WorkerPool {
+ public:
+  static WorkerPool& get() {
+    static WorkerPool* p = new WorkerPool();  // never destroyed: workers may still sleep at exit
+    return *p;
+  }
+
+  void run(int n, const std::function<void(int)>& fn) {
+    if (n <= 1) {
+      if (n == 1) fn(0);
+      return;
+    }
+    std::lock_guard<std::mutex> region(region_mu_);
+    if (pid_ != getpid()) {  // forked: the workers belong to the parent
+      for (auto& t : workers_) t.detach();
+      workers_.clear();
+      pid_ = getpid();
+    }
+    while (static_cast<int>(workers_.size()) < n - 1) workers_.emplace_back([this] { loop(); });
+    fn_.store(&fn, std::memory_order_relaxed);
+    n_.store(n, std::memory_order_relaxed);
+    pending_.store(n, std::memory_order_relaxed);
+    const uint64_t g = (state_.load(std::memory_order_relaxed) >> 32) + 1;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      state_.store(g << 32, std::memory_order_release);   // generation g, next task 0
+    }
+    cv_.notify_all();
+    work(g);
+    for (int spins = 0; pending_.load(std::memory_order_acquire) != 0; ++spins) {
+      if (spins < 4096) _mm_pause();
+      else std::this_thread::yield();
+    }
+  }
+
+ private:
+  WorkerPool() : pid_(getpid()) {}
+
+  // Claims tasks of generation g only: the (generation, next index) pair is one
+  // atomic word, so a worker still finishing an older region can never take a
+  // task of a newer one (whose fn_ / n_ it might not see yet).
+  void work(uint64_t g) {
+    for (;;) {
+      uint64_t st = state_.load(std::memory_order_acquire);
+      int t = -1;
+      while ((st >> 32) == g) {
+        const int idx = static_cast<int>(st & 0xffffffffu);
+        if (idx >= n_.load(std::memory_order_relaxed)) return;
+        if (state_.compare_exchange_weak(st, st + 1, std::memory_order_acq_rel, std::memory_order_acquire)) {
+          t = idx;
+          break;
+        }
+      }
+      if (t < 0) return;
+      (*fn_.load(std::memory_order_relaxed))(t);
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+
+  void loop() {
+    uint64_t seen = state_.load(std::memory_order_acquire) >> 32;
+    for (;;) {
+      uint64_t g = seen;
+      for (int spins = 0; spins < 20000 && (g = state_.load(std::memory_order_acquire) >> 32) == seen; ++spins)
+        _mm_pause();
+      if (g == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return (state_.load(std::memory_order_acquire) >> 32) != seen; });
+        g = state_.load(std::memory_order_acquire) >> 32;
+      }
+      seen = g;
+      work(g);
+    }
+  }
+
+  std::mutex region_mu_, mu_;
+  std::condition_variable cv_;
+  std::vector<std::thread> workers_;
+  std::atomic<const std::function<void(int)>*> fn_{nullptr};
+  std::atomic<int> n_{0}, pending_{0};
+  std::atomic<uint64_t> state_{0};   // generation << 32 | next task index
+  pid_t pid_;
+};
 
 constexpr int kD = 128;
 constexpr int kMaxG = 16;
@@ -436,10 +534,7 @@ extern "C" NEO_API neo_status neo_cpu_decode_attn(const neo_kv_pool* pool, int32
       else task_generic(jb, sg.b, sg.g, sg.j0, sg.j1, parts[t][i]);
     }
   };
-  std::vector<std::thread> pool_threads;
-  for (int t = 1; t < nth; ++t) pool_threads.emplace_back(worker, t);
-  worker(0);
-  for (auto& th : pool_threads) th.join();
+  WorkerPool::get().run(nth, worker);
 
   // merge the partials of each (b, g) in block order (threads are in block order)
   uint16_t* o = static_cast<uint16_t*>(out);

@@ -294,9 +294,10 @@ neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, c
 }
 
 // q_offsets [batch + 1]: 0 = q_offsets[0] <= ... <= q_offsets[batch] = total, and
-// each request's new tokens fit its context (q_len_b <= seq_lens[b]).
+// each request's new tokens fit its context (q_len_b <= seq_lens[b]) and the
+// call's max_q_len (the prefill schedule is sized by it).
 neo_status debug_validate_offsets(const int32_t* q_offsets, const int32_t* seq_lens, int32_t batch, int32_t total,
-                                  cudaStream_t stream) {
+                                  int32_t max_q_len, cudaStream_t stream) {
   std::vector<int32_t> off(batch + 1), sl(batch);
   cudaError_t e = cudaMemcpyAsync(off.data(), q_offsets, sizeof(int32_t) * (batch + 1), cudaMemcpyDeviceToHost, stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(sl.data(), seq_lens, sizeof(int32_t) * batch, cudaMemcpyDeviceToHost, stream);
@@ -306,6 +307,11 @@ neo_status debug_validate_offsets(const int32_t* q_offsets, const int32_t* seq_l
   for (int32_t b = 0; b < batch; ++b)
     if (off[b + 1] < off[b] || off[b + 1] - off[b] > sl[b])
       return fail(NEO_ERR_INVALID_ARG, "request " + std::to_string(b) + ": q length negative or above seq_lens");
+  for (int32_t b = 0; b < batch; ++b)
+    if (off[b + 1] - off[b] > max_q_len)
+      return fail(NEO_ERR_INVALID_ARG, "request " + std::to_string(b) + ": q length " +
+                                           std::to_string(off[b + 1] - off[b]) + " above max_q_len " +
+                                           std::to_string(max_q_len));
   return NEO_OK;
 }
 
@@ -324,6 +330,36 @@ struct neo_kv_pool {
   std::vector<uint8_t> host_used;
   int64_t host_free;
   std::mutex mu;
+  // Swap pipeline (created on first staged swap; see swap_common): the staging
+  // buffer is used as two halves; gather/scatter kernels run on the caller's
+  // stream, PCIe copies on `copy_stream`, and per half `ready` (contents landed)
+  // and `free_` (last reader done) events order them.  `next_half` alternates
+  // across calls, so call l+1's gather overlaps call l's D2H (P:240 layer-wise
+  // swapping issues one call per layer).
+  int device = -1;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr};
+  cudaEvent_t ev_free[2] = {nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_join = nullptr;
+  bool half_used[2] = {false, false};
+  int next_half = 0;
+  ~neo_kv_pool() {
+    if (copy_stream) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (device >= 0 && cur != device) cudaSetDevice(device);
+      cudaStreamSynchronize(copy_stream);
+      for (int h = 0; h < 2; ++h) {
+        if (ev_ready[h]) cudaEventDestroy(ev_ready[h]);
+        if (ev_free[h]) cudaEventDestroy(ev_free[h]);
+      }
+      if (ev_start) cudaEventDestroy(ev_start);
+      if (ev_join) cudaEventDestroy(ev_join);
+      cudaStreamDestroy(copy_stream);
+      if (device >= 0 && cur >= 0 && cur != device) cudaSetDevice(cur);
+    }
+  }
 };
 
 using neo::fail;
@@ -706,7 +742,7 @@ NEO_API neo_status neo_prefill_attn(const void* q, const void* k_pages, const vo
     st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_blocks * page_size,
                                   num_pages, s);
     if (st != NEO_OK) return st;
-    st = neo::debug_validate_offsets(q_offsets, seq_lens, batch, total_tokens, s);
+    st = neo::debug_validate_offsets(q_offsets, seq_lens, batch, total_tokens, max_q_len, s);
     if (st != NEO_OK) return st;
   }
   CUtensorMap tmq, tmk, tmv;
@@ -812,7 +848,7 @@ NEO_API neo_status neo_prefill_append(void* q_inout, int32_t hq, const float* in
     st = neo::debug_validate_attn(block_table, max_blocks, seq_lens, batch, page_size, max_blocks * page_size,
                                   num_pages, s);
     if (st != NEO_OK) return st;
-    st = neo::debug_validate_offsets(q_offsets, seq_lens, batch, total_tokens, s);
+    st = neo::debug_validate_offsets(q_offsets, seq_lens, batch, total_tokens, INT32_MAX, s);
     if (st != NEO_OK) return st;
   }
   return neo::launch_rope_append(static_cast<uint16_t*>(q_inout), hq, inv_freq, static_cast<uint16_t*>(k_pages),
@@ -832,10 +868,63 @@ NEO_API neo_status neo_kv_swap_staging_bytes(const neo_kv_pool* pool, int32_t n,
   return NEO_OK;
 }
 
+// Creates the pool's copy stream and events on the current device (once).
+static neo_status ensure_swap_pipeline(neo_kv_pool* pool) {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return neo::cuda_fail(e, "cudaGetDevice");
+  if (pool->copy_stream) {
+    if (dev != pool->device)
+      return fail(NEO_ERR_INVALID_ARG, "staged swaps of one pool must run on one device (pool's copy stream is on "
+                                       "device " + std::to_string(pool->device) + ")");
+    return NEO_OK;
+  }
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev[6] = {};
+  e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    for (int i = 0; i < 6; ++i)
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    if (cs) cudaStreamDestroy(cs);
+    return neo::cuda_fail(e, "creating the swap copy stream / events");
+  }
+  pool->device = dev;
+  pool->copy_stream = cs;
+  pool->ev_ready[0] = ev[0];
+  pool->ev_ready[1] = ev[1];
+  pool->ev_free[0] = ev[2];
+  pool->ev_free[1] = ev[3];
+  pool->ev_start = ev[4];
+  pool->ev_join = ev[5];
+  return NEO_OK;
+}
+
+// One PCIe copy between staging rows [i, j) of a chunk starting at page c0 and
+// the host pages host_ids[c0 + i ..] (consecutive ids: one 2D copy per run).
+static cudaError_t copy_runs(neo_kv_pool* pool, bool to_host, const int32_t* host_ids, int32_t c0, int32_t cn,
+                             uint8_t* stg, size_t per_page, size_t host_page, size_t host_off, cudaStream_t s) {
+  for (int32_t i = 0; i < cn;) {
+    int32_t j = i + 1;
+    while (j < cn && host_ids[c0 + j] == host_ids[c0 + j - 1] + 1) ++j;
+    uint8_t* host = pool->host_base + static_cast<size_t>(host_ids[c0 + i]) * host_page + host_off;
+    uint8_t* dev = stg + static_cast<size_t>(i) * per_page;
+    cudaError_t e = to_host ? cudaMemcpy2DAsync(host, host_page, dev, per_page, per_page, j - i,
+                                                cudaMemcpyDeviceToHost, s)
+                            : cudaMemcpy2DAsync(dev, per_page, host, host_page, per_page, j - i,
+                                                cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    i = j;
+  }
+  return cudaSuccess;
+}
+
 static neo_status swap_common(neo_kv_pool* pool, bool out_dir, int32_t n, const int32_t* gpu_ids,
                               const int32_t* host_ids, int32_t l0, int32_t l1, void* staging, size_t staging_bytes,
-                              void* stream) {
+                              uint32_t flags, void* stream) {
   if (!pool) return fail(NEO_ERR_INVALID_ARG, "pool is NULL");
+  if (flags & ~static_cast<uint32_t>(NEO_SWAP_DEFER_JOIN)) return fail(NEO_ERR_INVALID_ARG, "unknown swap flags");
+  if ((flags & NEO_SWAP_DEFER_JOIN) && !out_dir) return fail(NEO_ERR_INVALID_ARG, "NEO_SWAP_DEFER_JOIN is swap-out only");
   if (n < 0) return fail(NEO_ERR_INVALID_ARG, "n_pages < 0");
   if (l0 < 0 || l1 > pool->geo.num_layers || l0 >= l1) return fail(NEO_ERR_INVALID_ARG, "layer range out of bounds");
   if (n == 0) return NEO_OK;
@@ -844,6 +933,25 @@ static neo_status swap_common(neo_kv_pool* pool, bool out_dir, int32_t n, const 
   const size_t per_page = static_cast<size_t>(l1 - l0) * 2 * pool->layer_bytes;
   if (staging && staging_bytes < per_page)
     return fail(NEO_ERR_INVALID_ARG, "staging smaller than one page's layer range");
+  // ---- validation: everything that can be checked is checked before the
+  // first enqueue, so a non-OK return leaves the streams untouched.
+  std::lock_guard<std::mutex> lk(pool->mu);
+  {
+    neo_status st = check_ids(pool->gpu_used, n, gpu_ids, "GPU page");
+    if (st != NEO_OK) return st;
+    st = check_ids(pool->host_used, n, host_ids, "host page");
+    if (st != NEO_OK) return st;
+  }
+  {
+    cudaError_t e = cudaPeekAtLastError();
+    if (e != cudaSuccess) return neo::cuda_fail(e, "a previous CUDA error is pending; nothing enqueued");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap_st) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(NEO_ERR_INVALID_ARG, "invalid stream");
+  }
   uint16_t* host_dev = nullptr;
   if (!staging) {  // zero-copy: the CPU-cache must be device-mapped (UVA pinned memory)
     void* dp = nullptr;
@@ -853,15 +961,19 @@ static neo_status swap_common(neo_kv_pool* pool, bool out_dir, int32_t n, const 
       return fail(NEO_ERR_UNSUPPORTED, "zero-copy swap needs device-mapped pinned host memory");
     }
     host_dev = static_cast<uint16_t*>(dp);
+  } else if (cap_st == cudaStreamCaptureStatusNone) {  // (pointer queries are skipped under graph capture)
+    cudaPointerAttributes at{};
+    cudaError_t e = cudaPointerGetAttributes(&at, staging);
+    if (e != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      return fail(NEO_ERR_INVALID_ARG, "staging must be device memory");
+    }
+    e = cudaPointerGetAttributes(&at, pool->host_base);
+    if (e != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return fail(NEO_ERR_INVALID_ARG, "the CPU-cache must be pinned (page-locked) host memory");
+    }
   }
-  {
-    std::lock_guard<std::mutex> lk(pool->mu);
-    neo_status st = check_ids(pool->gpu_used, n, gpu_ids, "GPU page");
-    if (st != NEO_OK) return st;
-    st = check_ids(pool->host_used, n, host_ids, "host page");
-    if (st != NEO_OK) return st;
-  }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!staging) {
     for (int32_t c0 = 0; c0 < n; c0 += neo::kMaxZeroCopyPairs) {
       const int32_t cn = std::min<int32_t>(neo::kMaxZeroCopyPairs, n - c0);
@@ -878,53 +990,119 @@ static neo_status swap_common(neo_kv_pool* pool, bool out_dir, int32_t n, const 
   }
   const size_t host_page = static_cast<size_t>(pool->geo.num_layers) * 2 * pool->layer_bytes;
   const size_t host_off = static_cast<size_t>(l0) * 2 * pool->layer_bytes;
-  const int64_t cap = std::min<int64_t>(staging_bytes / per_page, neo::kMaxSwapIdsPerLaunch);
   uint8_t* stg = static_cast<uint8_t*>(staging);
-  const uint16_t* gpu16 = reinterpret_cast<const uint16_t*>(pool->gpu_base);
+  uint16_t* gpu16 = reinterpret_cast<uint16_t*>(pool->gpu_base);
+  // Pipelined when two halves of the staging hold a page each and the stream is
+  // not being captured into a graph (a capture cannot wait on the pipeline's
+  // events from earlier, uncaptured calls); otherwise one buffer, serially on
+  // the caller's stream.
+  const size_t half_pages = staging_bytes / 2 / per_page;
+  const bool pipelined = half_pages >= 1 && cap_st == cudaStreamCaptureStatusNone;
+  if (pipelined) {
+    neo_status st = ensure_swap_pipeline(pool);
+    if (st != NEO_OK) return st;
+  }
+  const int64_t cap = std::min<int64_t>(pipelined ? half_pages : staging_bytes / per_page, neo::kMaxSwapIdsPerLaunch);
+  const size_t half_bytes = pipelined ? half_pages * per_page : 0;
+  cudaStream_t cs = pool->copy_stream;
+  cudaError_t e = cudaSuccess;
+  if (pipelined) {  // the copy stream starts after the work the caller enqueued before this call
+    e = cudaEventRecord(pool->ev_start, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, pool->ev_start, 0);
+    if (e != cudaSuccess) return neo::cuda_fail(e, "swap pipeline start");
+  } else if (cs && cap_st == cudaStreamCaptureStatusNone) {
+    // one-buffer path after pipelined calls: a deferred D2H may still read the staging
+    for (int h = 0; h < 2 && e == cudaSuccess; ++h)
+      if (pool->half_used[h]) e = cudaStreamWaitEvent(s, pool->ev_free[h], 0);
+    if (e != cudaSuccess) return neo::cuda_fail(e, "swap pipeline wait");
+  }
+  int last_half = -1;
   for (int32_t c0 = 0; c0 < n; c0 += static_cast<int32_t>(cap)) {
     const int32_t cn = static_cast<int32_t>(std::min<int64_t>(cap, n - c0));
     neo::SwapBatch ids;
     for (int32_t i = 0; i < cn; ++i) ids.ids[i] = gpu_ids[c0 + i];
-    if (!out_dir) {  // host -> staging, per run of consecutive host ids
-      for (int32_t i = 0; i < cn;) {
-        int32_t j = i + 1;
-        while (j < cn && host_ids[c0 + j] == host_ids[c0 + j - 1] + 1) ++j;
-        cudaError_t e = cudaMemcpy2DAsync(stg + static_cast<size_t>(i) * per_page, per_page,
-                                          pool->host_base + static_cast<size_t>(host_ids[c0 + i]) * host_page + host_off,
-                                          host_page, per_page, j - i, cudaMemcpyHostToDevice, s);
+    if (!pipelined) {
+      if (!out_dir) {
+        e = copy_runs(pool, false, host_ids, c0, cn, stg, per_page, host_page, host_off, s);
         if (e != cudaSuccess) return neo::cuda_fail(e, "cudaMemcpy2DAsync(H2D swap-in)");
-        i = j;
+        neo_status st = neo::launch_scatter(gpu16, reinterpret_cast<const uint16_t*>(stg), ids, cn,
+                                            pool->geo.num_gpu_pages, pool->page_elems, l0, l1, s);
+        if (st != NEO_OK) return st;
+      } else {
+        neo_status st = neo::launch_gather(gpu16, reinterpret_cast<uint16_t*>(stg), ids, cn, pool->geo.num_gpu_pages,
+                                           pool->page_elems, l0, l1, s);
+        if (st != NEO_OK) return st;
+        e = copy_runs(pool, true, host_ids, c0, cn, stg, per_page, host_page, host_off, s);
+        if (e != cudaSuccess) return neo::cuda_fail(e, "cudaMemcpy2DAsync(D2H swap-out)");
       }
-      neo_status st = neo::launch_scatter(reinterpret_cast<uint16_t*>(pool->gpu_base),
-                                          reinterpret_cast<const uint16_t*>(stg), ids, cn, pool->geo.num_gpu_pages,
-                                          pool->page_elems, l0, l1, s);
-      if (st != NEO_OK) return st;
-    } else {
-      neo_status st = neo::launch_gather(gpu16, reinterpret_cast<uint16_t*>(stg), ids, cn, pool->geo.num_gpu_pages,
+      continue;
+    }
+    const int h = pool->next_half;
+    pool->next_half ^= 1;
+    last_half = h;
+    uint8_t* buf = stg + h * half_bytes;
+    if (out_dir) {
+      // gather into half h (after its previous reader finished) on the caller's
+      // stream, then D2H on the copy stream
+      if (pool->half_used[h]) e = cudaStreamWaitEvent(s, pool->ev_free[h], 0);
+      if (e != cudaSuccess) return neo::cuda_fail(e, "swap pipeline wait");
+      neo_status st = neo::launch_gather(gpu16, reinterpret_cast<uint16_t*>(buf), ids, cn, pool->geo.num_gpu_pages,
                                          pool->page_elems, l0, l1, s);
       if (st != NEO_OK) return st;
-      for (int32_t i = 0; i < cn;) {
-        int32_t j = i + 1;
-        while (j < cn && host_ids[c0 + j] == host_ids[c0 + j - 1] + 1) ++j;
-        cudaError_t e = cudaMemcpy2DAsync(pool->host_base + static_cast<size_t>(host_ids[c0 + i]) * host_page + host_off,
-                                          host_page, stg + static_cast<size_t>(i) * per_page, per_page, per_page, j - i,
-                                          cudaMemcpyDeviceToHost, s);
-        if (e != cudaSuccess) return neo::cuda_fail(e, "cudaMemcpy2DAsync(D2H swap-out)");
-        i = j;
-      }
+      e = cudaEventRecord(pool->ev_ready[h], s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, pool->ev_ready[h], 0);
+      if (e == cudaSuccess) e = copy_runs(pool, true, host_ids, c0, cn, buf, per_page, host_page, host_off, cs);
+      if (e == cudaSuccess) e = cudaEventRecord(pool->ev_free[h], cs);
+      if (e != cudaSuccess) return neo::cuda_fail(e, "swap-out D2H");
+    } else {
+      // H2D into half h on the copy stream, then scatter on the caller's stream
+      if (pool->half_used[h]) e = cudaStreamWaitEvent(cs, pool->ev_free[h], 0);
+      if (e == cudaSuccess) e = copy_runs(pool, false, host_ids, c0, cn, buf, per_page, host_page, host_off, cs);
+      if (e == cudaSuccess) e = cudaEventRecord(pool->ev_ready[h], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, pool->ev_ready[h], 0);
+      if (e != cudaSuccess) return neo::cuda_fail(e, "swap-in H2D");
+      neo_status st = neo::launch_scatter(gpu16, reinterpret_cast<const uint16_t*>(buf), ids, cn,
+                                          pool->geo.num_gpu_pages, pool->page_elems, l0, l1, s);
+      if (st != NEO_OK) return st;
+      e = cudaEventRecord(pool->ev_free[h], s);
+      if (e != cudaSuccess) return neo::cuda_fail(e, "swap pipeline record");
     }
+    pool->half_used[h] = true;
+  }
+  // The caller's stream completes only after the last copy: swap-out's final
+  // D2H ran on the copy stream (in order, so it covers every earlier one).
+  // NEO_SWAP_DEFER_JOIN leaves that to neo_kv_swap_join, so the next layer's
+  // gather on the same stream is not held behind this layer's D2H.
+  if (pipelined && out_dir && last_half >= 0 && !(flags & NEO_SWAP_DEFER_JOIN)) {
+    e = cudaStreamWaitEvent(s, pool->ev_free[last_half], 0);
+    if (e != cudaSuccess) return neo::cuda_fail(e, "swap pipeline join");
   }
   return NEO_OK;
 }
 
 NEO_API neo_status neo_kv_swap_out(neo_kv_pool* pool, int32_t n, const int32_t* gpu_ids, const int32_t* host_ids,
                                    int32_t l0, int32_t l1, void* staging, size_t staging_bytes, void* stream) {
-  return swap_common(pool, true, n, gpu_ids, host_ids, l0, l1, staging, staging_bytes, stream);
+  return swap_common(pool, true, n, gpu_ids, host_ids, l0, l1, staging, staging_bytes, 0u, stream);
+}
+
+NEO_API neo_status neo_kv_swap_out_ex(neo_kv_pool* pool, int32_t n, const int32_t* gpu_ids, const int32_t* host_ids,
+                                      int32_t l0, int32_t l1, void* staging, size_t staging_bytes, uint32_t flags,
+                                      void* stream) {
+  return swap_common(pool, true, n, gpu_ids, host_ids, l0, l1, staging, staging_bytes, flags, stream);
 }
 
 NEO_API neo_status neo_kv_swap_in(neo_kv_pool* pool, int32_t n, const int32_t* host_ids, const int32_t* gpu_ids,
                                   int32_t l0, int32_t l1, void* staging, size_t staging_bytes, void* stream) {
-  return swap_common(pool, false, n, gpu_ids, host_ids, l0, l1, staging, staging_bytes, stream);
+  return swap_common(pool, false, n, gpu_ids, host_ids, l0, l1, staging, staging_bytes, 0u, stream);
+}
+
+NEO_API neo_status neo_kv_swap_join(neo_kv_pool* pool, void* stream) {
+  if (!pool) return fail(NEO_ERR_INVALID_ARG, "pool is NULL");
+  std::lock_guard<std::mutex> lk(pool->mu);
+  if (!pool->copy_stream) return NEO_OK;  // no pipelined swap was ever issued
+  cudaError_t e = cudaEventRecord(pool->ev_join, pool->copy_stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pool->ev_join, 0);
+  return e == cudaSuccess ? NEO_OK : neo::cuda_fail(e, "neo_kv_swap_join");
 }
 
 }  // extern "C"

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/neo.h"
@@ -18,6 +19,20 @@ constexpr int kTileBytes = kTileTokens * kHeadDim * 2;  // 4096: one K (or V) ti
 constexpr int kMaxGroup = 8;                          // G <= 8 (MMA N = 8)
 constexpr int kMaxChunkTokens = 1024;                 // <= 64 tiles per work unit
 constexpr int kDefaultMaxChunk = 512;                 // cap of the shape-only default chunk
+
+// Runs f(device) once per CUDA device for one call site (kernel attributes such
+// as the dynamic shared-memory limit are per device); thread-safe -- two
+// threads racing on a first launch both run the idempotent f.
+template <typename F>
+inline neo_status once_per_device(std::atomic<uint64_t>& done_mask, F&& f) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done_mask.load(std::memory_order_acquire) & bit) return NEO_OK;
+  const neo_status st = f(dev);
+  if (st == NEO_OK) done_mask.fetch_or(bit, std::memory_order_acq_rel);
+  return st;
+}
 
 // thread-local error text for neo_last_error()
 void set_error(const std::string& msg);
@@ -79,7 +94,7 @@ neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, c
                                int32_t batch, int32_t page_size, int32_t max_seq_len, int64_t num_pages,
                                cudaStream_t stream);
 neo_status debug_validate_offsets(const int32_t* q_offsets, const int32_t* seq_lens, int32_t batch, int32_t total,
-                                  cudaStream_t stream);
+                                  int32_t max_q_len, cudaStream_t stream);
 
 // ---- tensor maps (neo_host.cu; cached by pointer and shape)
 neo_status tensor_map(const void* ptr, int64_t page_stride, int64_t num_pages, int32_t hkv, int32_t P,

@@ -209,7 +209,9 @@ __device__ __forceinline__ int tiles_of_request(const PArgs& a, int b, int rows_
 // all threads of the CTA; ends with __syncthreads
 __device__ void build_sched(const PArgs& a, int rows_tok, Sched& sc, int* nct_tmp) {
   for (int b = threadIdx.x; b < a.batch; b += blockDim.x) {
-    nct_tmp[b] = tiles_of_request(a, b, rows_tok);
+    // clamp: a request longer than max_q_len (caller error; NEO_DEBUG_VALIDATE
+    // reports it) loses its tail rows instead of corrupting the item map
+    nct_tmp[b] = min(tiles_of_request(a, b, rows_tok), a.n_ct_max);
     sc.q_off[b] = a.q_offsets[b];
     sc.ctx[b] = a.seq_lens[b];
   }
@@ -640,15 +642,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, const CUtensorMap& tmk,
                                const CUtensorMap& tmv, const CUtensorMap& tmo) {
-  static int num_sms = 0;
-  if (!num_sms) {
+  static std::atomic<uint64_t> configured{0};
+  static std::atomic<int> sms_of[64];
+  neo_status st = once_per_device(configured, [](int dev) {
     cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e != cudaSuccess) return cuda_fail(e, "prefill smem attribute");
-    int dev = 0;
-    cudaGetDevice(&dev);
-    e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    int n = 0;
+    e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(e, "SM count");
-  }
+    sms_of[dev & 63].store(n, std::memory_order_relaxed);
+    return NEO_OK;
+  });
+  if (st != NEO_OK) return st;
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  const int num_sms = sms_of[cur_dev & 63].load(std::memory_order_relaxed);
   const int G = L.hq / L.hkv;
   const int n_ct_max = (L.max_q_len * G + kTiles * kBM - 1) / (kTiles * kBM);
   const int64_t n_items = static_cast<int64_t>(n_ct_max) * L.batch * L.hkv;   // upper bound

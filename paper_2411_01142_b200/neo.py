@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("NEO_LIB") or os.path.join(_HERE, "libneo.so")   # NEO
 NEO_OK, NEO_ERR_INVALID_ARG, NEO_ERR_OUT_OF_PAGES, NEO_ERR_UNSUPPORTED, NEO_ERR_CUDA, NEO_ERR_INTERNAL = range(6)
 NEO_GPU, NEO_HOST = 0, 1
 NEO_CHUNK_GROUPED = -1          # chunk_tokens selecting the grouped split-K kernel (include/neo.h)
+NEO_SWAP_DEFER_JOIN = 1         # neo_kv_swap_out_ex flag (include/neo.h)
 STATUS_NAMES = {0: "NEO_OK", 1: "NEO_ERR_INVALID_ARG", 2: "NEO_ERR_OUT_OF_PAGES", 3: "NEO_ERR_UNSUPPORTED",
                 4: "NEO_ERR_CUDA", 5: "NEO_ERR_INTERNAL"}
 
@@ -28,7 +29,7 @@ EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_c
             "neo_decode_attn_default_chunk", "neo_decode_attn_plan_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
             "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
             "neo_kv_append", "neo_schedule", "neo_rope_append", "neo_prefill_append", "neo_prefill_attn",
-            "neo_decode_attn_append"]
+            "neo_decode_attn_append", "neo_kv_swap_out_ex", "neo_kv_swap_join"]
 
 
 class NeoError(RuntimeError):
@@ -70,6 +71,8 @@ def lib() -> ctypes.CDLL:
                 "neo_decode_attn_workspace_init": [P, sz, P],
                 "neo_kv_swap_out": [P, i32, P, P, i32, i32, P, sz, P],
                 "neo_kv_swap_in": [P, i32, P, P, i32, i32, P, sz, P],
+                "neo_kv_swap_out_ex": [P, i32, P, P, i32, i32, P, sz, ctypes.c_uint32, P],
+                "neo_kv_swap_join": [P, P],
                 "neo_kv_swap_staging_bytes": [P, i32, i32, i32, P],
                 "neo_cpu_decode_attn": [P, i32, P, P, i32, P, P, i32, i32, ctypes.c_float, i32],
                 "neo_kv_append": [P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
@@ -492,15 +495,24 @@ class KVPool:
         return out.value
 
     def swap_out(self, gpu_ids, host_ids, staging, layer_begin: int = 0, layer_end: int | None = None,
-                 stream=None) -> None:
-        """neo_kv_swap_out; staging=None selects the zero-copy path."""
+                 stream=None, defer_join: bool = False) -> None:
+        """neo_kv_swap_out (defer_join: neo_kv_swap_out_ex with NEO_SWAP_DEFER_JOIN);
+        staging=None selects the zero-copy path."""
         g, h = _ids(gpu_ids), _ids(host_ids)
         if len(g) != len(h):
             raise ValueError("gpu_ids and host_ids differ in length")
         le = self.geo.num_layers if layer_end is None else layer_end
         nbytes = 0 if staging is None else staging.numel() * staging.element_size()
-        check(lib().neo_kv_swap_out(self._h, len(g), g.ctypes.data, h.ctypes.data, layer_begin, le,
-                                    _ptr(staging), nbytes, _stream(stream)))
+        if defer_join:
+            check(lib().neo_kv_swap_out_ex(self._h, len(g), g.ctypes.data, h.ctypes.data, layer_begin, le,
+                                           _ptr(staging), nbytes, NEO_SWAP_DEFER_JOIN, _stream(stream)))
+        else:
+            check(lib().neo_kv_swap_out(self._h, len(g), g.ctypes.data, h.ctypes.data, layer_begin, le,
+                                        _ptr(staging), nbytes, _stream(stream)))
+
+    def swap_join(self, stream=None) -> None:
+        """neo_kv_swap_join: `stream` waits for every PCIe copy of this pool's swaps so far."""
+        check(lib().neo_kv_swap_join(self._h, _stream(stream)))
 
     def swap_in(self, host_ids, gpu_ids, staging, layer_begin: int = 0, layer_end: int | None = None,
                 stream=None) -> None:

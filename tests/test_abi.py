@@ -372,3 +372,17 @@ def test_swap_validation_without_gpu():
     dup = np.array([g[0], g[0]], dtype=np.int32)
     assert L.neo_kv_swap_in(pool.handle, 2, hi.ctypes.data, dup.ctypes.data, 0, 4, 16, per, 0) == 1
     assert L.neo_kv_swap_out(pool.handle, 0, None, None, 0, 4, None, 0, 0) == 0    # n = 0 no-op
+
+
+def test_swap_ex_flag_validation_without_gpu():
+    pool = neo.KVPool(4, 8, num_gpu_pages=10, num_host_pages=10, allocate=False)
+    g = np.ascontiguousarray(pool.alloc(neo.NEO_GPU, 2))
+    h = np.ascontiguousarray(pool.alloc(neo.NEO_HOST, 2))
+    L = neo.lib()
+    per = pool.staging_bytes(1, 0, 4)
+    # unknown flag bits
+    assert L.neo_kv_swap_out_ex(pool.handle, 2, g.ctypes.data, h.ctypes.data, 0, 4, 16, per, 6, 0) == 1
+    # n = 0 is a no-op with the defer flag too; join without any pipelined swap is a no-op
+    assert L.neo_kv_swap_out_ex(pool.handle, 0, None, None, 0, 4, None, 0, neo.NEO_SWAP_DEFER_JOIN, 0) == 0
+    assert L.neo_kv_swap_join(pool.handle, 0) == 0
+    assert L.neo_kv_swap_join(None, 0) == 1

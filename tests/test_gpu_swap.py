@@ -43,7 +43,7 @@ def host_np(pool):
 
 
 @pytest.mark.parametrize("l0,l1", [(0, 4), (1, 3), (3, 4)])
-@pytest.mark.parametrize("staging_pages", [100, 3, 1, 0])
+@pytest.mark.parametrize("staging_pages", [100, 7, 3, 2, 1, 0])
 def test_swap_out_matches_gather_definition(l0, l1, staging_pages):
     import torch
     from paper_2411_01142_b200 import NEO_GPU, NEO_HOST
@@ -144,3 +144,120 @@ def test_attention_bitwise_after_swap_cycle():
         ref = orc.decode_attention(qb, kb, vb, np.float32(1 / np.sqrt(128)))
         got = ni.bf16_bits_to_f64(outs2[layer][1].view(torch.int16).cpu().numpy().view(np.uint16))
         assert within_tol(got, ref)[0]
+
+
+# ---- NEXT-1: layer-wise swap pipeline --------------------
+
+
+@pytest.mark.parametrize("staging_pages", [2, 5, 64])
+def test_layerwise_pipelined_swap_out_with_deferred_join(staging_pages):
+    """NEO's layer-wise swapping: in a layer loop, layer l's pages are written on
+    the main stream, then swapped out for layer l only on a side stream ordered
+    by an event (neo_kv_swap_out_ex + NEO_SWAP_DEFER_JOIN, the next layer's
+    gather overlapping this layer's D2H); one neo_kv_swap_join at the end.  The
+    host record is bit-exact against the oracle's gather definition of the final
+    GPU-cache, and later writes to the GPU pages (after the deferred call's
+    gather) never reach the host record."""
+    import torch
+    from paper_2411_01142_b200 import NEO_GPU, NEO_HOST
+    L = 4
+    pool = make_pool(L=L, npages=64, nhost=64)
+    gids = pool.alloc(NEO_GPU, 40)
+    sel = gids[[5, 17, 2, 33, 8, 9, 10, 11, 39, 0, 1]]
+    hids = pool.alloc(NEO_HOST, 11)
+    staging = torch.empty(pool.staging_bytes(staging_pages, 0, 1), dtype=torch.uint8, device="cuda")
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    view = pool.gpu_view()
+    sel_t = torch.from_numpy(sel.astype(np.int64)).cuda()
+    expect = []
+    for l in range(L):
+        # "compute" layer l's KV on the main stream (a write to exactly those pages)
+        view[l, :, sel_t] = view[l, :, sel_t] + 1 if l % 2 else view[l, :, sel_t].neg()
+        expect.append(oracle.gather_pages(gpu_np(pool), sel, l, l + 1))   # syncs: the bits that must move
+        ev = torch.cuda.Event()
+        ev.record(main)
+        side.wait_event(ev)
+        pool.swap_out(sel, hids, staging, l, l + 1, stream=side, defer_join=True)
+        # once the side stream passed the call, the GPU pages may be overwritten
+        done = torch.cuda.Event()
+        done.record(side)
+        main.wait_event(done)
+        view[l, :, sel_t] = 0
+    pool.swap_join(stream=side)
+    side.synchronize()
+    host = host_np(pool)
+    for l in range(L):
+        assert np.array_equal(oracle.host_record(host, hids, l, l + 1), expect[l]), l
+
+
+@pytest.mark.parametrize("staging_pages", [1, 2, 3, 40])
+def test_swap_out_in_multichunk_roundtrip(staging_pages):
+    """Many chunks through both halves (and the one-buffer path at 1 page):
+    out to host, back in to fresh ids, bit-exact."""
+    import torch
+    from paper_2411_01142_b200 import NEO_GPU, NEO_HOST
+    pool = make_pool(L=3, npages=96, nhost=40)
+    old = pool.alloc(NEO_GPU, 37)
+    hids = pool.alloc(NEO_HOST, 37)
+    staging = torch.empty(pool.staging_bytes(staging_pages), dtype=torch.uint8, device="cuda")
+    before = gpu_np(pool)
+    side = torch.cuda.Stream()
+    pool.swap_out(old, hids, staging, stream=side)
+    side.synchronize()
+    assert np.array_equal(oracle.host_record(host_np(pool), hids, 0, 3), oracle.gather_pages(before, old, 0, 3))
+    new = pool.alloc(NEO_GPU, 37)
+    pool.gpu_view()[:, :, torch.from_numpy(new.astype(np.int64)).cuda()] = 0
+    torch.cuda.synchronize()
+    pool.swap_in(hids, new, staging, stream=side)
+    side.synchronize()
+    after = gpu_np(pool)
+    assert np.array_equal(oracle.gather_pages(after, new, 0, 3), oracle.gather_pages(before, old, 0, 3))
+
+
+def test_swap_out_inside_cuda_graph():
+    """Graph capture takes the one-buffer path (no cross-call events); replay is bit-exact."""
+    import torch
+    from paper_2411_01142_b200 import NEO_GPU, NEO_HOST
+    pool = make_pool()
+    gids = pool.alloc(NEO_GPU, 20)
+    hids = pool.alloc(NEO_HOST, 20)
+    staging = torch.empty(pool.staging_bytes(6), dtype=torch.uint8, device="cuda")
+    pool.swap_out(gids[:2], hids[:2], staging)           # the pool's pipeline exists before the capture
+    torch.cuda.synchronize()
+    pool.host.view(torch.int16).fill_(0x7FC0)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            pool.swap_out(gids, hids, staging, stream=s)
+    torch.cuda.synchronize()
+    assert (host_np(pool) == 0x7FC0).all()                # capture ran nothing
+    before = gpu_np(pool)
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(oracle.host_record(host_np(pool), hids, 0, 4), oracle.gather_pages(before, gids, 0, 4))
+
+
+def test_swap_validation_enqueues_nothing():
+    """All-or-nothing: a staging buffer in host memory, an unallocated id or a
+    bad flag is rejected before anything is enqueued (the host pages keep their
+    fill)."""
+    import torch
+    from paper_2411_01142_b200 import NEO_GPU, NEO_HOST, neo
+    pool = make_pool()
+    gids = pool.alloc(NEO_GPU, 8)
+    hids = pool.alloc(NEO_HOST, 8)
+    torch.cuda.synchronize()
+    host_stg = torch.empty(pool.staging_bytes(8), dtype=torch.uint8).pin_memory()
+    with pytest.raises(neo.NeoError):
+        pool.swap_out(gids, hids, host_stg)
+    stg = torch.empty(pool.staging_bytes(8), dtype=torch.uint8, device="cuda")
+    with pytest.raises(neo.NeoError):
+        pool.swap_out(np.append(gids[:7], 63), hids, stg)
+    L = neo.lib()
+    g, h = np.ascontiguousarray(gids), np.ascontiguousarray(hids)
+    assert L.neo_kv_swap_out_ex(pool.handle, 8, g.ctypes.data, h.ctypes.data, 0, 4, stg.data_ptr(),
+                                stg.numel(), 2, 0) == neo.NEO_ERR_INVALID_ARG
+    torch.cuda.synchronize()
+    assert (host_np(pool) == 0x7FC0).all()
