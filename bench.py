@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-swap", action="store_true", help="c3: skip the concurrent swap-out")
     p.add_argument("--no-prefill", action="store_true", help="skip the NEXT-3 prefill leg")
     p.add_argument("--graph", action="store_true", help="capture the step's launches in a CUDA graph")
+    p.add_argument("--no-kv-stable", action="store_true",
+                   help="plain neo_decode_attn (no NEO_ATTN_KV_STABLE early KV prefetch before the PDL wait)")
     return p.parse_args()
 
 
@@ -264,10 +266,15 @@ def run_neo(args):
     out = torch.empty(L, gb.B, gb.hq, 128, dtype=torch.bfloat16, device="cuda")
     torch.cuda.synchronize()
 
+    # every layer call reads KV that no kernel of the step writes (one
+    # attention launch per layer over immutable earlier-token pages), so the
+    # calls declare NEO_ATTN_KV_STABLE (include/neo.h)
+    kv_stable = not args.no_kv_stable
+
     def attn_layer(l):
         k, v = gb.layer(l)
         neo.decode_attn(gb.q[l % gb.layers], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=out[l],
-                        chunk_tokens=chunk, workspace=ws, stream=stream)
+                        chunk_tokens=chunk, workspace=ws, stream=stream, kv_stable=kv_stable)
 
     def step(events=None):
         for l in range(L):
@@ -414,6 +421,7 @@ def run_neo(args):
                        ">> 126 MB L2; no flush") if flush is None else
                       "L2 flushed (512 MB read) before every step, outside the timed attention window",
                 "cuda_graph": bool(graph is not None),
+                "kv_stable": kv_stable,
             },
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
@@ -698,7 +706,9 @@ def run_swap(args, gb, L, step, attn_layer, stream):
     # attention while a swap-out runs on the side stream
     steps = max(2, min(args.steps, 5))
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0 = time.perf_counter()
     sa, sb = timed(lambda: pool.swap_out(gpu_ids, host_ids, staging, stream=side), side)
+    enqueue_ms = (time.perf_counter() - h0) * 1e3
     s0.record(stream)
     for _ in range(steps):
         step()
@@ -747,6 +757,10 @@ def run_swap(args, gb, L, step, attn_layer, stream):
             "attention_gbs_during_swap": round(gb.kv_bytes_per_call() * L * steps / t_att / 1e9, 2),
             "attention_steps_during_swap": steps, "staging_bytes": int(staging.numel()),
             "swap_outlasted_attention": bool(sa.elapsed_time(s1) < sa.elapsed_time(sb)),
+            "concurrent_leg": {"swap_enqueue_host_ms": round(enqueue_ms, 3),
+                               "attention_start_after_swap_start_ms": round(sa.elapsed_time(s0), 3),
+                               "attention_end_after_swap_start_ms": round(sa.elapsed_time(s1), 3),
+                               "swap_ms": round(sa.elapsed_time(sb), 3)},
             "layerwise_pipeline": {
                 "what": "per decode step: attention(l) on the main stream, then swap-out of the 16 victims' "
                         "layer-l pages on a side stream (neo_kv_swap_out_ex, NEO_SWAP_DEFER_JOIN; staging split "
@@ -807,7 +821,7 @@ def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
             stream.wait_event(ev_in[i][l])
             k, v = gb.layer(l)
             neo.decode_attn(q_dev[i][l], k, v, bt_dev[i], sl_dev[i], gb.max_seq_len, out=out_dev[i][l],
-                            chunk_tokens=chunk, workspace=ws, stream=stream)
+                            chunk_tokens=chunk, workspace=ws, stream=stream, kv_stable=not args.no_kv_stable)
             ev_att[i][l].record(stream)
         ev_used[i].record(stream)
         with torch.cuda.stream(d2h_s):

@@ -148,11 +148,12 @@ NEO_API neo_status neo_kv_layer_view(const neo_kv_pool* pool, int32_t layer, voi
  *   scale       softmax scale, typically 1/sqrt(D) (DESIGN c1).
  *   chunk_tokens split-K chunk length C (multiple of 16 and of P, <= 1024), or 0 for
  *               the library default neo_decode_attn_default_chunk(), or
- *               NEO_CHUNK_GROUPED (-1), -2 or -4: the grouped kernel -- each
- *               request's tiles split into ceil(tiles / (256/k)) equal groups
- *               (k = 1, 2, 4: groups of at most 4096, 2048, 1024 tokens) of four
- *               equal per-warp ranges, one CTA per group, merged in shared
- *               memory; single-group requests need no partials.
+ *               NEO_CHUNK_GROUPED (-1), -2 or -4, or -T for T a multiple of 16
+ *               in [64, 4096]: the grouped kernel -- each request's tiles split
+ *               into ceil(tiles / (T/16)) equal groups (-1, -2, -4 = groups of at
+ *               most 4096, 2048, 1024 tokens; -T = at most T tokens), the tiles
+ *               of a group dealt round-robin to four warps, one CTA per group,
+ *               merged in shared memory; single-group requests need no partials.
  *               neo_decode_attn_plan_chunk() picks among these and the split
  *               chunks.  The result for
  *               request b depends only on (its inputs, C): outputs are bitwise
@@ -169,6 +170,26 @@ NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const voi
                                    int32_t num_kv_heads, int32_t head_dim, int32_t page_size, int32_t max_seq_len,
                                    float scale, int32_t chunk_tokens, void* workspace, size_t workspace_bytes,
                                    void* stream);
+
+/* neo_decode_attn with flags.  NEO_ATTN_KV_STABLE: the caller guarantees that
+ * the kernels still running on `stream` when this call is enqueued write none
+ * of the KV pages, block table or seq_lens this call reads -- except each
+ * request's newest token slot (a preceding neo_kv_append / neo_rope_append).
+ * With programmatic dependent launch the kernel then reads the metadata and
+ * streams its first KV tiles (never a tile holding a newest token) BEFORE
+ * waiting on the preceding kernel, overlapping that kernel's tail; q is read
+ * and every output written only after the wait.  Holds for the layers of a
+ * decode step (earlier tokens' KV is immutable); do NOT set it right after a
+ * swap-in scatter or neo_prefill_append into pages this call reads.  Same
+ * result bit for bit; other arguments and errors as neo_decode_attn
+ * (NEO_ERR_INVALID_ARG for unknown flag bits). */
+#define NEO_ATTN_KV_STABLE 1u
+NEO_API neo_status neo_decode_attn_ex(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+                                      int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
+                                      const int32_t* seq_lens, void* out, int32_t batch, int32_t num_q_heads,
+                                      int32_t num_kv_heads, int32_t head_dim, int32_t page_size, int32_t max_seq_len,
+                                      float scale, int32_t chunk_tokens, void* workspace, size_t workspace_bytes,
+                                      uint32_t flags, void* stream);
 
 /* Append this decode step's K and V rows to the paged cache (the
  * decoding stage "read-and-appends the KV cache"), before neo_decode_attn:
@@ -266,7 +287,8 @@ NEO_API neo_status neo_decode_attn_append(const void* q, const float* inv_freq, 
                                           void* stream);
 
 /* chunk_tokens value selecting the grouped split-K kernel with groups of <= 4096
- * tokens; -2 and -4 select groups of <= 2048 and <= 1024 tokens (neo_decode_attn). */
+ * tokens; -2 and -4 select groups of <= 2048 and <= 1024 tokens, -T (T a
+ * multiple of 16 in [64, 4096]) groups of <= T tokens (neo_decode_attn). */
 #define NEO_CHUNK_GROUPED (-1)
 
 /* Default split-K chunk length for a call shape (deterministic in its inputs). */
@@ -278,7 +300,8 @@ NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_head
  * neo_decode_attn_append call over these requests (DESIGN §6 "chunk planner"):
  *  - a replay of the GPU's in-order CTA dispatch scores the split kernel at
  *    C in {1024, 640, 512, 448, 384, 320, 256} (multiples of page_size) and the
- *    grouped kernel at groups of 4096 / 2048 / 1024 tokens (-1 / -2 / -4);
+ *    grouped kernel at groups of 4096 / 3072 / 2048 / 1536 / 1024 tokens
+ *    (returned as -1 / -3072 / -2 / -1536 / -4);
  *    a smaller C, a smaller group, and the grouped kernel over the split one
  *    must each win by > 1 %;
  *  - grids of >= 16 waves at C = 1024 score only that split chunk;
@@ -289,7 +312,7 @@ NEO_API int32_t neo_decode_attn_default_chunk(int32_t batch, int32_t num_kv_head
  * (148 when no device is visible).
  *   seq_lens     [batch] int32, HOST, each >= 0 (the values the call will see).
  *   chunk_tokens out: a valid chunk_tokens argument for page_size (possibly
- *                -1, -2 or -4: the grouped kernel).
+ *                -1, -3072, -2, -1536 or -4: the grouped kernel).
  * Any choice is correct (the result depends on it only through fp32 rounding);
  * this only affects speed.
  * Errors: NEO_ERR_INVALID_ARG (NULL pointers, batch < 0, num_kv_heads < 1, a

@@ -55,6 +55,11 @@ struct KArgs {
   int64_t page_stride;
   int32_t probe;              // experiment knob (NEO_ATTN_PROBE bits): 1 no epilogue, 2 no tile math,
                               // 4 no combine, 8 partial stores only (no counter); 0 in production
+  int32_t early;              // NEO_ATTN_KV_STABLE (see kernel prologues)
+  int32_t l2pf;               // L2 prefetch distance in tiles beyond the smem ring (0 = off)
+  int32_t l2pro;              // tiles prefetched into L2 in the prologue only (before the PDL wait)
+  int32_t first_wave;         // CTAs of the first resident wave (the ones that start during the
+                              // previous grid's tail under PDL)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -556,6 +561,21 @@ __device__ __forceinline__ void issue_tile(const CUtensorMap* tmk, const CUtenso
   tma_load_tile(dst + kTileBytes, tmv, tok_in_page, g, pid, bar, policy);
 }
 
+// L2 prefetch of one K + V tile (TMA, no shared memory, no barrier): deepens the
+// memory-level parallelism beyond the smem ring.  The L2 is the GPU's point of
+// coherence, so a prefetch can never make a later load see stale data.
+__device__ __forceinline__ void prefetch_tile_l2(const CUtensorMap* tmk, const CUtensorMap* tmv, int tok_in_page,
+                                                 int g, int pid) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmk)),
+               "r"(0), "r"(0), "r"(tok_in_page), "r"(g), "r"(pid)
+               : "memory");
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmv)),
+               "r"(0), "r"(0), "r"(tok_in_page), "r"(g), "r"(pid)
+               : "memory");
+}
+
 // ------------------------------------------------- kernel 1: one unit per warp
 
 // kStreamOnly = roofline probe (NEO_ATTN_CFG="s4,2"): identical grid, page walk
@@ -596,7 +616,10 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
   const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
   const uint32_t bar0 = smem_u32(&bars[warp][0]);
   init_ring(bar0, kStages, lane);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // NEO_ATTN_KV_STABLE: metadata and the first KV tiles before the wait (as in
+  // decode_attn_group_kernel); otherwise wait before touching any input
+  const bool early = !kFuse && a.early;
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int64_t unit = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
@@ -624,9 +647,10 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
     my_pid2 = __ldg(a.block_table + static_cast<int64_t>(b) * a.max_blocks + pg);
   }
   uint4 qf[4];
-  load_q(a, b, g, r, qd, qf);
+  if (!early) load_q(a, b, g, r, qd, qf);
   const int ctx = __ldg(a.seq_lens + b);
   if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
+    if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (c == 0) write_zero_row(a, b, g, lane);
     return;
   }
@@ -647,8 +671,22 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
                  pid, policy);
     }
   };
+  auto prefetch = [&](int j) {   // tile j of the unit into L2 (j warp-uniform)
+    if (j >= nt) return;
+    const int pid = j < 32 ? __shfl_sync(kFull, my_pid, j) : __shfl_sync(kFull, my_pid2, j - 32);
+    if (lane == 0) prefetch_tile_l2(&tmk, &tmv, ((t_begin + j) * kTileTokens) % a.page_size, g, pid);
+  };
   const int npro = nt < kStages ? nt : kStages;
-  for (int j = 0; j < npro; ++j) issue(j);
+  int pre = npro;   // tiles issued before the wait: never the newest token's (the last tile)
+  if (early)
+    while (pre > 0 && t_begin + pre - 1 >= ntile_total - 1) --pre;
+  for (int j = 0; j < pre; ++j) issue(j);
+  for (int j = npro; j < npro + a.l2pf + (early && blockIdx.x < a.first_wave ? a.l2pro : 0); ++j) prefetch(j);
+  if (early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    load_q(a, b, g, r, qd, qf);
+    for (int j = pre; j < npro; ++j) issue(j);
+  }
 
   Acc acc;
   acc_reset(acc);
@@ -664,6 +702,7 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
     if (j + kStages < nt) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(j + kStages);
+      if (a.l2pf) prefetch(j + kStages + a.l2pf);
     }
       if (!kStreamOnly && !(a.probe & 2)) compute_tile(f, qf, ctx - (t_begin + j) * kTileTokens, a.scale_log2, r, qd, acc);
   }
@@ -745,7 +784,13 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   const uint32_t sbase = smem_u32(base) + warp * (kStages * kStageBytes);
   const uint32_t bar0 = smem_u32(&bars[warp][0]);
   init_ring(bar0, kStages, lane);
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // NEO_ATTN_KV_STABLE: the caller guarantees the kernels still running on the
+  // stream write none of the metadata and KV this call reads except each
+  // request's newest token, so the metadata and the first KV tiles (not the
+  // newest token's) are read BEFORE waiting on the previous grid: the KV
+  // stream starts during its tail.  q, and everything written, after the wait.
+  const bool early = !kFuse && a.early;
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
   const int q = static_cast<int>(blockIdx.x / BH);
@@ -753,7 +798,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   const int b = bg / a.hkv;
   const int g = bg - b * a.hkv;
   uint4 qf[4];
-  load_q(a, b, g, r, qd, qf);
+  if (!early) load_q(a, b, g, r, qd, qf);
   // Warp w takes tiles g0 + w, g0 + w + 4, ... of its group (interleaved), so for
   // the first group (g0 = 0, every single-group request) lane i's page ids --
   // tiles w + 4i and w + 4(i + 32) -- are known before seq_lens arrives: issue
@@ -766,6 +811,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   }
   const int ctx = __ldg(a.seq_lens + b);
   if (ctx <= 0) {  // reading c4: empty context -> zero row, pages never read
+    if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (q == 0 && warp == 0) write_zero_row(a, b, g, lane);
     return;
   }
@@ -790,8 +836,22 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
                  ((first + kGroupWarps * j) * kTileTokens) % a.page_size, g, pid, policy);
     }
   };
+  auto prefetch = [&](int j) {   // this warp's tile j into L2 (j warp-uniform)
+    if (j >= nt) return;
+    const int pid = j < 32 ? __shfl_sync(kFull, my_pid, j) : __shfl_sync(kFull, my_pid2, j - 32);
+    if (lane == 0) prefetch_tile_l2(&tmk, &tmv, ((first + kGroupWarps * j) * kTileTokens) % a.page_size, g, pid);
+  };
   const int npro = nt < kStages ? nt : kStages;
-  for (int j = 0; j < npro; ++j) issue(j);
+  int pre = npro;   // tiles issued before the wait: never the newest token's (the last tile)
+  if (early)
+    while (pre > 0 && first + kGroupWarps * (pre - 1) >= ntile_total - 1) --pre;
+  for (int j = 0; j < pre; ++j) issue(j);
+  for (int j = npro; j < npro + a.l2pf + (early && blockIdx.x < a.first_wave ? a.l2pro : 0); ++j) prefetch(j);
+  if (early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    load_q(a, b, g, r, qd, qf);
+    for (int j = pre; j < npro; ++j) issue(j);
+  }
 
   Acc acc;
   acc_reset(acc);
@@ -807,6 +867,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
     if (j + kStages < nt) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(j + kStages);
+      if (a.l2pf) prefetch(j + kStages + a.l2pf);
     }
     compute_tile(f, qf, ctx - (first + kGroupWarps * j) * kTileTokens, a.scale_log2, r, qd, acc);
   }
@@ -937,7 +998,9 @@ static neo_status launch_unit(const KArgs& a, const CUtensorMap& tmk, const CUte
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S, kStreamOnly, kFuse>, tmk, tmv, a);
+  KArgs ka = a;
+  ka.first_wave = device_sm_count() * ctas_per_sm<W, S>();
+  cudaLaunchKernelEx(&cfg, decode_attn_kernel<W, S, kStreamOnly, kFuse>, tmk, tmv, ka);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_attn_kernel launch");
   return NEO_OK;
@@ -974,7 +1037,9 @@ static neo_status launch_group(const KArgs& a, const CUtensorMap& tmk, const CUt
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, decode_attn_group_kernel<S, kFuse>, tmk, tmv, a);
+  KArgs ka = a;
+  ka.first_wave = device_sm_count() * ctas_per_sm<kGroupWarps, S>();
+  cudaLaunchKernelEx(&cfg, decode_attn_group_kernel<S, kFuse>, tmk, tmv, ka);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "decode_attn_group_kernel launch");
   return NEO_OK;
@@ -1029,6 +1094,17 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
     return v ? std::atoi(v) : 0;
   }();
   a.probe = probe;
+  a.early = L.early ? 1 : 0;
+  static const int l2pf = [] {
+    const char* v = std::getenv("NEO_ATTN_L2PF");
+    return v ? std::max(0, std::min(16, std::atoi(v))) : 0;
+  }();
+  a.l2pf = l2pf;
+  static const int l2pro = [] {
+    const char* v = std::getenv("NEO_ATTN_L2PRO");
+    return v ? std::max(0, std::min(32, std::atoi(v))) : 2;
+  }();
+  a.l2pro = l2pro;
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
   if (L.grouped) {   // grouped kernel: max_chunks = groups per request, chunk_tiles = group tiles
     a.chunk_tiles = group_tiles_of(L.chunk_tokens);

@@ -249,15 +249,6 @@ double plan_score_grouped(const std::vector<int32_t>& ntiles, int32_t hkv, int32
   return makespan > 0 ? static_cast<double>(total) * hkv / makespan : 0.0;
 }
 
-int device_sm_count() {
-  int dev = 0, n = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
-    cudaGetLastError();   // no device visible (CPU box): plan for a B200
-    return 148;
-  }
-  return n;
-}
 
 neo_status check_chunk(int32_t C, int32_t P) {
   if (C <= 0 || C % kTileTokens != 0 || C % P != 0 || C > kMaxChunkTokens)
@@ -267,6 +258,22 @@ neo_status check_chunk(int32_t C, int32_t P) {
 }
 
 }  // namespace
+
+int device_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();   // no device visible (CPU box): plan for a B200
+    return 148;
+  }
+  if ((n = cache[dev & 63].load(std::memory_order_relaxed)) > 0) return n;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    return 148;
+  }
+  cache[dev & 63].store(n, std::memory_order_relaxed);
+  return n;
+}
 
 // debug validation: copies device metadata back (synchronous; debug only)
 neo_status debug_validate_attn(const int32_t* block_table, int32_t max_blocks, const int32_t* seq_lens,
@@ -592,15 +599,17 @@ NEO_API neo_status neo_decode_attn_plan_chunk(const int32_t* seq_lens, int32_t b
       }
     }
   }
-  // the grouped kernel (groups of 4096, 2048 or 1024 tokens, largest first) must
-  // beat the best split chunk -- and a smaller group the larger one -- by > 1 %
+  // the grouped kernel (groups of 4096 ... 1024 tokens, largest first) must beat
+  // the best split chunk -- and a smaller group the larger one -- by > 1 %
   double best_g = -1.0;
-  int32_t best_k = 0;
-  for (int32_t k : {1, 2, 4}) {
-    const double sc = neo::plan_score_grouped(ntiles, hkv, neo::kGroupTiles / k, sms);
-    if (sc > best_g * 1.01) best_g = sc, best_k = k;
+  int32_t best_t = 0;
+  for (int32_t T : {4096, 3072, 2048, 1536, 1024}) {
+    const double sc = neo::plan_score_grouped(ntiles, hkv, T / neo::kTileTokens, sms);
+    if (sc > best_g * 1.01) best_g = sc, best_t = T;
   }
-  *chunk_tokens = best_g > best_score * 1.01 ? -best_k : best;
+  // the legacy codes for the power-of-two group sizes (-1, -2, -4), -T otherwise
+  const int32_t gcode = best_t == 4096 ? -1 : best_t == 2048 ? -2 : best_t == 1024 ? -4 : -best_t;
+  *chunk_tokens = best_g > best_score * 1.01 ? gcode : best;
   return NEO_OK;
 }
 
@@ -642,7 +651,8 @@ static neo_status decode_attn_impl(const void* q, const void* k_pages, const voi
                                    const int32_t* seq_lens, void* out, int32_t batch, int32_t hq, int32_t hkv,
                                    int32_t d, int32_t page_size, int32_t max_seq_len, float scale,
                                    int32_t chunk_tokens, void* workspace, size_t workspace_bytes, void* stream,
-                                   const float* inv_freq, const void* k_new, const void* v_new) {
+                                   const float* inv_freq, const void* k_new, const void* v_new, uint32_t flags = 0) {
+  if (flags & ~static_cast<uint32_t>(NEO_ATTN_KV_STABLE)) return fail(NEO_ERR_INVALID_ARG, "unknown attention flags");
   if (page_size < 16 || page_size % 16 != 0) return fail(NEO_ERR_UNSUPPORTED, "page_size must be a multiple of 16");
   neo_status st = attn_shape(batch, hq, hkv, d, max_seq_len, &chunk_tokens, page_size);
   if (st != NEO_OK) return st;
@@ -677,6 +687,7 @@ static neo_status decode_attn_impl(const void* q, const void* k_pages, const voi
   neo::AttnLaunch L{q, out, block_table, seq_lens, workspace, workspace_bytes, batch, hq, hkv, page_size,
                     max_blocks, chunk_tokens, max_chunks, scale, s};
   L.grouped = grouped;
+  L.early = (flags & NEO_ATTN_KV_STABLE) && !k_new;
   if (k_new) {
     L.inv_freq = inv_freq;
     L.k_new = k_new;
@@ -696,6 +707,17 @@ NEO_API neo_status neo_decode_attn(const void* q, const void* k_pages, const voi
   return decode_attn_impl(q, k_pages, v_pages, page_stride, num_pages, block_table, max_blocks, seq_lens, out, batch,
                           hq, hkv, d, page_size, max_seq_len, scale, chunk_tokens, workspace, workspace_bytes, stream,
                           nullptr, nullptr, nullptr);
+}
+
+NEO_API neo_status neo_decode_attn_ex(const void* q, const void* k_pages, const void* v_pages, int64_t page_stride,
+                                      int64_t num_pages, const int32_t* block_table, int32_t max_blocks,
+                                      const int32_t* seq_lens, void* out, int32_t batch, int32_t hq, int32_t hkv,
+                                      int32_t d, int32_t page_size, int32_t max_seq_len, float scale,
+                                      int32_t chunk_tokens, void* workspace, size_t workspace_bytes, uint32_t flags,
+                                      void* stream) {
+  return decode_attn_impl(q, k_pages, v_pages, page_stride, num_pages, block_table, max_blocks, seq_lens, out, batch,
+                          hq, hkv, d, page_size, max_seq_len, scale, chunk_tokens, workspace, workspace_bytes, stream,
+                          nullptr, nullptr, nullptr, flags);
 }
 
 NEO_API neo_status neo_decode_attn_append(const void* q, const float* inv_freq, const void* k_new, const void* v_new,

@@ -34,6 +34,9 @@ inline neo_status once_per_device(std::atomic<uint64_t>& done_mask, F&& f) {
   return st;
 }
 
+// SM count of the current device (148 when no device is visible)
+int device_sm_count();
+
 // thread-local error text for neo_last_error()
 void set_error(const std::string& msg);
 neo_status fail(neo_status st, const std::string& msg);
@@ -58,11 +61,15 @@ struct AttnLaunch {
   void* v_pages = nullptr;
   int64_t page_stride = 0;
   bool grouped = false;        // NEO_CHUNK_GROUPED: max_chunks holds the group count
+  bool early = false;          // NEO_ATTN_KV_STABLE: metadata + first KV tiles before the PDL wait
 };
 constexpr int kGroupTiles = 4 * 64;                   // largest group of the grouped kernel (tiles)
-// chunk_tokens -k (k = 1, 2, 4) selects groups of kGroupTiles / k tiles
-inline bool is_grouped_chunk(int32_t c) { return c == -1 || c == -2 || c == -4; }
-inline int32_t group_tiles_of(int32_t c) { return kGroupTiles / (-c); }
+// chunk_tokens -k (k = 1, 2, 4) selects groups of kGroupTiles / k tiles; any
+// other negative value -T (T a multiple of 16 in [64, 4096]) groups of T tokens
+inline bool is_grouped_chunk(int32_t c) {
+  return c == -1 || c == -2 || c == -4 || (c <= -64 && c >= -kGroupTiles * kTileTokens && (-c) % kTileTokens == 0);
+}
+inline int32_t group_tiles_of(int32_t c) { return c >= -4 ? kGroupTiles / (-c) : (-c) / kTileTokens; }
 inline int32_t max_groups_for(int32_t max_seq_len, int32_t group_tiles) {
   const int32_t tiles = (max_seq_len + kTileTokens - 1) / kTileTokens;
   return tiles > 0 ? (tiles + group_tiles - 1) / group_tiles : 1;

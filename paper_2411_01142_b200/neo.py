@@ -21,6 +21,7 @@ NEO_OK, NEO_ERR_INVALID_ARG, NEO_ERR_OUT_OF_PAGES, NEO_ERR_UNSUPPORTED, NEO_ERR_
 NEO_GPU, NEO_HOST = 0, 1
 NEO_CHUNK_GROUPED = -1          # chunk_tokens selecting the grouped split-K kernel (include/neo.h)
 NEO_SWAP_DEFER_JOIN = 1         # neo_kv_swap_out_ex flag (include/neo.h)
+NEO_ATTN_KV_STABLE = 1          # neo_decode_attn_ex flag (include/neo.h)
 STATUS_NAMES = {0: "NEO_OK", 1: "NEO_ERR_INVALID_ARG", 2: "NEO_ERR_OUT_OF_PAGES", 3: "NEO_ERR_UNSUPPORTED",
                 4: "NEO_ERR_CUDA", 5: "NEO_ERR_INTERNAL"}
 
@@ -29,7 +30,7 @@ EXPORTED = ["neo_last_error", "neo_version", "neo_kv_pool_bytes", "neo_kv_pool_c
             "neo_decode_attn_default_chunk", "neo_decode_attn_plan_chunk", "neo_decode_attn_workspace_bytes", "neo_decode_attn_workspace_init",
             "neo_kv_swap_out", "neo_kv_swap_in", "neo_kv_swap_staging_bytes", "neo_cpu_decode_attn",
             "neo_kv_append", "neo_schedule", "neo_rope_append", "neo_prefill_append", "neo_prefill_attn",
-            "neo_decode_attn_append", "neo_kv_swap_out_ex", "neo_kv_swap_join"]
+            "neo_decode_attn_append", "neo_kv_swap_out_ex", "neo_kv_swap_join", "neo_decode_attn_ex"]
 
 
 class NeoError(RuntimeError):
@@ -73,6 +74,8 @@ def lib() -> ctypes.CDLL:
                 "neo_kv_swap_in": [P, i32, P, P, i32, i32, P, sz, P],
                 "neo_kv_swap_out_ex": [P, i32, P, P, i32, i32, P, sz, ctypes.c_uint32, P],
                 "neo_kv_swap_join": [P, P],
+                "neo_decode_attn_ex": [P, P, P, i64, i64, P, i32, P, P, i32, i32, i32, i32, i32, i32,
+                                       ctypes.c_float, i32, P, sz, ctypes.c_uint32, P],
                 "neo_kv_swap_staging_bytes": [P, i32, i32, i32, P],
                 "neo_cpu_decode_attn": [P, i32, P, P, i32, P, P, i32, i32, ctypes.c_float, i32],
                 "neo_kv_append": [P, P, i64, i64, P, i32, P, P, P, i32, i32, i32, i32, P],
@@ -164,8 +167,9 @@ def make_workspace(batch: int, num_q_heads: int, num_kv_heads: int, max_seq_len:
 
 
 def decode_attn(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, *, out=None, scale=None,
-                chunk_tokens: int = 0, workspace=None, stream=None, num_pages=None):
-    """Batched paged GQA decode attention: ``neo_decode_attn``.
+                chunk_tokens: int = 0, workspace=None, stream=None, num_pages=None, kv_stable: bool = False):
+    """Batched paged GQA decode attention: ``neo_decode_attn``
+    (``neo_decode_attn_ex`` with NEO_ATTN_KV_STABLE when ``kv_stable``).
 
     q [B][Hq][D] bf16 cuda; k_pages/v_pages [num_pages][Hkv][P][D] bf16 cuda views
     (page stride taken from ``stride(0)``; inner [Hkv][P][D] must be contiguous);
@@ -193,11 +197,14 @@ def decode_attn(q, k_pages, v_pages, block_table, seq_lens, max_seq_len: int, *,
         scale = 1.0 / math.sqrt(d)
     if workspace is None:
         workspace = make_workspace(B, hq, hkv, max_seq_len, chunk_tokens, device=q.device, stream=stream)
-    check(lib().neo_decode_attn(
-        q.data_ptr(), k_pages.data_ptr(), v_pages.data_ptr(), k_pages.stride(0),
-        int(num_pages if num_pages is not None else npages), block_table.data_ptr(), block_table.shape[1],
-        seq_lens.data_ptr(), out.data_ptr(), B, hq, hkv, d, P, int(max_seq_len), float(scale), int(chunk_tokens),
-        workspace.data_ptr(), workspace.numel(), _stream(stream)))
+    args = (q.data_ptr(), k_pages.data_ptr(), v_pages.data_ptr(), k_pages.stride(0),
+            int(num_pages if num_pages is not None else npages), block_table.data_ptr(), block_table.shape[1],
+            seq_lens.data_ptr(), out.data_ptr(), B, hq, hkv, d, P, int(max_seq_len), float(scale), int(chunk_tokens),
+            workspace.data_ptr(), workspace.numel())
+    if kv_stable:
+        check(lib().neo_decode_attn_ex(*args, NEO_ATTN_KV_STABLE, _stream(stream)))
+    else:
+        check(lib().neo_decode_attn(*args, _stream(stream)))
     return out
 
 

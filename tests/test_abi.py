@@ -178,12 +178,13 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=2.0, om=2.0):
             sc = split_score(C)
             if sc > best_sc * 1.01:
                 best, best_sc = C, sc
-    best_g, best_k = -1.0, 0
-    for k in (1, 2, 4):
-        sc = grouped_score(256 // k)
+    best_g, best_t = -1.0, 0
+    for T in (4096, 3072, 2048, 1536, 1024):
+        sc = grouped_score(T // 16)
         if sc > best_g * 1.01:
-            best_g, best_k = sc, k
-    return -best_k if best_g > best_sc * 1.01 else best
+            best_g, best_t = sc, T
+    code = {4096: -1, 2048: -2, 1024: -4}.get(best_t, -best_t)
+    return code if best_g > best_sc * 1.01 else best
 
 
 def test_plan_chunk():
@@ -195,7 +196,7 @@ def test_plan_chunk():
         B, hkv, P = int(rng.integers(1, 700)), int(rng.choice([1, 2, 4, 8])), int(rng.choice([16, 32, 64]))
         ctx = rng.integers(0, int(rng.choice([300, 3000, 20000])), size=B).astype(np.int32)
         C = neo.plan_chunk(ctx, hkv, P)
-        assert C in (-1, -2, -4) or (C % 16 == 0 and C % P == 0 and 16 <= C <= 1024)
+        assert C in (-1, -2, -4, -3072, -1536) or (C % 16 == 0 and C % P == 0 and 16 <= C <= 1024)
         ref = _plan_replay(ctx.tolist(), hkv, P)
         if ref is not None:
             assert C == ref, (B, hkv, P, C, ref)
@@ -207,6 +208,8 @@ def test_plan_chunk():
     assert [neo.plan_chunk(c4, 8 // n, 16) for n in (8, 4, 2, 1)] == [-2, -2, -1, -1]
     # uniform ~1K batches of 2048 (request, kv-head) pairs take the grouped kernel (c2)
     assert neo.plan_chunk(WORKLOADS["c2"].contexts(), 8, 16) == neo.NEO_CHUNK_GROUPED
+    # c3 (4K-8K): 3072-token groups (profiles/r02_group_sweep.md: 6931-6963 GB/s vs 6719-6960 for split 640)
+    assert neo.plan_chunk(WORKLOADS["c3"].contexts(), 8, 16) == -3072
     assert neo.plan_chunk([], 8, 16) == neo.default_chunk(0, 8, 0)
     assert neo.plan_chunk(WORKLOADS["c1"].contexts(), 32, 16) == neo.NEO_CHUNK_GROUPED   # latency-bound c1
     with pytest.raises(neo.NeoError) as e:
@@ -230,10 +233,17 @@ def test_grouped_workspace_and_chunk_validation():
     assert three >= units * 4 * 8 + units * 4 * 128 * 4
     four = neo.workspace_bytes(256, 32, 8, 4096, chunk_tokens=-4)   # 1024-token groups: 4 per request
     assert four >= 256 * 8 * 4 * (4 * 8 + 4 * 128 * 4)
-    with pytest.raises(neo.NeoError) as e:
-        neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=-3)
-    assert e.value.status == neo.NEO_ERR_UNSUPPORTED
+    # any group of T tokens, T a multiple of 16 in [64, 4096]: -1536 -> 3 groups of a 4096-token request
+    t1536 = neo.workspace_bytes(256, 32, 8, 4096, chunk_tokens=-1536)
+    assert t1536 >= 256 * 8 * 3 * (4 * 8 + 4 * 128 * 4)
+    assert neo.workspace_bytes(256, 32, 8, 4096, chunk_tokens=-4096) == neo.workspace_bytes(
+        256, 32, 8, 4096, chunk_tokens=-1)
+    for bad in (-3, -5, -48, -1000, -4112, -8192):
+        with pytest.raises(neo.NeoError) as e:
+            neo.workspace_bytes(256, 32, 8, 1126, chunk_tokens=bad)
+        assert e.value.status == neo.NEO_ERR_UNSUPPORTED, bad
     assert _attn(C=-1) != neo.NEO_ERR_UNSUPPORTED           # accepted (fails later only on fake pointers)
+    assert _attn(C=-768) != neo.NEO_ERR_UNSUPPORTED
 
 
 def test_pool_bytes_and_layer_view():

@@ -419,7 +419,7 @@ def test_decode_attn_append_rope_vs_oracle(chunk, P):
 GROUPED = -1
 
 
-@pytest.mark.parametrize("k", [-1, -2, -4])
+@pytest.mark.parametrize("k", [-1, -2, -4, -64, -400, -1536, -3072, -4096])
 @pytest.mark.parametrize("hq,hkv", [(32, 8), (64, 8), (32, 32), (28, 4), (24, 8), (8, 1), (40, 8)])
 def test_parity_grouped(hq, hkv, k):
     """One CTA per group of <= 256 / -k tiles, 4 per-warp ranges merged in shared
@@ -465,3 +465,73 @@ def test_grouped_workspace_reuse():
     eager = case.run(chunk_tokens=GROUPED, workspace=ws).clone()
     again = case.run(chunk_tokens=GROUPED, workspace=ws).clone()
     assert torch.equal(eager.view(torch.int16), again.view(torch.int16))
+
+
+# ---- NEO_ATTN_KV_STABLE (neo_decode_attn_ex): metadata and first KV tiles before the PDL wait
+
+
+@pytest.mark.parametrize("chunk", [0, 64, 640, -1, -2, -1536])
+def test_kv_stable_after_append_is_bitwise_and_sees_new_token(chunk):
+    """A PDL neo_kv_append of every request's newest token immediately followed
+    by a kv_stable attention call (its first KV tiles read before the wait): the
+    newest token's tile is never read early, so the output is bitwise the output
+    of the plain call and within tolerance of the oracle -- repeated, with the
+    newest slots re-poisoned with NaN before every append."""
+    import torch
+    from paper_2411_01142_b200 import neo
+    ctx_new = [1, 2, 16, 17, 33, 64, 65, 200, 512, 1000, 2049, 4100]
+    case = Case(ctx_new, 32, 8, seed=91)
+    P = case.P
+    k_new = np.stack([case.k_req[b][n - 1] for b, n in enumerate(ctx_new)])
+    v_new = np.stack([case.v_req[b][n - 1] for b, n in enumerate(ctx_new)])
+    kn = torch.from_numpy(k_new.view(np.int16)).cuda().view(torch.bfloat16)
+    vn = torch.from_numpy(v_new.view(np.int16)).cuda().view(torch.bfloat16)
+    ws = neo.make_workspace(case.B, 32, 8, case.max_seq_len, chunk)
+    ref = neo.decode_attn(case.q_dev, case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.max_seq_len,
+                          chunk_tokens=chunk, workspace=ws).clone()
+    got = case.out_f64(ref)
+    for b in range(case.B):
+        assert within_tol(got[b], case.oracle(b))[0]
+    pages = torch.tensor([int(case.table[b, (n - 1) // P]) for b, n in enumerate(ctx_new)], device="cuda")
+    slots = torch.tensor([(n - 1) % P for n in ctx_new], device="cuda")
+    out = torch.empty_like(ref)
+    for rep in range(12):
+        case.k_dev[pages, :, slots] = float("nan")
+        case.v_dev[pages, :, slots] = float("nan")
+        neo.kv_append(case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, kn, vn)
+        neo.decode_attn(case.q_dev, case.k_dev, case.v_dev, case.bt_dev, case.sl_dev, case.max_seq_len, out=out,
+                        chunk_tokens=chunk, workspace=ws, kv_stable=True)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), ref.view(torch.int16)), rep
+
+
+@pytest.mark.parametrize("chunk", [512, -1, -2])
+def test_kv_stable_back_to_back_layers(chunk):
+    """Three layer pools called back to back with kv_stable (the bench's decode
+    step): every output bitwise equals its plain call."""
+    import torch
+    from paper_2411_01142_b200 import neo
+    cases = [Case([5, 300, 1100, 40, 5000, 2048], 64, 8, seed=95 + i, layer=i) for i in range(3)]
+    ws = neo.make_workspace(6, 64, 8, 5000, chunk_tokens=chunk)
+    plain = [c.run(chunk_tokens=chunk, workspace=ws).clone() for c in cases]
+    outs = [torch.empty_like(p) for p in plain]
+    for rep in range(5):
+        for c, o in zip(cases, outs):
+            neo.decode_attn(c.q_dev, c.k_dev, c.v_dev, c.bt_dev, c.sl_dev, c.max_seq_len, out=o, chunk_tokens=chunk,
+                            workspace=ws, kv_stable=True)
+        torch.cuda.synchronize()
+        for p, o in zip(plain, outs):
+            assert torch.equal(p.view(torch.int16), o.view(torch.int16)), rep
+
+
+def test_kv_stable_rejects_unknown_flags():
+    import torch
+    from paper_2411_01142_b200 import neo
+    c = Case([10, 20], 32, 8, seed=97)
+    ws = neo.make_workspace(2, 32, 8, c.max_seq_len, 64)
+    out = torch.empty_like(c.q_dev)
+    rc = neo.lib().neo_decode_attn_ex(c.q_dev.data_ptr(), c.k_dev.data_ptr(), c.v_dev.data_ptr(), c.k_dev.stride(0),
+                                      c.k_dev.shape[0], c.bt_dev.data_ptr(), c.bt_dev.shape[1], c.sl_dev.data_ptr(),
+                                      out.data_ptr(), 2, 32, 8, 128, 16, c.max_seq_len, 0.088, 64, ws.data_ptr(),
+                                      ws.numel(), 2, None)
+    assert rc == neo.NEO_ERR_INVALID_ARG

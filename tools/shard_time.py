@@ -49,7 +49,8 @@ def time_batch(gb, reps, layers, chunk=0):
         for l in range(layers):
             k, v = gb.layer(l)
             neo.decode_attn(gb.q[l % gb.layers], k, v, gb.block_table, gb.seq_lens, gb.max_seq_len, out=out,
-                            chunk_tokens=chunk, workspace=ws, stream=s)
+                            chunk_tokens=chunk, workspace=ws, stream=s,
+                            kv_stable=os.environ.get("NEO_KV_STABLE", "1") != "0")
 
     for _ in range(3):
         if flush is not None:
@@ -93,6 +94,9 @@ def sweep(configs, ns, chunks, reps):
 
 
 def main():
+    # accept --opt=value as well as --opt value
+    sys.argv = [sys.argv[0]] + [x for a in sys.argv[1:] for x in (a.split("=", 1) if a.startswith("--") and "=" in a
+                                                                   else [a])]
     argv = sys.argv[1:]
     args = [a for i, a in enumerate(argv) if not a.startswith("--") and (i == 0 or not argv[i - 1].startswith("--"))]
     reps = 5
@@ -136,7 +140,7 @@ def main():
                 t1 = t_step
             print(json.dumps({"config": name, "n": n, "per_rank_us": [round(x * 1e6, 1) for x in per_rank],
                               "step_us": round(t_step * 1e6, 1), "kv_gbs_total": round(kv_total / t_step / 1e9, 1),
-                              "speedup_vs_1": round(t1 / t_step, 3), "imbalance": round(t_step / np.mean(per_rank), 4),
+                              "speedup_vs_1": round(t1 / t_step, 3) if t1 else None, "imbalance": round(t_step / np.mean(per_rank), 4),
                               "chunk": chunk}), flush=True)
 
 
