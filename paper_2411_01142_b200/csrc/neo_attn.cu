@@ -60,6 +60,7 @@ struct KArgs {
   int32_t l2pro;              // tiles prefetched into L2 in the prologue only (before the PDL wait)
   int32_t first_wave;         // CTAs of the first resident wave (the ones that start during the
                               // previous grid's tail under PDL)
+  int32_t req_major;          // grouped kernel: CTA order (q, b, g) -> (b, q, g)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -793,8 +794,15 @@ __global__ void __launch_bounds__(kGroupWarps * 32, ctas_per_sm<kGroupWarps, kSt
   if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   const int64_t BH = static_cast<int64_t>(a.batch) * a.hkv;
-  const int q = static_cast<int>(blockIdx.x / BH);
-  const int bg = static_cast<int>(blockIdx.x - static_cast<int64_t>(q) * BH);
+  int q = static_cast<int>(blockIdx.x / BH);
+  int bg = static_cast<int>(blockIdx.x - static_cast<int64_t>(q) * BH);
+  if (a.req_major) {   // request-major order: a request's groups adjacent (see launch_decode_attn)
+    const int64_t per_b = static_cast<int64_t>(a.max_chunks) * a.hkv;
+    const int bb = static_cast<int>(blockIdx.x / per_b);
+    const int rem = static_cast<int>(blockIdx.x - bb * per_b);
+    q = rem / a.hkv;
+    bg = bb * a.hkv + (rem - q * a.hkv);
+  }
   const int b = bg / a.hkv;
   const int g = bg - b * a.hkv;
   uint4 qf[4];
@@ -1108,6 +1116,14 @@ neo_status launch_decode_attn(const AttnLaunch& L, const CUtensorMap& tmk, const
   const int64_t units = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
   if (L.grouped) {   // grouped kernel: max_chunks = groups per request, chunk_tiles = group tiles
     a.chunk_tiles = group_tiles_of(L.chunk_tokens);
+    // CTA order: group-major (all first groups, then all second groups, ...) for
+    // up to two groups per request; request-major from three on, so that the
+    // empty CTAs (q >= the request's group count) are spread over the grid instead
+    // of bunched at its end, and a long request's groups start together (same-box
+    // A/B, profiles/r02_group_sweep.md: skewed c2s +6 %, c5 +1 %, c3 +0.5 %; the
+    // two-group c4 shard at N = 8 is 5 % faster group-major).  neo_decode_attn_plan_chunk
+    // replays the same order.
+    a.req_major = L.max_chunks >= 3 ? 1 : 0;
     const int64_t ctas = static_cast<int64_t>(L.max_chunks) * L.batch * L.hkv;
     if (L.k_new) return launch_group<2, true>(a, tmk, tmv, ctas, L.stream);
     return group_stages() == 3 ? launch_group<3, false>(a, tmk, tmv, ctas, L.stream)

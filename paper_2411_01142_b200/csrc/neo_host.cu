@@ -214,7 +214,8 @@ double plan_score(const std::vector<int32_t>& ntiles, int32_t hkv, int32_t chunk
   return makespan > 0 ? static_cast<double>(total) * hkv / makespan : 0.0;
 }
 
-// The grouped kernel in the same replay: CTA (q, b, g) in group-major order,
+// The grouped kernel in the same replay: CTA (q, b, g) in group-major order
+// (request-major from three groups per request on, as launch_decode_attn),
 // 3 CTAs per SM, cost = kPlanGroupOverheadTiles + its per-warp tile range, plus
 // kPlanGroupMultiTiles when the request has several groups (partial + combine).
 // Fitted on the same-box sweep profiles/r01_grouped_sweep.txt (11 shard rows x
@@ -231,19 +232,24 @@ double plan_score_grouped(const std::vector<int32_t>& ntiles, int32_t hkv, int32
     total += t;
   }
   std::vector<double> slot(static_cast<size_t>(sms) * 3, 0.0);
-  for (int32_t q = 0; q < max_groups; ++q) {
-    for (int32_t t : ntiles) {
-      const int32_t ng = (t + group_tiles - 1) / group_tiles;
-      if (q >= ng) continue;
-      const int32_t tg = (t + ng - 1) / ng;
-      const int32_t g0 = q * tg, g1 = std::min(g0 + tg, t);
-      const int32_t tw = (g1 - g0 + 3) / 4;
-      for (int32_t g = 0; g < hkv; ++g) {
-        std::pop_heap(slot.begin(), slot.end(), std::greater<double>());
-        slot.back() += kPlanGroupOverheadTiles + tw + (ng > 1 ? kPlanGroupMultiTiles : 0.0);
-        std::push_heap(slot.begin(), slot.end(), std::greater<double>());
-      }
+  auto dispatch = [&](int32_t t, int32_t q) {
+    const int32_t ng = (t + group_tiles - 1) / group_tiles;
+    if (q >= ng) return;
+    const int32_t tg = (t + ng - 1) / ng;
+    const int32_t g0 = q * tg, g1 = std::min(g0 + tg, t);
+    const int32_t tw = (g1 - g0 + 3) / 4;
+    for (int32_t g = 0; g < hkv; ++g) {
+      std::pop_heap(slot.begin(), slot.end(), std::greater<double>());
+      slot.back() += kPlanGroupOverheadTiles + tw + (ng > 1 ? kPlanGroupMultiTiles : 0.0);
+      std::push_heap(slot.begin(), slot.end(), std::greater<double>());
     }
+  };
+  if (max_groups >= 3) {   // request-major CTA order (launch_decode_attn)
+    for (int32_t t : ntiles)
+      for (int32_t q = 0; q < max_groups; ++q) dispatch(t, q);
+  } else {
+    for (int32_t q = 0; q < max_groups; ++q)
+      for (int32_t t : ntiles) dispatch(t, q);
   }
   const double makespan = *std::max_element(slot.begin(), slot.end());
   return makespan > 0 ? static_cast<double>(total) * hkv / makespan : 0.0;

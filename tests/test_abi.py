@@ -153,15 +153,15 @@ def _plan_replay(ctx, hkv, P, sms=148, o=6.0, og=2.0, om=2.0):
     def grouped_score(gt):
         heap = [0.0] * (sms * 3)
         mg = max([-(-t // gt) for t in nt] + [1])
-        for q in range(mg):
-            for t in nt:
-                ng = -(-t // gt)
-                if q >= ng:
-                    continue
-                tg = -(-t // ng)
-                g0, g1 = q * tg, min(q * tg + tg, t)
-                for _ in range(hkv):
-                    heapq.heapreplace(heap, heap[0] + og + -(-(g1 - g0) // 4) + (om if ng > 1 else 0.0))
+        order = [(q, t) for t in nt for q in range(mg)] if mg >= 3 else [(q, t) for q in range(mg) for t in nt]
+        for q, t in order:
+            ng = -(-t // gt)
+            if q >= ng:
+                continue
+            tg = -(-t // ng)
+            g0, g1 = q * tg, min(q * tg + tg, t)
+            for _ in range(hkv):
+                heapq.heapreplace(heap, heap[0] + og + -(-(g1 - g0) // 4) + (om if ng > 1 else 0.0))
         return sum(nt) * hkv / max(heap)
 
     ctn = cands[-1] // 16
