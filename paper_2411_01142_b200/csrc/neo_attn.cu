@@ -723,7 +723,7 @@ __global__ void __launch_bounds__(kWarps * 32, ctas_per_sm<kWarps, kStages>())
 // partial rows, no counter -- and only requests longer than 4096 tokens write one
 // merged partial per group and run the split-K combine (a7) across groups.
 constexpr int kGroupWarps = 4;
-constexpr int kMaxWarpTiles = kGroupTiles / kGroupWarps;   // per-warp range <= 64 tiles
+static_assert(kGroupTiles / kGroupWarps <= 64, "per-warp range <= 64 tiles (two page-id registers per lane)");
 
 template <int G>
 __device__ __forceinline__ void group_merge(const KArgs& a, const uint8_t* base, int stage_bytes, int warp, int lane,

@@ -169,3 +169,33 @@ def test_prefill_cuda_graph_matches_eager():
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(out.view(torch.int16), eager.view(torch.int16))
+
+
+@pytest.mark.parametrize("n,variant", [(8192, 0), (16384, 0), (8192, ni.VARIANT_PEAKED),
+                                       (16384, ni.VARIANT_PEAKED), (16384, ni.VARIANT_PEAKED | ni.VARIANT_SINK),
+                                       (8192, ni.VARIANT_SINK)])
+def test_prefill_parity_long_prompts_sampled(n, variant):
+    """Whole 8K / 16K prompts (the lengths DESIGN §11 quotes TF/s for), plain,
+    peaked (q x 8: the running max keeps growing, so the lazy O rescale -- only
+    when the max grows by > 2^8 -- fires with P up to 2^8 accumulated) and
+    attention-sink inputs.  The oracle checks sampled rows one by one: each row
+    is the decode definition over its visible prefix (tile edges, page edges,
+    the first and last rows, and random rows)."""
+    import os
+    import oracle
+    import torch
+    case = PrefillCase([n], [n], 32, 8, seed=800 + n // 1024 + variant, variant=variant)
+    out = case.run()
+    got = ni.bf16_bits_to_f64(out.view(torch.int16).cpu().numpy().view(np.uint16))
+    rng = np.random.default_rng(n + variant)
+    rows = sorted(set([0, 1, 15, 16, 17, 127, 128, 129, 255, 256, 1000, 4095, 4096, n // 2, n - 129, n - 128,
+                       n - 2, n - 1] + rng.integers(0, n, 30).tolist()))
+    q = case.qp[rows]
+    ks = [case.k_req[0][:i + 1] for i in rows]
+    vs = [case.v_req[0][:i + 1] for i in rows]
+    ref = oracle.decode_attention_batch(q, ks, vs, np.float32(case.scale), nthreads=os.cpu_count() or 1)
+    worst = 0.0
+    for j, i in enumerate(rows):
+        ok, ratio = within_tol(got[i], ref[j])
+        worst = max(worst, ratio)
+        assert ok, f"n={n} variant={variant} row={i} err/tol={ratio:.3f}"

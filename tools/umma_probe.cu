@@ -2,11 +2,13 @@
 //   mode 0: D[128 x N] = A[128 x 128] . B[N x 128]^T   (A, B K-major SW128)  N in {64, 128, 256}
 //   mode 1: D[128 x 128] = P[128 x 128] . V[128 x 128]  (P K-major, V MN-major SW128)
 //   mode 2: as mode 1 with P in TMEM (written by tcgen05.st, lane = row, column c = pair 2c, 2c+1)
+//   mode 3: as mode 2 with P in fp16 (A format f16) against bf16 V (B format bf16): mixed kind::f16
 // Operands are written into shared memory with TMA's SWIZZLE_128B pattern by
 // plain stores, then a single thread issues the MMAs; the 4 warps read the
 // accumulator back with tcgen05.ld 32x32b and the host compares with fp64.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++17 -o umma_probe tools/umma_probe.cu && ./umma_probe
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -62,7 +64,7 @@ __global__ void probe(const uint16_t* a, const uint16_t* b, float* d, int mode, 
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tm = tbase;
-  if (mode == 2) {  // P rows into TMEM columns 128.. (64 columns of bf16 pairs), one row per lane
+  if (mode >= 2) {  // P rows into TMEM columns 128.. (64 columns of bf16 pairs), one row per lane
     const int row = warp * 32 + (tid & 31);
     for (int c0 = 0; c0 < 64; c0 += 32) {
       uint32_t r[32];
@@ -88,8 +90,9 @@ __global__ void probe(const uint16_t* a, const uint16_t* b, float* d, int mode, 
       } else {
         bd = umma::desc_sw128(B + k * 2048, 16384, 1024);
         id = umma::idesc_bf16_f32(128, 128, false, true);
+        if (mode == 3) id &= ~(7u << 7);   // A format 0 = f16
       }
-      if (mode == 2) umma::mma_bf16_ts(tm, tm + 128 + k * 8, bd, id, k > 0);
+      if (mode >= 2) umma::mma_bf16_ts(tm, tm + 128 + k * 8, bd, id, k > 0);
       else umma::mma_bf16(tm, ad, bd, id, k > 0);
     }
     umma::commit(smem_u32(&bar));
@@ -119,6 +122,8 @@ static uint16_t f2bf(float f) {
   u += 0x7FFF + ((u >> 16) & 1);
   return static_cast<uint16_t>(u >> 16);
 }
+static uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
+static double h2d(uint16_t h) { return static_cast<double>(__half2float(__ushort_as_half(h))); }
 static double bf2d(uint16_t b) {
   uint32_t u = static_cast<uint32_t>(b) << 16;
   float f;
@@ -130,7 +135,9 @@ static int run(int mode, int N) {
   const int rowsB = mode == 0 ? N : 128;
   std::vector<uint16_t> a(128 * 128), b(rowsB * 128);
   srand(1234 + mode * 7 + N);
-  for (auto& x : a) x = f2bf(static_cast<float>(rand()) / RAND_MAX * 2.f - 1.f);
+  for (auto& x : a)
+    x = mode == 3 ? f2h(static_cast<float>(rand()) / RAND_MAX * 256.f)       // P in [0, 256], fp16
+                  : f2bf(static_cast<float>(rand()) / RAND_MAX * 2.f - 1.f);
   for (auto& x : b) x = f2bf(static_cast<float>(rand()) / RAND_MAX * 2.f - 1.f);
   const int ncols = mode == 0 ? N : 128;
   uint16_t *da, *db;
@@ -155,8 +162,10 @@ static int run(int mode, int N) {
     for (int n = 0; n < ncols; ++n) {
       double ref = 0;
       for (int k = 0; k < 128; ++k)
-        ref += mode == 0 ? bf2d(a[m * 128 + k]) * bf2d(b[n * 128 + k]) : bf2d(a[m * 128 + k]) * bf2d(b[k * 128 + n]);
-      worst = std::max(worst, std::fabs(ref - d[m * ncols + n]));
+        ref += mode == 0   ? bf2d(a[m * 128 + k]) * bf2d(b[n * 128 + k])
+               : mode == 3 ? h2d(a[m * 128 + k]) * bf2d(b[k * 128 + n])
+                           : bf2d(a[m * 128 + k]) * bf2d(b[k * 128 + n]);
+      worst = std::max(worst, std::fabs(ref - d[m * ncols + n]) / (mode == 3 ? 256.0 : 1.0));
     }
   printf("mode %d N %3d: max |err| = %.3e  %s\n", mode, N, worst, worst < 1e-3 ? "OK" : "FAIL");
   cudaFree(da);
@@ -172,6 +181,7 @@ int main() {
   bad += run(0, 256);
   bad += run(1, 128);
   bad += run(2, 128);
+  bad += run(3, 128);
   printf(bad ? "PROBE FAILED\n" : "PROBE OK\n");
   return bad;
 }
