@@ -414,7 +414,8 @@ def run_neo(args):
                 "seq_len_mean": round(float(gb.ctx.mean()), 1), "seq_len_min": int(gb.ctx.min()),
                 "seq_len_max": int(gb.ctx.max()),
                 "layers_per_step": L, "distinct_layer_pools": gb.layers,
-                "chunk_tokens": chunk, "chunk_mode": f"grouped (groups <= {4096 // -chunk} tokens)" if chunk < 0 else "split",
+                "chunk_tokens": chunk, "chunk_mode": f"grouped (groups <= {4096 // -chunk if chunk >= -4 else -chunk} tokens)" if chunk < 0
+                else "split",
                 "chunk_plan": "explicit --chunk" if args.chunk else
                 "neo_decode_attn_plan_chunk (host lengths)", "parallelism": par,
                 "l2": (f"inputs {gb.layers * gb.kv_bytes_per_call() / 1e9:.1f} GB of distinct KV cycled per step "
