@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "neo_internal.cuh"
 #include "umma.cuh"
@@ -49,15 +50,24 @@ constexpr int kSmemAlloc = kSmemBytes + 1024;               // + alignment slack
 constexpr uint32_t kTmemCols = 512;             // per tile: S/P (128) + O (128)
 constexpr uint32_t kTileCols = 256;
 constexpr uint32_t kColO = 128;
+// P.V precision (DESIGN "prefill P.V"), a template parameter of the kernel:
+//  - kHiLo = false (prompts of >= kFp16MinQLen tokens): P.V in fp16 -- P (scaled
+//    by 2^7, <= 2^15 under the lazy rescale) rounded to fp16 in TMEM, V converted
+//    bf16 -> fp16 in place in shared memory by the softmax warps at the start of
+//    each step -- one MMA per K16 step; a quarter of the exponentials run on the
+//    FMA pipe (exp2_poly2);
+//  - kHiLo = true (short prompts, where the conversion does not pay): P split
+//    into bf16 hi + lo by truncation, two MMAs per step, V bf16 as loaded.
+constexpr int kFp16MinQLen = 256;
+constexpr int kConvWarps = 0;
 constexpr uint32_t kIdescS = umma::idesc_bf16_f32(kBM, kBN, false, false);
-constexpr uint32_t kIdescO = umma::idesc_bf16_f32(kBM, 128, false, true);
-constexpr int kThreads = 320;
+constexpr int kThreads = 320 + 32 * kConvWarps;
 constexpr int kProducerWarp = 8, kMmaWarp = 9;
 
 // barrier slots
 constexpr int kBarQFull = 0, kBarQEmpty = 1, kBarKFull = 2, kBarVFull = kBarKFull + kStages, kBarKEmpty = kBarVFull + kStages,
               kBarVEmpty = kBarKEmpty + kStages, kBarSFull = kBarVEmpty + kStages, kBarPFull = kBarSFull + kTiles,
-              kBarODone = kBarPFull + kTiles, kNumBars = kBarODone + kTiles;
+              kBarODone = kBarPFull + kTiles, kBarVConv = kBarODone + kTiles, kNumBars = kBarVConv + kStages;
 
 struct PArgs {
   uint16_t* out;
@@ -171,6 +181,43 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// bf16 pair -> fp16 pair (round to nearest even; beyond fp16's range saturates
+// to +-65504 -- DESIGN "prefill P.V": V must lie within fp16's range)
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
+  const float lo = __uint_as_float(w << 16), hi = __uint_as_float(w & 0xffff0000u);
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// exp2 of a packed pair on the FMA pipe: round x to j with the 1.5 * 2^23
+// shifter, 2^(x - j) by a degree-4 Taylor polynomial on [-0.5, 0.5] (relative
+// error <= 4.3e-5, below fp16's 4.9e-4 rounding of P), exponent j added with one
+// integer multiply-add per element.  x is clamped to >= -125 (keeps the biased
+// exponent >= 1; 2^-125 is 0 after the fp16 rounding of P).
+constexpr int kPolyPairs = 1;   // of every 4 column pairs use exp2_poly2 (fp16 path; 2 or 3 measured slower)
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  float2 x = unf2(x2);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const uint64_t magic = f2(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(f2(x.x, x.y), magic);
+  const uint64_t fr = fsub2(f2(x.x, x.y), fsub2(t, magic));
+  uint64_t p = ffma2(fr, f2(0.0096181291f, 0.0096181291f), f2(0.0555041087f, 0.0555041087f));
+  p = ffma2(p, fr, f2(0.2402265070f, 0.2402265070f));
+  p = ffma2(p, fr, f2(0.6931471806f, 0.6931471806f));
+  p = ffma2(p, fr, f2(1.f, 1.f));
+  const float2 tt = unf2(t), pv = unf2(p);
+  const uint32_t r0 = __float_as_uint(tt.x) * (1u << 23) + __float_as_uint(pv.x);
+  const uint32_t r1 = __float_as_uint(tt.y) * (1u << 23) + __float_as_uint(pv.y);
+  return f2(__uint_as_float(r0), __uint_as_float(r1));
+}
+
 // One work item = (request b, kv-head g, CTA tile ct: 2 x 128 rows).
 struct Item {
   int b, g, q0, q_len, ctx, i0, nt0, nt1;
@@ -257,6 +304,7 @@ __device__ __forceinline__ void make_item(const PArgs& a, const Sched& sc, int k
 // Persistent: one CTA per SM walks its snake-ordered share of the items; the
 // TMA ring, the S/P and O TMEM buffers and all barrier phases run on across
 // items, so one item's epilogue overlaps the next item's loads and first S.
+template <bool kHiLo>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill_attn_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
                         const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmo,
@@ -264,6 +312,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t bars[kNumBars];
   __shared__ uint32_t tmem_sh;
+  constexpr float kPBias = kHiLo ? 0.f : 7.f;   // log2 scale of P in the fp16 path
+  constexpr uint32_t kIdescO = kHiLo ? umma::idesc_bf16_f32(kBM, 128, false, true)
+                                     : umma::idesc_f16_f32(kBM, 128, false, true);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = a.G, rows_tok = kBM / G;
   __shared__ Sched sched;
@@ -289,6 +340,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(bar(kBarVFull + s), 1);
       mbar_init(bar(kBarKEmpty + s), 1);
       mbar_init(bar(kBarVEmpty + s), 1);
+      mbar_init(bar(kBarVConv + s), 8);   // 8 softmax-warp arrivals per V tile (fp16 path)
     }
     for (int t = 0; t < kTiles; ++t) {
       mbar_init(bar(kBarSFull + t), 1);
@@ -311,6 +363,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   build_sched(a, rows_tok, sched, nct_tmp);
   const int n_items = sched.pref[a.n_ct_max];
 
+  // registers: the softmax warpgroups hold a 128-column row each; the producer /
+  // MMA / converter warpgroup needs few (setmaxnreg moves them, warpgroup-wide)
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -377,7 +431,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto issue_pv = [&](int t, int st, int ksteps, bool acc0) {
       const uint32_t tp = tmem + t * kTileCols;
       const uint64_t bv = dv0 + static_cast<uint64_t>(st) * kStageDesc;
-      if (ksteps == 8) {
+      if (!kHiLo) {            // fp16 P in columns [0, 64), one MMA per K16 step
+        if (ksteps == 8) {
+          umma::mma_block_pv128_single(tp + kColO, tp, bv, kIdescO, acc0);
+        } else if (lane == 0) {
+          for (int kq = 0; kq < ksteps; ++kq)
+            umma::mma_bf16_ts(tp + kColO, tp + kq * 8, bv + (kq * 2048) / 16, kIdescO, kq > 0 || acc0);
+        }
+      } else if (ksteps == 8) {
         umma::mma_block_pv128(tp + kColO, tp, bv, kIdescO, acc0);
       } else if (lane == 0) {
         for (int kq = 0; kq < ksteps; ++kq) {
@@ -409,11 +470,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++kc;
       for (int j = 0; j < nt; ++j, ++vc) {
         const int st = vc % kStages;
-        mbar_wait(bar(kBarVFull + st), (vc / kStages) & 1);
+        mbar_wait(bar((kHiLo ? kBarVFull : kBarVConv) + st), (vc / kStages) & 1);
         const int nvalid = min(kBN, it.ctx - j * kBN);
         const int ksteps = (nvalid + 15) / 16;
         const uint32_t vb = sb + kOffK + st * kStageBytes + 2 * kKVHalf;
-        if (nvalid & 15) {
+        if (kHiLo && (nvalid & 15)) {
           // rows nvalid .. 16*ksteps-1 hold page-tail slots: zero them (P is 0
           // there, but 0 * NaN would poison O)
           const int nrows = 16 * ksteps - nvalid;
@@ -469,13 +530,61 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl = a.scale_log2;
     uint32_t sc = 0, oc = 0;                         // S tiles and items consumed so far
     uint32_t kbase = 0;                              // K/V tiles of earlier items (ring position)
+    // fp16 path: V tile `vidx` bf16 -> fp16 in place, this warp's 16 of its 128
+    // rows (all 8 softmax warps convert every V tile, in ring order, so no warp
+    // ever waits on a phase two ahead of a stage's current one); rows past the
+    // context zeroed (P = 0 there, but 0 * NaN = NaN)
+    // Exception: the last V tile of an item whose tile 1 stages its output in
+    // that V stage is converted by tile 1's warps alone (32 rows each, double
+    // arrival), so every generic write to the stage before the staging comes
+    // from the staging warp itself (ordered by __syncwarp, not only by the
+    // mbarrier / tcgen05.commit chain, which racecheck does not model).
+    const int wi = t * 4 + quarter;
+    auto convert_v = [&](uint32_t vidx, int left, int row0, int nrow, int arrivals) {
+      const int st = static_cast<int>(vidx % kStages);
+      const int nvalid = min(kBN, left);
+      const int rows = max(0, min(16 * ((nvalid + 15) / 16) - row0, nrow));
+      const uint32_t vb = sb + kOffK + st * kStageBytes + 2 * kKVHalf;
+      mbar_wait(bar(kBarVFull + st), (vidx / kStages) & 1);
+      for (int e0 = 0; e0 < rows * 16; e0 += 128) {
+        uint32_t w[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = e0 + 32 * i + lane;
+          const int row = row0 + (e >> 4);
+          w[i][0] = w[i][1] = w[i][2] = w[i][3] = 0;
+          if (e < rows * 16 && row < nvalid)
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
+                         : "r"(vb + ((e >> 3) & 1) * kKVHalf + row * 128 + (e & 7) * 16));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = e0 + 32 * i + lane;
+          const int row = row0 + (e >> 4);
+          if (e < rows * 16)
+            sts128(vb + ((e >> 3) & 1) * kKVHalf + row * 128 + (e & 7) * 16, bf16x2_to_f16x2(w[i][0]),
+                   bf16x2_to_f16x2(w[i][1]), bf16x2_to_f16x2(w[i][2]), bf16x2_to_f16x2(w[i][3]));
+        }
+      }
+      umma::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (arrivals == 1) mbar_arrive(bar(kBarVConv + st));
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(bar(kBarVConv + st)) : "memory");
+      }
+    };
     for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
       Item it;
       make_item(a, sched, k, rows_tok, it);
       const int my_nt = t ? it.nt1 : it.nt0;
       const int nt_item = max(it.nt0, it.nt1);
       kbase += nt_item;
-      if (my_nt == 0) continue;
+      if (my_nt == 0) {                            // single-tile item: tile 1 only converts
+        if (!kHiLo)
+          for (int j = 0; j < nt_item; ++j) convert_v(kbase - nt_item + j, it.ctx - j * kBN, wi * 16, 16, 1);
+        continue;
+      }
       const int i_row = it.i0 + t * rows_tok + r / G;
       const int pos = it.ctx - it.q_len + min(i_row, it.q_len - 1);
       float m = -INFINITY;
@@ -483,6 +592,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < my_nt; ++j, ++sc) {
         if (quarter == 0 && lane == 0) TRACE(t, sc, 0);
         if (quarter == 0 && lane == 0 && j == 0) TRACE(t, sc, 7);     // item start
+        if (!kHiLo) {
+          if (j == nt_item - 1 && it.staged_v()) {   // tile 1 stages into this V stage
+            if (t == 1) convert_v(kbase - nt_item + j, it.ctx - j * kBN, quarter * 32, 32, 2);
+          } else {
+            convert_v(kbase - nt_item + j, it.ctx - j * kBN, wi * 16, 16, 1);
+          }
+        }
         mbar_wait(bar(kBarSFull + t), sc & 1);
         umma::fence_after_sync();
         if (quarter == 0 && lane == 0) TRACE(t, sc, 1);
@@ -517,9 +633,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           l2 = fmul2(l2, f2(alpha, alpha));
           m = m_new;
         }
-        const uint64_t sl2 = f2(sl, sl), nm2 = f2(-m * sl, -m * sl);
+        const uint64_t sl2 = f2(sl, sl), nm2 = f2(kPBias - m * sl, kPBias - m * sl);
+        if (!kHiLo) {
+          // fp16 P (scaled by 2^kPBias; l carries the same scale, so O / l is
+          // unchanged) into columns [0, 64)
 #pragma unroll
-        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          for (int c0 = 0; c0 < kBN; c0 += 32) {
+            uint32_t hw[16];
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+              const uint64_t xx = ffma2(f2(s[c0 + 2 * w], s[c0 + 2 * w + 1]), sl2, nm2);
+              float p0, p1;
+              if ((w & 3) < kPolyPairs) {      // exp2 on the FMA pipe (MUFU relief)
+                const float2 pp = unf2(exp2_poly2(xx));
+                p0 = pp.x;
+                p1 = pp.y;
+              } else {
+                const float2 x = unf2(xx);
+                p0 = ex2(x.x);
+                p1 = ex2(x.y);
+              }
+              l2 = fadd2(l2, f2(p0, p1));
+              hw[w] = pack_f16(p0, p1);
+            }
+            umma::st16(tS + c0 / 2, hw);
+          }
+        }
+#pragma unroll
+        for (int c0 = 0; c0 < (kHiLo ? kBN : 0); c0 += 32) {
           uint32_t hw[16], lw[16];
 #pragma unroll
           for (int w = 0; w < 16; ++w) {
@@ -569,6 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // tensor store per token and dim-half; rows past q_len are never written.
         const int st_last = static_cast<int>((kbase - 1) % kStages);
         const uint32_t buf = sb + kOffK + st_last * kStageBytes + (t ? 2 * kKVHalf : 0);
+
 #pragma unroll 1
         for (int c0 = 0; c0 < 128; c0 += 32) {
           uint32_t o[32];
@@ -630,6 +772,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       umma::fence_before_sync();
       if (quarter == 0 && lane == 0) TRACE(t, sc - 1, 10);
+      // V tiles of steps this tile does not run (tile 0 when tile 1 sees more keys)
+      if (!kHiLo)
+        for (int j = my_nt; j < nt_item; ++j) convert_v(kbase - nt_item + j, it.ctx - j * kBN, wi * 16, 16, 1);
     }
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // output stores complete
@@ -645,7 +790,10 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   static std::atomic<uint64_t> configured{0};
   static std::atomic<int> sms_of[64];
   neo_status st = once_per_device(configured, [](int dev) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+    cudaError_t e =
+        cudaFuncSetAttribute(prefill_attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(prefill_attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e != cudaSuccess) return cuda_fail(e, "prefill smem attribute");
     int n = 0;
     e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -683,7 +831,13 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, prefill_attn_kernel, tmq, tmk, tmv, tmo, a);
+  // P.V in fp16 for prompt chunks of >= kFp16MinQLen tokens, hi + lo below
+  // (tools/prefill_time.py A/B: 1 x 16384 +18 %, 8 x ~1000 +3-5 %, 64 x 128 -12 %)
+  const char* pv = std::getenv("NEO_PREFILL_PV");   // test / experiment knob: "hilo" | "fp16"
+  const int force = pv ? (pv[0] == 'h' ? 1 : 2) : 0;
+  const bool hilo = force ? force == 1 : L.max_q_len < kFp16MinQLen;
+  if (hilo) cudaLaunchKernelEx(&cfg, prefill_attn_kernel<true>, tmq, tmk, tmv, tmo, a);
+  else cudaLaunchKernelEx(&cfg, prefill_attn_kernel<false>, tmq, tmk, tmv, tmo, a);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? NEO_OK : cuda_fail(e, "prefill attention kernel launch");
 }

@@ -35,6 +35,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, bool a_mn_ma
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// ---- the same with f16 A and B (formats 0)
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N, bool a_mn_major, bool b_mn_major) {
+  return (1u << 4) | (static_cast<uint32_t>(a_mn_major) << 15) | (static_cast<uint32_t>(b_mn_major) << 16) |
+         (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
 // ---- TMEM allocation (one full warp executes these)
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem), "r"(ncols)
@@ -151,6 +157,35 @@ __device__ __forceinline__ void mma_block_pv128(uint32_t tmem_d, uint32_t tmem_a
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l6], b6, %3, pt;\n"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h7], b7, %3, pt;\n"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [l7], b7, %3, pt;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(static_cast<uint32_t>(acc0))
+      : "memory");
+}
+
+// PV block with a single-precision-class P: D (+)= A . B over K = 128 as 8 K16
+// steps, A in TMEM at columns a + 8k, B MN-major SW128 advancing 2 KiB per step.
+__device__ __forceinline__ void mma_block_pv128_single(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                                       uint32_t idesc, bool acc0) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p0, pt;\n"
+      ".reg .b32 h1, h2, h3, h4, h5, h6, h7;\n"
+      ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n"
+      "setp.ne.b32 p0, %4, 0;\n"
+      "setp.eq.b32 pt, 0, 0;\n"
+      "add.u32 h1, %1, 8;\n add.u32 h2, %1, 16;\n add.u32 h3, %1, 24;\n add.u32 h4, %1, 32;\n"
+      "add.u32 h5, %1, 40;\n add.u32 h6, %1, 48;\n add.u32 h7, %1, 56;\n"
+      "add.s64 b1, %2, 128;\n add.s64 b2, %2, 256;\n add.s64 b3, %2, 384;\n add.s64 b4, %2, 512;\n"
+      "add.s64 b5, %2, 640;\n add.s64 b6, %2, 768;\n add.s64 b7, %2, 896;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h1], b1, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h2], b2, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h3], b3, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h4], b4, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h5], b5, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h6], b6, %3, pt;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [h7], b7, %3, pt;\n"
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(static_cast<uint32_t>(acc0))
       : "memory");

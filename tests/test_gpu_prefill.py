@@ -199,3 +199,17 @@ def test_prefill_parity_long_prompts_sampled(n, variant):
         ok, ratio = within_tol(got[i], ref[j])
         worst = max(worst, ratio)
         assert ok, f"n={n} variant={variant} row={i} err/tol={ratio:.3f}"
+
+
+@pytest.mark.parametrize("pv", ["hilo", "fp16"])
+def test_prefill_both_pv_paths(pv, monkeypatch):
+    """Both P.V variants of prefill_attn_kernel (DESIGN "prefill P.V": fp16 P with V
+    converted to fp16 in shared memory, or the bf16 hi + lo split; the launch picks
+    by prompt length, NEO_PREFILL_PV forces one) on short and long prompts, chunks
+    after a prefix, single-tile items and page-size 32 pools, against the oracle."""
+    monkeypatch.setenv("NEO_PREFILL_PV", pv)
+    check_prefill(PrefillCase([1, 7, 64, 65, 128, 300, 1000], [1, 7, 64, 65, 128, 300, 1000], 64, 8,
+                              seed=900), f"{pv} G=8")
+    check_prefill(PrefillCase([500, 200, 129, 1500, 33], [100, 1, 64, 257, 33], 32, 8, P=32, seed=901),
+                  f"{pv} P=32")
+    check_prefill(PrefillCase([77, 2100], [77, 2100], 16, 1, seed=902, variant=ni.VARIANT_PEAKED), f"{pv} G=16")
