@@ -234,8 +234,12 @@ NEO_API neo_status neo_rope_append(void* q_inout, int32_t num_q_heads, const flo
  *   max_q_len  >= every n_q (sizes the grid; rows beyond a request's n_q idle)
  *   G = Hq / Hkv in {1, 2, 4, 8, 16}; D = 128; P a multiple of 16;
  *   batch <= 512 and max_q_len * G <= 262144 (the per-CTA schedule table).
- * Numerics: bf16 x bf16 products exact in fp32 (tcgen05.mma), softmax in fp32
- * (exp2 domain), P applied as bf16 hi + lo, output RNE to bf16.  Deterministic.
+ * Numerics: Q.K^T with bf16 x bf16 products exact in fp32 (tcgen05.mma), softmax
+ * in fp32 (exp2 domain).  P.V: for max_q_len >= 256, P (scaled by 2^7) and V are
+ * rounded to fp16 (RNE; V saturates beyond fp16's range, so V entries must lie
+ * within |v| <= 65504) with fp32 accumulation; shorter calls apply P as bf16
+ * hi + lo against bf16 V (DESIGN "prefill P.V").  Output RNE to bf16.
+ * Deterministic for a fixed call shape.
  * Page-tail slots beyond seq_lens are never read into the result (NaN-safe).
  * Errors: NEO_ERR_INVALID_ARG, NEO_ERR_UNSUPPORTED, NEO_ERR_CUDA; NEO_DEBUG_VALIDATE=1
  * checks the metadata on the host.  batch == 0 or total_tokens == 0 is a no-op. */
