@@ -575,8 +575,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     };
     for (int round = 0, k = first_item(0); k < n_items; k = first_item(++round)) {
+      if (quarter == 0 && lane == 0) TRACE(t, sc, 12);
       Item it;
       make_item(a, sched, k, rows_tok, it);
+      if (quarter == 0 && lane == 0) TRACE(t, sc, 11);
       const int my_nt = t ? it.nt1 : it.nt0;
       const int nt_item = max(it.nt0, it.nt1);
       kbase += nt_item;

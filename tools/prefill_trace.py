@@ -50,4 +50,5 @@ for j in range(64):
         print(f"{j:4d}{mark}{t:4d} | {r[1]-r[0]:8d} {r[2]-r[1]:6d} {r[3]-r[2]:8d} | {r[5]-r[4] if r[4] else 0:8d} "
               f"{r[6]-r[5] if r[6] else 0:6d} | {per:6d}   S@{r[1]-t0}"
               + (f"  epi: P->wait {r[8]-r[3]} o_done {r[9]-r[8]} store {r[10]-r[9]}" if r[8] else "")
-              + (f"  next-wait {tr[t, j + 1, 0] - r[10]}" if r[10] and j + 1 < 64 and tr[t, j + 1, 0] else ""))
+              + (f"  next-wait {tr[t, j + 1, 0] - r[10]} (loop top {tr[t, j + 1, 12] - r[10]}, make_item "
+                 f"{tr[t, j + 1, 11] - tr[t, j + 1, 12]})" if r[10] and j + 1 < 64 and tr[t, j + 1, 0] else ""))
