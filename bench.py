@@ -513,6 +513,7 @@ def run_prefill(args):
             att.append(e[1].elapsed_time(e[2]) / 1e3)
     flops = sum(4.0 * d * hq * n * (n + 1) / 2 for n in lens)
     t_att = float(np.mean(att))
+    long_prompt = run_prefill_long(flush)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):          # ncu --set full of this launch (profiles/r01_ncu_full_prefill.md)
@@ -529,11 +530,49 @@ def run_prefill(args):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "prefill_attn_kernel",
                      "algorithmic_flops_per_launch": flops, "peak_source": src,
                      "algorithmic_bytes_per_launch": T * (2 * hq + 2 * hkv) * d * 2,
-                     "mma_flops_per_algorithmic_flop": 1.5,
-                     "note": "algorithmic = causal 4*D per (q-head, row, visible key); P.V runs as bf16 hi + lo "
-                             "(two MMAs) for the tolerance, so the tensor core executes 1.5x these flops"},
+                     "mma_flops_per_algorithmic_flop": 1.0,
+                     "note": "algorithmic = causal 4*D per (q-head, row, visible key); prompts >= 256 tokens run "
+                             "P.V in fp16 (one MMA per K16 step, DESIGN reading n1), so the tensor core executes "
+                             "these flops (plus the masked halves of diagonal tiles)"},
         "l2": "flushed (512 MB read) before every rep",
+        "long_prompt": long_prompt,
     }
+
+
+def run_prefill_long(flush, n=16384):
+    """The same kernel on one whole 16K-token prompt (the long end of P:364's
+    mixes; the steady state without item switches), for context beside the
+    NEO-sized leg above."""
+    import torch
+
+    from paper_2411_01142_b200 import neo
+    hq, hkv, d, P = 32, 8, 128, 16
+    g = torch.Generator(device="cuda").manual_seed(11)
+    npg = n // P
+    k_pages = torch.randn(npg, hkv, P, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    v_pages = torch.randn(npg, hkv, P, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    bt = torch.randperm(npg, device="cuda", generator=g).to(torch.int32).view(1, npg)
+    sl = torch.tensor([n], dtype=torch.int32, device="cuda")
+    qo = torch.tensor([0, n], dtype=torch.int32, device="cuda")
+    q = torch.randn(n, hq, d, device="cuda", dtype=torch.bfloat16, generator=g)
+    out = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+    ts = []
+    for rep in range(2 + 5):
+        flush.sum()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        neo.prefill_attn(q, k_pages, v_pages, bt, sl, qo, n, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if rep >= 2:
+            ts.append(e0.elapsed_time(e1) / 1e3)
+    t = float(np.mean(ts))
+    flops = 4.0 * d * hq * n * (n + 1) / 2
+    peak, src = tensor_peak()
+    return {"workload": f"1 whole prompt of {n} tokens, LLaMa-3.1-8B layer shapes", "attn_us": round(t * 1e6, 1),
+            "achieved_tflops": round(flops / t / 1e12, 1), "frac": round(flops / t / 1e12 / peak, 4),
+            "peak": peak}
 
 
 def run_cpu_share(args, wl, ctx_all, n_gpu, t_ga):
