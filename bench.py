@@ -195,6 +195,7 @@ def reassemble_heads_into(full_l, gathered_l):
 
 
 READBW_SO = os.path.join(ROOT, "tools", "libreadbw.so")
+COLL_DEV = "cuda"      # device of the bench's own collective tensors ("cpu" under the gloo harness check)
 
 
 def build_readbw():
@@ -252,9 +253,21 @@ def run_neo(args):
     local = int(os.environ.get("LOCAL_RANK", 0))
     if world != args.gpus and rank == 0:
         print(f"note: WORLD_SIZE={world} but --gpus={args.gpus}", file=sys.stderr)
+    # Harness check on ONE GPU (never a measurement): NEO_BENCH_DIST_BACKEND=gloo
+    # with NEO_BENCH_SHARE_GPU=1 runs every rank on cuda:0 with gloo collectives
+    # on host copies, so the multi-rank code paths (rank plans, per-rank timing,
+    # aggregation, head reassembly) execute end to end under torchrun.
+    global COLL_DEV
+    backend = os.environ.get("NEO_BENCH_DIST_BACKEND", "nccl")
+    COLL_DEV = "cpu" if backend == "gloo" else "cuda"
+    if os.environ.get("NEO_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = WORKLOADS[args.config]
     ctx_all, req_ids, kvh, qh, scaling, par = shard_plan(wl, rank, world, args.fraction)
     gb = GpuBatch(wl, ctx=ctx_all, req_ids=req_ids, kv_heads=kvh, q_heads=qh)
@@ -343,7 +356,7 @@ def run_neo(args):
     tok_local = int(gb.ctx.astype(np.int64).sum()) * L * args.steps
     t_max, kv_total, tok_total, per_rank = aggregate_ranks(t_ms / 1e3, kv_local, tok_local, args.steps, world,
                                                            head_sharded=(wl.name == "c4"), dist=dist,
-                                                           device="cuda")
+                                                           device=COLL_DEV)
     value = kv_total / t_max / 1e9
     # The step is exactly L back-to-back launches of the decode kernel and nothing
     # else on the stream (profiles/r02_launches_c3.md: 100 % of the timed
@@ -661,7 +674,12 @@ def run_reassembly(args, gb, L, step, stream, world, dist):
             evs[l].record(stream)
             comm.wait_event(evs[l])
             with torch.cuda.stream(comm):
-                dist.all_gather_into_tensor(gbuf[l].view(-1), outl[l].view(-1))
+                if COLL_DEV == "cpu":      # gloo harness check: host copies
+                    hb = torch.empty(gbuf[l].numel() // 2, dtype=torch.int32)     # (gloo has no 16-bit types)
+                    dist.all_gather_into_tensor(hb, outl[l].view(-1).view(torch.int32).cpu())
+                    gbuf[l].view(-1).view(torch.int32).copy_(hb)
+                else:
+                    dist.all_gather_into_tensor(gbuf[l].view(-1), outl[l].view(-1))
                 reassemble_heads_into(full[l], gbuf[l])
         stream.wait_stream(comm)
 
@@ -675,7 +693,7 @@ def run_reassembly(args, gb, L, step, stream, world, dist):
         step_gather()
     e1.record(stream)
     torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=COLL_DEV)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return {"ms_per_step_with_allgather": round(float(t.item()), 4),
             "allgather_bytes_per_layer_per_rank": int(outl[0].numel() * 2),
@@ -887,8 +905,8 @@ def run_e2e(args, gb, L, chunk, ws, stream, world, dist):
     drain()                                        # every step's outputs are on the host
     e1.record(stream)
     torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
-    kv = torch.tensor([float(gb.kv_bytes_per_call() * L * args.steps)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device=COLL_DEV)
+    kv = torch.tensor([float(gb.kv_bytes_per_call() * L * args.steps)], dtype=torch.float64, device=COLL_DEV)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(kv, op=dist.ReduceOp.SUM)
