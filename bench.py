@@ -527,10 +527,12 @@ def run_prefill(args):
     flops = sum(4.0 * d * hq * n * (n + 1) / 2 for n in lens)
     t_att = float(np.mean(att))
     long_prompt = run_prefill_long(flush)
+    # the launch picks the stream kernel for prompts up to 3072 tokens (neo_prefill.cu kStreamMaxQLen)
+    kernel = "prefill_attn_stream_kernel" if max(lens) <= 3072 else "prefill_attn_kernel"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):          # ncu --set full of this launch (profiles/r01_ncu_full_prefill.md)
-        traffic = json.load(open(tpath)).get("prefill")
+    if os.path.exists(tpath):          # ncu capture of this launch (profiles/r02_ncu_prefill_stream.md)
+        traffic = json.load(open(tpath)).get("prefill_stream" if kernel.endswith("stream_kernel") else "prefill")
     peak, src = tensor_peak()
     achieved = flops / t_att / 1e12
     return {
@@ -540,7 +542,7 @@ def run_prefill(args):
         "attn_us": round(t_att * 1e6, 2), "append_rope_us": round(float(np.mean(app)) * 1e6, 2),
         "gpu_launches": 2 * 10,
         "roofline": {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "prefill_attn_kernel",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kernel,
                      "algorithmic_flops_per_launch": flops, "peak_source": src,
                      "algorithmic_bytes_per_launch": T * (2 * hq + 2 * hkv) * d * 2,
                      "mma_flops_per_algorithmic_flop": 1.0,

@@ -59,6 +59,10 @@ constexpr uint32_t kColO = 128;
 //  - kHiLo = true (short prompts, where the conversion does not pay): P split
 //    into bf16 hi + lo by truncation, two MMAs per step, V bf16 as loaded.
 constexpr int kFp16MinQLen = 256;
+constexpr int kStreamMaxQLen = 3072;             // fp16 path: stream kernel up to here, item-major above
+#ifndef NEO_PF_EXP
+#define NEO_PF_EXP 0   // timing experiments only (results wrong): 1 no V conversion, 2 no softmax math + no conversion, 3 no softmax math
+#endif
 constexpr int kConvWarps = 0;
 constexpr uint32_t kIdescS = umma::idesc_bf16_f32(kBM, kBN, false, false);
 constexpr int kThreads = 320 + 32 * kConvWarps;
@@ -200,6 +204,10 @@ __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
 // error <= 4.3e-5, below fp16's 4.9e-4 rounding of P), exponent j added with one
 // integer multiply-add per element.  x is clamped to >= -125 (keeps the biased
 // exponent >= 1; 2^-125 is 0 after the fp16 rounding of P).
+#ifndef NEO_PF_POLY
+#define NEO_PF_POLY 0   // stream kernel's share (of 4 column pairs) on the FMA pipe: 0 measured best there
+#endif
+constexpr int kPolyPairsStream = NEO_PF_POLY;
 constexpr int kPolyPairs = 1;   // of every 4 column pairs use exp2_poly2 (fp16 path; 2 or 3 measured slower)
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
   float2 x = unf2(x2);
@@ -546,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rows = max(0, min(16 * ((nvalid + 15) / 16) - row0, nrow));
       const uint32_t vb = sb + kOffK + st * kStageBytes + 2 * kKVHalf;
       mbar_wait(bar(kBarVFull + st), (vidx / kStages) & 1);
-      for (int e0 = 0; e0 < rows * 16; e0 += 128) {
+      for (int e0 = 0; e0 < ((NEO_PF_EXP == 1 || NEO_PF_EXP == 2) ? 0 : rows * 16); e0 += 128) {
         uint32_t w[4][4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -614,6 +622,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int c = 0; c < 32; ++c) s[c0 + c] = __uint_as_float(u[c]);
           }
+        }
+        if (NEO_PF_EXP >= 2) {
+          uint32_t hw[16];
+#pragma unroll
+          for (int w = 0; w < 16; ++w) hw[w] = __float_as_uint(s[w] * 0.f);
+#pragma unroll
+          for (int c0 = 0; c0 < kBN; c0 += 32) umma::st16(tS + c0 / 2, hw);
+          l2 = f2(1.f, 1.f);
+          umma::wait_st();
+          umma::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(kBarPFull + t));
+          continue;
         }
         const int lim = pos - j * kBN;               // last visible column of this row in the tile
         if (lim < kBN - 1) {
@@ -785,6 +806,575 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kMmaWarp) umma::tmem_dealloc(tmem, kTmemCols);
 }
 
+
+// ============================================================================
+// Stream kernel (fp16 P.V path, prompts >= kFp16MinQLen tokens).
+//
+// Same math and tile shapes as prefill_attn_kernel<false>, re-organised so an
+// item boundary costs no pipeline drain (the clock64 trace of the item-major
+// kernel showed ~6.5K cycles per boundary on 8 x 1024: epilogue stores 3.3K,
+// item decode 1K, the next item's first S waiting for both tiles' epilogues):
+//   * the MMA warp runs one continuous stream: after the last PV of an item on
+//     tile t it issues the NEXT item's first S on tile t at once (per-tile Q
+//     buffers, loaded by their own warp as soon as the tile's last S of the
+//     previous item completes);
+//   * a dedicated epilogue warpgroup (warps 8-11, one per TMEM lane quarter)
+//     drains O / l of each finished tile, releases the O columns (o_free) and
+//     stores bf16 rows straight to global, off the softmax critical path;
+//   * both tiles of an item run the same number of key tiles (the earlier
+//     tile's extra steps are fully masked and add exact zeros), so the S, P and
+//     V pipelines of the two tiles stay in lock step across items;
+//   * every CTA's item list is decoded once in the prologue into shared memory;
+//   * setmaxnreg: 168 registers for the softmax warpgroups, 96 for the epilogue,
+//     80 for the producer / MMA warpgroup (sum = the 128 x 512 launch pool).
+//   warps 0-3 / 4-7  softmax of tile 0 / 1 (thread = row = TMEM lane)
+//   warps 8-11       V bf16 -> fp16 conversion (32 rows each) and the epilogue
+//   warp 12          K/V TMA producer      warp 13  MMA issuer
+//   warp 14          Q TMA producer        warp 15  idle
+// ============================================================================
+namespace s2 {
+constexpr int kThreads = 512;
+constexpr int kEpiWarp0 = 8, kProdWarp = 12, kMmaWarp = 13, kQWarp = 14;
+constexpr int kBarQFull = 0, kBarQEmpty = 2, kBarKFull = 4, kBarVFull = 6, kBarKEmpty = 8, kBarVEmpty = 10,
+              kBarVConv = 12, kBarSFull = 14, kBarPFull = 16, kBarODone = 18, kBarOFree = 20, kBarLReady = 22,
+              kNumBars = 24;
+constexpr int kMaxCtaItems = 512;   // items decoded in the prologue (later ones decode on the fly)
+}  // namespace s2
+
+
+#ifndef NEO_PF_PINGPONG
+#define NEO_PF_PINGPONG 0   // stream kernel (measured slower, kept for A/B): the two tiles' softmax phases alternate (named barriers 1, 2)
+#endif
+#ifndef NEO_PF_CONV_EPI
+#define NEO_PF_CONV_EPI 0   // stream kernel: 0 = the softmax warps convert V (16 rows each), 1 = the epilogue warps (32 rows)
+#endif
+// V tile vi (ring stage vi % kStages): rows [row0, row0 + NR) bf16 -> fp16 in
+// place once the tile has landed; rows past the context are zeroed (P = 0
+// there, but 0 * NaN = NaN); then one arrival on the conversion barrier.
+template <int NR>
+__device__ __forceinline__ void convert_v_rows(uint32_t sb, uint32_t vfull_bar, uint32_t vconv_bar, uint32_t vi,
+                                               int left, int row0, int lane) {
+  const int st = static_cast<int>(vi % kStages);
+  const int nvalid = min(kBN, left);
+  const int rows = max(0, min(16 * ((nvalid + 15) / 16) - row0, NR));
+  const uint32_t vb = sb + kOffK + st * kStageBytes + 2 * kKVHalf;
+  mbar_wait(vfull_bar + 8u * st, (vi / kStages) & 1);
+  if (NEO_PF_EXP == 1 || NEO_PF_EXP == 2) {
+  } else if (nvalid == kBN) {
+    // full tile: NR rows x 256 B, unconditional 16-byte chunks (a quarter-warp
+    // reads one 128-byte row half: conflict-free)
+#pragma unroll
+    for (int i0 = 0; i0 < NR / 2; i0 += 8) {
+      uint32_t w[8][4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = 32 * (i0 + i) + lane;
+        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
+                     : "r"(vb + ((e >> 3) & 1) * kKVHalf + (row0 + (e >> 4)) * 128 + (e & 7) * 16));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = 32 * (i0 + i) + lane;
+        sts128(vb + ((e >> 3) & 1) * kKVHalf + (row0 + (e >> 4)) * 128 + (e & 7) * 16, bf16x2_to_f16x2(w[i][0]),
+               bf16x2_to_f16x2(w[i][1]), bf16x2_to_f16x2(w[i][2]), bf16x2_to_f16x2(w[i][3]));
+      }
+    }
+  } else {
+    for (int e0 = 0; e0 < rows * 16; e0 += 128) {
+      uint32_t w[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = e0 + 32 * i + lane;
+        const int row = row0 + (e >> 4);
+        w[i][0] = w[i][1] = w[i][2] = w[i][3] = 0;
+        if (e < rows * 16 && row < nvalid)
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
+                       : "r"(vb + ((e >> 3) & 1) * kKVHalf + row * 128 + (e & 7) * 16));
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int e = e0 + 32 * i + lane;
+        const int row = row0 + (e >> 4);
+        if (e < rows * 16)
+          sts128(vb + ((e >> 3) & 1) * kKVHalf + row * 128 + (e & 7) * 16, bf16x2_to_f16x2(w[i][0]),
+                 bf16x2_to_f16x2(w[i][1]), bf16x2_to_f16x2(w[i][2]), bf16x2_to_f16x2(w[i][3]));
+      }
+    }
+  }
+  umma::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(vconv_bar + 8u * st);
+}
+
+// packed (b, g, ct) of one item: b < 1024, g < 64, ct < 1024
+__device__ __forceinline__ uint32_t pack_item(const Item& it, int ct) {
+  return static_cast<uint32_t>(it.b) | (static_cast<uint32_t>(it.g) << 10) | (static_cast<uint32_t>(ct) << 16);
+}
+__device__ __forceinline__ void unpack_item(const PArgs& a, const Sched& sc, uint32_t w, int rows_tok, Item& it) {
+  it.b = static_cast<int>(w & 1023u);
+  it.g = static_cast<int>((w >> 10) & 63u);
+  const int ct = static_cast<int>(w >> 16);
+  it.q0 = sc.q_off[it.b];
+  it.q_len = sc.q_off[it.b + 1] - it.q0;
+  it.ctx = sc.ctx[it.b];
+  it.i0 = ct * kTiles * rows_tok;
+  const int f0 = it.i0, f1 = it.i0 + rows_tok;
+  it.nt0 = (it.ctx - it.q_len + min(f0 + rows_tok, it.q_len) - 1) / kBN + 1;
+  it.nt1 = f1 < it.q_len ? (it.ctx - it.q_len + min(f1 + rows_tok, it.q_len) - 1) / kBN + 1 : 0;
+}
+
+__global__ void __launch_bounds__(s2::kThreads, 1)
+    prefill_attn_stream_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
+                               const __grid_constant__ CUtensorMap tmv, const PArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t bars[s2::kNumBars];
+  __shared__ uint32_t tmem_sh;
+  __shared__ Sched sched;
+  __shared__ int nct_tmp[kMaxSchedBatch];
+  __shared__ uint32_t citems[s2::kMaxCtaItems];
+  __shared__ float lbuf[kTiles][2][kBM];          // row sums handed to the epilogue (double-buffered by item)
+  constexpr float kPBias = 7.f;                    // log2 scale of P (fp16 path, DESIGN "prefill P.V")
+  constexpr uint32_t kIdescO = umma::idesc_f16_f32(kBM, 128, false, true);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.G, rows_tok = kBM / G;
+  const int cta = static_cast<int>(blockIdx.x), grid = static_cast<int>(gridDim.x);
+  auto first_item = [&](int round) { return round * grid + ((round & 1) ? grid - 1 - cta : cta); };
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t bar0 = smem_u32(bars);
+  auto bar = [bar0](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
+
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < kTiles; ++t) {
+      mbar_init(bar(s2::kBarQFull + t), 1);
+      mbar_init(bar(s2::kBarQEmpty + t), 1);
+      mbar_init(bar(s2::kBarSFull + t), 1);
+      mbar_init(bar(s2::kBarPFull + t), 4);
+      mbar_init(bar(s2::kBarODone + t), 1);
+      mbar_init(bar(s2::kBarOFree + t), 4);
+      mbar_init(bar(s2::kBarLReady + t), 4);
+    }
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(bar(s2::kBarKFull + s), 1);
+      mbar_init(bar(s2::kBarVFull + s), 1);
+      mbar_init(bar(s2::kBarKEmpty + s), 1);
+      mbar_init(bar(s2::kBarVEmpty + s), 1);
+      mbar_init(bar(s2::kBarVConv + s), NEO_PF_CONV_EPI ? 4 : 8);   // converting warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == s2::kMmaWarp) {
+    umma::tmem_alloc(smem_u32(&tmem_sh), kTmemCols);
+    umma::tmem_relinquish();
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // metadata and q may come from the previous kernel
+  build_sched(a, rows_tok, sched, nct_tmp);
+  const int n_items = sched.pref[a.n_ct_max];
+  int n_rounds = 0;                                   // items of this CTA
+  while (first_item(n_rounds) < n_items) ++n_rounds;
+  for (int r = threadIdx.x; r < min(n_rounds, s2::kMaxCtaItems); r += blockDim.x) {
+    Item it;
+    const int k = first_item(r);
+    make_item(a, sched, k, rows_tok, it);
+    int lo = 0, hi = a.n_ct_max - 1;                  // the item's level -> ct
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (sched.pref[mid] <= k) lo = mid;
+      else hi = mid - 1;
+    }
+    citems[r] = pack_item(it, a.n_ct_max - 1 - lo);
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tmem = tmem_sh;
+  auto get_item = [&](int r, Item& it) {
+    if (r < s2::kMaxCtaItems) unpack_item(a, sched, citems[r], rows_tok, it);
+    else make_item(a, sched, first_item(r), rows_tok, it);
+  };
+  // both tiles of an item run nt key tiles (tile 0's extra ones fully masked)
+  auto steps_of = [](const Item& it) { return it.nt0 > it.nt1 ? it.nt0 : it.nt1; };
+
+  if (warp >= s2::kEpiWarp0 + 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
+    if (warp == s2::kProdWarp) {
+      // ---------------------------------------------------------- K/V producer
+      if (lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmk)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmv)) : "memory");
+      }
+      uint32_t kc = 0;
+      for (int r = 0; r < n_rounds; ++r) {
+        Item it;
+        get_item(r, it);
+        const int nt = steps_of(it);
+        const int32_t* bt = a.block_table + static_cast<int64_t>(it.b) * a.max_blocks;
+        for (int j = 0; j < nt; ++j, ++kc) {
+          const int st = kc % kStages;
+          const int kv0 = j * kBN;
+          const int groups = min(kBN / 16, (it.ctx - kv0 + 15) / 16);
+          int page = 0, slot = 0;
+          if (lane < groups) {
+            const int t = kv0 + 16 * lane;
+            page = bt[t / a.page_size];
+            slot = t % a.page_size;
+          }
+          const uint32_t dk = sb + kOffK + st * kStageBytes, dv = dk + 2 * kKVHalf;
+          const uint32_t bytes = static_cast<uint32_t>(groups) * 2 * 2048;
+          if (kc >= kStages) mbar_wait(bar(s2::kBarKEmpty + st), ((kc / kStages) - 1) & 1);
+          if (lane == 0) mbar_expect_tx(bar(s2::kBarKFull + st), bytes);
+          __syncwarp();
+          if (lane < groups)
+            for (int h = 0; h < 2; ++h)
+              tma_load_5d(dk + h * kKVHalf + lane * 2048, &tmk, 0, slot, h, it.g, page, bar(s2::kBarKFull + st));
+          if (kc >= kStages) mbar_wait(bar(s2::kBarVEmpty + st), ((kc / kStages) - 1) & 1);
+          if (lane == 0) mbar_expect_tx(bar(s2::kBarVFull + st), bytes);
+          __syncwarp();
+          if (lane < groups)
+            for (int h = 0; h < 2; ++h)
+              tma_load_5d(dv + h * kKVHalf + lane * 2048, &tmv, 0, slot, h, it.g, page, bar(s2::kBarVFull + st));
+        }
+      }
+    } else if (warp == s2::kQWarp) {
+      // ---------------------------------------------------------- Q producer
+      if (lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
+        for (int r = 0; r < n_rounds; ++r) {
+          Item it;
+          get_item(r, it);
+          for (int t = 0; t < kTiles; ++t) {
+            if (r > 0) mbar_wait(bar(s2::kBarQEmpty + t), (r - 1) & 1);
+            mbar_expect_tx(bar(s2::kBarQFull + t), 2 * kQHalf);
+            for (int h = 0; h < 2; ++h)   // rows past the tensor's tokens are zero-filled by TMA
+              tma_load_4d(sb + (t * 2 + h) * kQHalf, &tmq, 0, it.g * G, it.q0 + it.i0 + t * rows_tok, h,
+                          bar(s2::kBarQFull + t));
+          }
+        }
+      }
+    } else if (warp == s2::kMmaWarp) {
+      // ---------------------------------------------------------- MMA issuer
+      const uint64_t dq0 = umma::desc_sw128(sb, 16, 1024), dq1 = umma::desc_sw128(sb + 2 * kQHalf, 16, 1024);
+      const uint64_t dk0 = umma::desc_sw128(sb + kOffK, 16, 1024);
+      const uint64_t dv0 = umma::desc_sw128(sb + kOffK + 2 * kKVHalf, kKVHalf, 1024);
+      constexpr uint64_t kStageDesc = kStageBytes / 16;
+      auto issue_s = [&](int t, int st) {
+        umma::mma_block_k128<kQHalf, kKVHalf>(tmem + t * kTileCols, t ? dq1 : dq0,
+                                              dk0 + static_cast<uint64_t>(st) * kStageDesc, kIdescS);
+      };
+      auto issue_pv = [&](int t, int st, int ksteps, bool acc0) {
+        const uint32_t tp = tmem + t * kTileCols;
+        const uint64_t bv = dv0 + static_cast<uint64_t>(st) * kStageDesc;
+        if (ksteps == 8) {
+          umma::mma_block_pv128_single(tp + kColO, tp, bv, kIdescO, acc0);
+        } else if (lane == 0) {
+          for (int kq = 0; kq < ksteps; ++kq)
+            umma::mma_bf16_ts(tp + kColO, tp + kq * 8, bv + (kq * 2048) / 16, kIdescO, kq > 0 || acc0);
+        }
+        __syncwarp();
+      };
+      if (n_rounds > 0) {
+        uint32_t kc = 0, vc = 0, pc0 = 0, pc1 = 0;
+        Item cur;
+        get_item(0, cur);
+        int nt = steps_of(cur);
+        // the first item's first S on both tiles
+        mbar_wait(bar(s2::kBarKFull), 0);
+        for (int t = 0; t < kTiles; ++t) {
+          mbar_wait(bar(s2::kBarQFull + t), 0);
+          umma::fence_after_sync();
+          issue_s(t, 0);
+          umma::commit_elect(bar(s2::kBarSFull + t));
+          if (nt == 1) umma::commit_elect(bar(s2::kBarQEmpty + t));
+        }
+        umma::commit_elect(bar(s2::kBarKEmpty));
+        __syncwarp();
+        kc = 1;
+        for (int r = 0; r < n_rounds; ++r) {
+          Item nxt;
+          const bool has_next = r + 1 < n_rounds;
+          int nt_next = 0;
+          if (has_next) {
+            get_item(r + 1, nxt);
+            nt_next = steps_of(nxt);
+          }
+          for (int j = 0; j < nt; ++j, ++vc) {
+            const int st = vc % kStages;
+            const int nvalid = min(kBN, cur.ctx - j * kBN);
+            const int ksteps = (nvalid + 15) / 16;
+            const bool next_s = j + 1 < nt || has_next;   // an S follows this step's PVs
+            const bool next_first = j + 1 == nt;          // ... and it is the next item's first
+            // the S that follows is the last S of its item on the tile
+            const bool next_last = next_first ? nt_next == 1 : j + 2 == nt;
+            mbar_wait(bar(s2::kBarVConv + st), (vc / kStages) & 1);
+            if (next_s) mbar_wait(bar(s2::kBarKFull + kc % kStages), (kc / kStages) & 1);
+#pragma unroll
+            for (int t = 0; t < kTiles; ++t) {
+              if (lane == 0) TRACE(t, t ? pc1 : pc0, 4);
+              mbar_wait(bar(s2::kBarPFull + t), (t ? pc1 : pc0) & 1);
+              if (lane == 0) TRACE(t, t ? pc1 : pc0, 5);
+              if (t) ++pc1;
+              else ++pc0;
+              if (j == 0 && r > 0) mbar_wait(bar(s2::kBarOFree + t), (r - 1) & 1);   // epilogue read O
+              umma::fence_after_sync();
+              issue_pv(t, st, ksteps, j > 0);
+              if (t == kTiles - 1) umma::commit_elect(bar(s2::kBarVEmpty + st));
+              if (j == nt - 1) umma::commit_elect(bar(s2::kBarODone + t));
+              if (next_s) {
+                if (next_first) {
+                  mbar_wait(bar(s2::kBarQFull + t), (r + 1) & 1);
+                  umma::fence_after_sync();
+                }
+                issue_s(t, kc % kStages);
+                umma::commit_elect(bar(s2::kBarSFull + t));
+                if (next_last) umma::commit_elect(bar(s2::kBarQEmpty + t));
+                if (t == kTiles - 1) umma::commit_elect(bar(s2::kBarKEmpty + kc % kStages));
+              }
+              if (lane == 0) TRACE(t, (t ? pc1 : pc0) - 1, 6);
+              __syncwarp();
+            }
+            if (next_s) ++kc;
+          }
+          if (has_next) {
+            cur = nxt;
+            nt = nt_next;
+          }
+        }
+      }
+    }
+  } else if (warp >= s2::kEpiWarp0) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
+    // ------------------------------------------------- epilogue + V conversion
+    // One warp per TMEM lane quarter.  In ring order it converts its 32 rows of
+    // every V tile bf16 -> fp16 in place (rows past the context zeroed: P = 0
+    // there, but 0 * NaN = NaN) and, after the next item's first V tile, drains
+    // the previous item's O / l of both tiles to global.
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const int row0 = quarter * 32;
+    // O / l of item rd, tile t -> bf16 rows of `out`; o_free once O is read
+    auto epilogue = [&](int rd, const Item& it, int t, int trace_row) {
+      const uint32_t tO = tmem + t * kTileCols + kColO + (static_cast<uint32_t>(quarter * 32) << 16);
+      if (quarter == 0 && lane == 0) TRACE(t, trace_row, 8);
+      mbar_wait(bar(s2::kBarODone + t), rd & 1);
+      mbar_wait(bar(s2::kBarLReady + t), rd & 1);
+      umma::fence_after_sync();
+      if (quarter == 0 && lane == 0) TRACE(t, trace_row, 9);
+      const float inv_l = 1.f / lbuf[t][rd & 1][r];
+      const int tok = it.i0 + t * rows_tok + r / G;
+      uint16_t* orow = a.out + (static_cast<int64_t>(it.q0 + min(tok, it.q_len - 1)) * a.hq + it.g * G + r % G) * 128;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        uint32_t o[32];
+        umma::ld32(tO + c0, o);
+        umma::wait_ld();
+        if (c0 == 96) {                              // O read: the tile's next first PV may overwrite it
+          umma::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(s2::kBarOFree + t));
+        }
+        if (tok < it.q_len) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 16) {
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              w[e] = pack_bf16(__uint_as_float(o[c + 2 * e]) * inv_l, __uint_as_float(o[c + 2 * e + 1]) * inv_l);
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c0 + c), "r"(w[0]),
+                         "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                         : "memory");
+          }
+        }
+      }
+      if (quarter == 0 && lane == 0) TRACE(t, trace_row, 10);
+    };
+    uint32_t vidx = 0;
+    int steps_done = 0;                              // trace row of the previous item's last step
+    Item prev;
+    for (int rd = 0; rd < n_rounds; ++rd) {
+      Item it;
+      get_item(rd, it);
+      const int nt = steps_of(it);
+      for (int j = 0; j < nt; ++j) {
+        if (NEO_PF_CONV_EPI)
+          convert_v_rows<32>(sb, bar(s2::kBarVFull), bar(s2::kBarVConv), vidx++, it.ctx - j * kBN, row0, lane);
+        if (j == 0 && rd > 0)
+          for (int t = 0; t < kTiles; ++t) epilogue(rd - 1, prev, t, steps_done - 1);
+      }
+      steps_done += nt;
+      prev = it;
+    }
+    if (n_rounds > 0)
+      for (int t = 0; t < kTiles; ++t) epilogue(n_rounds - 1, prev, t, steps_done - 1);
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory");
+    // ------------------------------------------------------------ softmax warps
+    const int t = warp >> 2, quarter = warp & 3;
+    const int r = quarter * 32 + lane;               // row == TMEM lane
+    const uint32_t tS = tmem + t * kTileCols + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t tO = tS + kColO;
+    const float sl = a.scale_log2;
+    uint32_t sc = 0, vidx = 0;
+    // ping-pong: the two tiles' softmax phases alternate (named barrier 1 + t =
+    // "tile t's turn", granted by the other warpgroup), so each runs with the
+    // SMSPs' MUFU pipes to itself while the tensor core works on the other tile
+    int total_steps = 0;
+    if (NEO_PF_PINGPONG) {
+      for (int rd = 0; rd < n_rounds; ++rd) {
+        Item it;
+        get_item(rd, it);
+        total_steps += steps_of(it);
+      }
+      if (t == 1 && total_steps > 0) asm volatile("bar.arrive 1, 256;" ::: "memory");   // tile 0 goes first
+    }
+    for (int rd = 0; rd < n_rounds; ++rd) {
+      Item it;
+      get_item(rd, it);
+      const int nt = steps_of(it);
+      const int i_row = it.i0 + t * rows_tok + r / G;
+      const int pos = it.ctx - it.q_len + min(i_row, it.q_len - 1);
+      float m = -INFINITY;
+      uint64_t l2 = f2(0.f, 0.f);
+      for (int j = 0; j < nt; ++j, ++sc) {
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 0);
+        if (quarter == 0 && lane == 0 && j == 0) TRACE(t, sc, 7);
+        if (!NEO_PF_CONV_EPI)
+          convert_v_rows<16>(sb, bar(s2::kBarVFull), bar(s2::kBarVConv), vidx++, it.ctx - j * kBN, (t * 4 + quarter) * 16,
+                             lane);
+        mbar_wait(bar(s2::kBarSFull + t), sc & 1);
+        if (NEO_PF_PINGPONG) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
+        umma::fence_after_sync();
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 1);
+        float s[kBN];
+        {
+          uint32_t u[4][32];
+#pragma unroll
+          for (int c0 = 0; c0 < kBN; c0 += 32) umma::ld32(tS + c0, u[c0 / 32]);
+          umma::wait_ld();
+#pragma unroll
+          for (int c = 0; c < kBN; ++c) s[c] = __uint_as_float(u[c / 32][c % 32]);
+        }
+        if (NEO_PF_EXP >= 2) {
+          uint32_t hw[16];
+#pragma unroll
+          for (int w = 0; w < 16; ++w) hw[w] = __float_as_uint(s[w] * 0.f);
+#pragma unroll
+          for (int c0 = 0; c0 < kBN; c0 += 32) umma::st16(tS + c0 / 2, hw);
+          l2 = f2(1.f, 1.f);
+          umma::wait_st();
+          umma::fence_before_sync();
+          if (NEO_PF_PINGPONG && !(t == 1 && static_cast<int>(sc) == total_steps - 1))
+            asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(s2::kBarPFull + t));
+          continue;
+        }
+        // causal mask on diagonal tiles, by 32-column chunk with warp-uniform
+        // classification: chunks visible to every row of the warp are untouched,
+        // chunks past every row's limit skip the max and the exponentials (P = 0)
+        const int lim = pos - j * kBN;               // last visible column of this row in the tile
+        const bool any_mask = __any_sync(0xffffffffu, lim < kBN - 1);
+        const int lo_lim = any_mask ? __reduce_min_sync(0xffffffffu, lim) : kBN;
+        const int hi_lim = any_mask ? __reduce_max_sync(0xffffffffu, lim) : kBN;
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          if (c0 + 31 <= lo_lim || c0 > hi_lim) continue;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) s[c0 + c] = c0 + c > lim ? -INFINITY : s[c0 + c];
+        }
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 2);
+        // row max: four independent chains per chunk
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          if (c0 > hi_lim) continue;
+#pragma unroll
+          for (int c = 0; c < 32; c += 8)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mq[q] = fmaxf(mq[q], fmaxf(s[c0 + c + 2 * q], s[c0 + c + 2 * q + 1]));
+        }
+        const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+        const float m_new = fmaxf(m, mx);            // j > 0 on tile 0's masked extra steps: m_new = m
+        bool resc = false;
+        float alpha = 1.f;
+        if (j == 0) {
+          m = m_new;
+        } else if ((m_new - m) * sl > 8.f) {
+          resc = true;
+          alpha = ex2((m - m_new) * sl);
+          l2 = fmul2(l2, f2(alpha, alpha));
+          m = m_new;
+        }
+        const uint64_t sl2 = f2(sl, sl), nm2 = f2(kPBias - m * sl, kPBias - m * sl);
+        uint64_t la = f2(0.f, 0.f), lb = f2(0.f, 0.f);   // two row-sum chains
+        // all 128 exponentials first, the four TMEM stores after: no
+        // memory-clobbering asm inside the loop, so the scheduler can overlap
+        // one chunk's MUFU latency with the next chunk's work
+        uint32_t hw[64];
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) {
+          if (c0 > hi_lim) {
+#pragma unroll
+            for (int w = 0; w < 16; ++w) hw[c0 / 2 + w] = 0u;
+          } else {
+#pragma unroll
+            for (int w = 0; w < 16; ++w) {
+              const uint64_t xx = ffma2(f2(s[c0 + 2 * w], s[c0 + 2 * w + 1]), sl2, nm2);
+              float p0, p1;
+              if ((w & 3) < kPolyPairsStream) {
+                const float2 pp = unf2(exp2_poly2(xx));
+                p0 = pp.x;
+                p1 = pp.y;
+              } else {
+                const float2 x = unf2(xx);
+                p0 = ex2(x.x);
+                p1 = ex2(x.y);
+              }
+              if (w & 1) lb = fadd2(lb, f2(p0, p1));
+              else la = fadd2(la, f2(p0, p1));
+              hw[c0 / 2 + w] = pack_f16(p0, p1);
+            }
+          }
+        }
+#pragma unroll
+        for (int c0 = 0; c0 < kBN; c0 += 32) umma::st16(tS + c0 / 2, *reinterpret_cast<const uint32_t(*)[16]>(&hw[c0 / 2]));
+        l2 = fadd2(l2, fadd2(la, lb));
+        if (__any_sync(0xffffffffu, resc)) {
+          // PV_{j-1} is complete (the S_j commit covers it): scale O in place
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 32) {
+            uint32_t o[32];
+            umma::ld32(tO + c0, o);
+            umma::wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+            umma::st32(tO + c0, o);
+          }
+        }
+        umma::wait_st();
+        umma::fence_before_sync();
+        if (NEO_PF_PINGPONG && !(t == 1 && static_cast<int>(sc) == total_steps - 1))
+          asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");   // the other tile's turn
+        __syncwarp();
+        if (quarter == 0 && lane == 0) TRACE(t, sc, 3);
+        if (lane == 0) mbar_arrive(bar(s2::kBarPFull + t));
+      }
+      // row sum to the epilogue (its O wait is on o_done, committed after the
+      // last PV, which follows this item's last p_full)
+      const float2 lp = unf2(l2);
+      lbuf[t][rd & 1][r] = lp.x + lp.y;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(s2::kBarLReady + t));
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == s2::kMmaWarp) umma::tmem_dealloc(tmem, kTmemCols);
+}
+
 }  // namespace
 
 neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, const CUtensorMap& tmk,
@@ -796,6 +1386,8 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
         cudaFuncSetAttribute(prefill_attn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(prefill_attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(prefill_attn_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e != cudaSuccess) return cuda_fail(e, "prefill smem attribute");
     int n = 0;
     e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -838,8 +1430,22 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   const char* pv = std::getenv("NEO_PREFILL_PV");   // test / experiment knob: "hilo" | "fp16"
   const int force = pv ? (pv[0] == 'h' ? 1 : 2) : 0;
   const bool hilo = force ? force == 1 : L.max_q_len < kFp16MinQLen;
-  if (hilo) cudaLaunchKernelEx(&cfg, prefill_attn_kernel<true>, tmq, tmk, tmv, tmo, a);
-  else cudaLaunchKernelEx(&cfg, prefill_attn_kernel<false>, tmq, tmk, tmv, tmo, a);
+  // fp16 path: the stream kernel for prompts up to kStreamMaxQLen tokens (hkv <= 64
+  // for its packed item list), the item-major kernel above; NEO_PREFILL_KERNEL=
+  // item|stream forces one (tests run both)
+  const char* kn = std::getenv("NEO_PREFILL_KERNEL");
+  // (same-box A/B, tools/prefill_time.py: the stream kernel wins up to 2048-token
+  // prompts -- 8 x 1024 -6 %, 16 x 512 -11 %, ragged 8 x ~1000 -6..9 % -- and
+  // loses 2-5 % from 4096 on, where item boundaries are rare)
+  const bool stream = !hilo && L.hkv <= 64 && (kn ? kn[0] == 's' : L.max_q_len <= kStreamMaxQLen);
+  if (stream) {
+    cfg.blockDim = dim3(s2::kThreads);
+    cudaLaunchKernelEx(&cfg, prefill_attn_stream_kernel, tmq, tmk, tmv, a);
+  } else if (hilo) {
+    cudaLaunchKernelEx(&cfg, prefill_attn_kernel<true>, tmq, tmk, tmv, tmo, a);
+  } else {
+    cudaLaunchKernelEx(&cfg, prefill_attn_kernel<false>, tmq, tmk, tmv, tmo, a);
+  }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? NEO_OK : cuda_fail(e, "prefill attention kernel launch");
 }

@@ -201,13 +201,15 @@ def test_prefill_parity_long_prompts_sampled(n, variant):
         assert ok, f"n={n} variant={variant} row={i} err/tol={ratio:.3f}"
 
 
-@pytest.mark.parametrize("pv", ["hilo", "fp16"])
-def test_prefill_both_pv_paths(pv, monkeypatch):
-    """Both P.V variants of prefill_attn_kernel (DESIGN "prefill P.V": fp16 P with V
-    converted to fp16 in shared memory, or the bf16 hi + lo split; the launch picks
-    by prompt length, NEO_PREFILL_PV forces one) on short and long prompts, chunks
-    after a prefix, single-tile items and page-size 32 pools, against the oracle."""
+@pytest.mark.parametrize("pv,kernel", [("hilo", "item"), ("fp16", "item"), ("fp16", "stream")])
+def test_prefill_both_pv_paths(pv, kernel, monkeypatch):
+    """Every prefill kernel variant (DESIGN "prefill P.V": fp16 P with V converted
+    to fp16 in shared memory -- item-major or stream kernel -- or the bf16 hi + lo
+    split; the launch picks by prompt length, NEO_PREFILL_PV / NEO_PREFILL_KERNEL
+    force one) on short and long prompts, chunks after a prefix, single-tile items
+    and page-size 32 pools, against the oracle."""
     monkeypatch.setenv("NEO_PREFILL_PV", pv)
+    monkeypatch.setenv("NEO_PREFILL_KERNEL", kernel)
     check_prefill(PrefillCase([1, 7, 64, 65, 128, 300, 1000], [1, 7, 64, 65, 128, 300, 1000], 64, 8,
                               seed=900), f"{pv} G=8")
     check_prefill(PrefillCase([500, 200, 129, 1500, 33], [100, 1, 64, 257, 33], 32, 8, P=32, seed=901),
