@@ -1245,7 +1245,6 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
           convert_v_rows<16>(sb, bar(s2::kBarVFull), bar(s2::kBarVConv), vidx++, it.ctx - j * kBN, (t * 4 + quarter) * 16,
                              lane);
         mbar_wait(bar(s2::kBarSFull + t), sc & 1);
-        if (NEO_PF_PINGPONG) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
         umma::fence_after_sync();
         if (quarter == 0 && lane == 0) TRACE(t, sc, 1);
         float s[kBN];
@@ -1258,6 +1257,7 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
           for (int c = 0; c < kBN; ++c) s[c] = __uint_as_float(u[c / 32][c % 32]);
         }
         if (NEO_PF_EXP >= 2) {
+          if (NEO_PF_PINGPONG) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
           uint32_t hw[16];
 #pragma unroll
           for (int w = 0; w < 16; ++w) hw[w] = __float_as_uint(s[w] * 0.f);
@@ -1285,6 +1285,8 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
 #pragma unroll
           for (int c = 0; c < 32; ++c) s[c0 + c] = c0 + c > lim ? -INFINITY : s[c0 + c];
         }
+        // ping-pong turn: the MUFU-heavy max / exp / P phase (S already in registers)
+        if (NEO_PF_PINGPONG) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
         if (quarter == 0 && lane == 0) TRACE(t, sc, 2);
         // row max: four independent chains per chunk
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};

@@ -6,6 +6,9 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_2411_01142_b200/csrc/umma.cuh"
+#ifndef SPIN
+#define SPIN 0   // 1: one extra warp per SMSP spins in mbarrier.try_wait while the softmax warps run
+#endif
 #ifndef TM
 #define TM 0   // 1: S from TMEM (4 x ld32, one wait) and P to TMEM (4 x st16, wait) every step, as the kernel
 #endif
@@ -43,7 +46,11 @@ template <int kVariant>
 #ifndef LB
 #define LB 256
 #endif
-__global__ void __launch_bounds__(LB, 1) k(const float* in, uint32_t* out, long long* cyc, int steps) {
+__global__ void __launch_bounds__(LB, 1) k(const float* in, uint32_t* out, long long* cyc, int steps, int nsoft) {
+  __shared__ __align__(8) uint64_t done_bar;
+  if (threadIdx.x == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&done_bar))));
+  __syncthreads();
+  const uint32_t db = static_cast<uint32_t>(__cvta_generic_to_shared(&done_bar));
   float s[128];
 #pragma unroll
   for (int c = 0; c < 128; ++c) s[c] = in[(threadIdx.x * 7 + c) & 1023];
@@ -62,6 +69,13 @@ __global__ void __launch_bounds__(LB, 1) k(const float* in, uint32_t* out, long 
   uint32_t acc = 0;
   const float sl = 0.127f;
   __syncthreads();
+  if (static_cast<int>(threadIdx.x / 32) >= nsoft) {   // spinner
+    asm volatile(
+        "{\n.reg .pred P1;\nW:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@!P1 bra W;\n}\n" ::"r"(db) : "memory");
+    return;
+  }
   long long t0 = clock64();
   for (int j = 0; j < steps; ++j) {
     if (TM) {
@@ -103,8 +117,7 @@ __global__ void __launch_bounds__(LB, 1) k(const float* in, uint32_t* out, long 
     for (int c = 0; c < 128; c += 16) s[c] += __uint_as_float(acc & 0x00000001u);
   }
   long long t1 = clock64();
-  neo::umma::fence_before_sync();
-  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(db) : "memory");
   if (TM && threadIdx.x < 32) neo::umma::tmem_dealloc(tmem_sh, 512);
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc ^ __float_as_uint(unf2(l2).x);
   if (threadIdx.x % 32 == 0) cyc[threadIdx.x / 32] = t1 - t0;
@@ -115,7 +128,7 @@ int main() {
   cudaMalloc(&out, 1 << 20); cudaMalloc(&cyc, 64 * 8);
   for (int w : {1, 4, 8}) {
     const int steps = 100;
-    k<0><<<1, 32 * w>>>(in, out, cyc, steps);
+    k<0><<<1, 32 * (w + (SPIN ? 4 : 0))>>>(in, out, cyc, steps, w);
     cudaDeviceSynchronize();
     long long h[64];
     cudaMemcpy(h, cyc, 8 * w, cudaMemcpyDeviceToHost);
