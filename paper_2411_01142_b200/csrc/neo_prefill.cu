@@ -831,6 +831,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   warps 8-11       V bf16 -> fp16 conversion (32 rows each) and the epilogue
 //   warp 12          K/V TMA producer      warp 13  MMA issuer
 //   warp 14          Q TMA producer        warp 15  idle
+//
+// Barrier phases (each waiter tracks parity; no barrier can run two phases
+// ahead of a waiter, which would alias the parity):
+//   s_full / p_full (per tile): S_{j+1} is issued only after p_full of step j,
+//     and step j+1's softmax waits s_full before arriving p_full again.
+//   q_full / q_empty (per tile): the Q warp loads item r + 1 only after the
+//     tile's last S of item r completed; the MMA waits q_full of item r + 1
+//     before its first S.
+//   o_done / l_ready / o_free (per tile, once per item): o_done(r + 1) needs the
+//     tile's first PV of item r + 1, which waits o_free(r), which the epilogue
+//     arrives only after it waited o_done(r) and l_ready(r) and read O and l(r);
+//     the softmax writes l(r + 2) only after S_0(r + 2), i.e. after that PV, so
+//     the two l buffers (item parity) never collide.
+//   K / V rings (2 stages) and v_conv: a stage is refilled only after the
+//     previous occupant's consumers committed its `empty` barrier, and v_conv of
+//     a tile needs all 8 converting warps, so no warp runs two tiles ahead.
 // ============================================================================
 namespace s2 {
 constexpr int kThreads = 512;

@@ -201,6 +201,29 @@ def test_prefill_parity_long_prompts_sampled(n, variant):
         assert ok, f"n={n} variant={variant} row={i} err/tol={ratio:.3f}"
 
 
+@pytest.mark.parametrize("kernel", ["item", "stream"])
+def test_prefill_long_prompt_both_fp16_kernels(kernel, monkeypatch):
+    """An 8K whole prompt with peaked logits (the lazy O rescale fires) through
+    both fp16 kernels: the launch picks the item-major one at this length, the
+    stream kernel (NEO_PREFILL_KERNEL=stream) must be exact at any length too."""
+    import os
+    import oracle
+    import torch
+    monkeypatch.setenv("NEO_PREFILL_KERNEL", kernel)
+    n = 8192
+    case = PrefillCase([n], [n], 32, 8, seed=850, variant=ni.VARIANT_PEAKED)
+    out = case.run()
+    got = ni.bf16_bits_to_f64(out.view(torch.int16).cpu().numpy().view(np.uint16))
+    rng = np.random.default_rng(851)
+    rows = sorted(set([0, 31, 32, 63, 64, 127, 128, 4095, 4096, n - 65, n - 64, n - 1] + rng.integers(0, n, 20).tolist()))
+    ref = oracle.decode_attention_batch(case.qp[rows], [case.k_req[0][:i + 1] for i in rows],
+                                        [case.v_req[0][:i + 1] for i in rows], np.float32(case.scale),
+                                        nthreads=os.cpu_count() or 1)
+    for j, i in enumerate(rows):
+        ok, ratio = within_tol(got[i], ref[j])
+        assert ok, f"{kernel} row={i} err/tol={ratio:.3f}"
+
+
 @pytest.mark.parametrize("pv,kernel", [("hilo", "item"), ("fp16", "item"), ("fp16", "stream")])
 def test_prefill_both_pv_paths(pv, kernel, monkeypatch):
     """Every prefill kernel variant (DESIGN "prefill P.V": fp16 P with V converted
