@@ -61,7 +61,7 @@ constexpr uint32_t kColO = 128;
 constexpr int kFp16MinQLen = 256;
 constexpr int kStreamMaxQLen = 3072;             // fp16 path: stream kernel up to here, item-major above
 #ifndef NEO_PF_EXP
-#define NEO_PF_EXP 0   // timing experiments only (results wrong): 1 no V conversion, 2 no softmax math + no conversion, 3 no softmax math
+#define NEO_PF_EXP 0   // timing experiments only (results wrong): 1 no V conversion, 2 no softmax math + no conversion, 3 no softmax math, 4 (stream kernel) no MMAs (softmax math and conversion kept)
 #endif
 constexpr int kConvWarps = 0;
 constexpr uint32_t kIdescS = umma::idesc_bf16_f32(kBM, kBN, false, false);
@@ -1078,13 +1078,15 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
       const uint64_t dv0 = umma::desc_sw128(sb + kOffK + 2 * kKVHalf, kKVHalf, 1024);
       constexpr uint64_t kStageDesc = kStageBytes / 16;
       auto issue_s = [&](int t, int st) {
+        if (NEO_PF_EXP == 4) return;   // timing experiment: no tensor-core work at all
         umma::mma_block_k128<kQHalf, kKVHalf>(tmem + t * kTileCols, t ? dq1 : dq0,
                                               dk0 + static_cast<uint64_t>(st) * kStageDesc, kIdescS);
       };
       auto issue_pv = [&](int t, int st, int ksteps, bool acc0) {
         const uint32_t tp = tmem + t * kTileCols;
         const uint64_t bv = dv0 + static_cast<uint64_t>(st) * kStageDesc;
-        if (ksteps == 8) {
+        if (NEO_PF_EXP == 4) {
+        } else if (ksteps == 8) {
           umma::mma_block_pv128_single(tp + kColO, tp, bv, kIdescO, acc0);
         } else if (lane == 0) {
           for (int kq = 0; kq < ksteps; ++kq)
@@ -1272,7 +1274,7 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
 #pragma unroll
           for (int c = 0; c < kBN; ++c) s[c] = __uint_as_float(u[c / 32][c % 32]);
         }
-        if (NEO_PF_EXP >= 2) {
+        if (NEO_PF_EXP == 2 || NEO_PF_EXP == 3) {
           if (NEO_PF_PINGPONG) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
           uint32_t hw[16];
 #pragma unroll

@@ -42,6 +42,30 @@ __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+#ifndef POLY
+#define POLY 0   // of every 4 column pairs, how many take the FMA-pipe exp2 (degree-4, as the kernel)
+#endif
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  float2 x = unf2(x2);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const uint64_t magic = f2(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(f2(x.x, x.y), magic);
+  const uint64_t fr = fsub2(f2(x.x, x.y), fsub2(t, magic));
+  uint64_t p = ffma2(fr, f2(0.0096181291f, 0.0096181291f), f2(0.0555041087f, 0.0555041087f));
+  p = ffma2(p, fr, f2(0.2402265070f, 0.2402265070f));
+  p = ffma2(p, fr, f2(0.6931471806f, 0.6931471806f));
+  p = ffma2(p, fr, f2(1.f, 1.f));
+  const float2 tt = unf2(t), pv = unf2(p);
+  const uint32_t r0 = __float_as_uint(tt.x) * (1u << 23) + __float_as_uint(pv.x);
+  const uint32_t r1 = __float_as_uint(tt.y) * (1u << 23) + __float_as_uint(pv.y);
+  return f2(__uint_as_float(r0), __uint_as_float(r1));
+}
 template <int kVariant>
 #ifndef LB
 #define LB 256
@@ -98,8 +122,17 @@ __global__ void __launch_bounds__(LB, 1) k(const float* in, uint32_t* out, long 
     uint32_t hw[64];
 #pragma unroll
     for (int w = 0; w < 64; ++w) {
-      const float2 x = unf2(ffma2(f2(s[2 * w], s[2 * w + 1]), sl2, nm2));
-      const float p0 = ex2(x.x), p1 = ex2(x.y);
+      const uint64_t xx = ffma2(f2(s[2 * w], s[2 * w + 1]), sl2, nm2);
+      float p0, p1;
+      if ((w & 3) < POLY) {
+        const float2 pp = unf2(exp2_poly2(xx));
+        p0 = pp.x;
+        p1 = pp.y;
+      } else {
+        const float2 x = unf2(xx);
+        p0 = ex2(x.x);
+        p1 = ex2(x.y);
+      }
       if (w & 1) lb = fadd2(lb, f2(p0, p1));
       else la = fadd2(la, f2(p0, p1));
       hw[w] = pack_f16(p0, p1);
