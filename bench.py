@@ -531,7 +531,7 @@ def run_prefill(args):
     kernel = "prefill_attn_stream_kernel" if max(lens) <= 3072 else "prefill_attn_kernel"
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):          # ncu capture of this launch (profiles/r02_ncu_prefill_stream.md)
+    if os.path.exists(tpath):          # ncu --set full of this launch (profiles/r02_ncu_full_prefill_stream.md)
         traffic = json.load(open(tpath)).get("prefill_stream" if kernel.endswith("stream_kernel") else "prefill")
     peak, src = tensor_peak()
     achieved = flops / t_att / 1e12

@@ -80,6 +80,7 @@ struct PArgs {
   const int32_t* q_offsets;
   int32_t batch, hq, hkv, G, page_size, max_blocks, n_ct_max;
   float scale_log2;
+  int32_t epi_delay_ns;   // test knob (NEO_PREFILL_EPI_DELAY_NS): stream-kernel epilogue sleeps before each item
 #ifdef NEO_PREFILL_TRACE
   long long* trace;   // [2 tiles][64 steps][16] clock64 stamps of CTA 0 (tools/prefill_trace.py)
 #endif
@@ -111,6 +112,25 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+#ifdef NEO_PF_DEBUG_HANG
+// debug build: report (block, warp, barrier offset, parity) and trap after 2^16 polls
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  for (uint32_t n = 0;; ++n) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (n == (1u << 16)) {
+      printf("HANG block %d warp %d lane %d bar+%u parity %u\n", blockIdx.x, threadIdx.x / 32, threadIdx.x % 32,
+             bar & 0xffff, parity);
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -124,6 +144,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
                                             int c4, uint32_t bar) {
   asm volatile(
@@ -841,9 +862,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 //     before its first S.
 //   o_done / l_ready / o_free (per tile, once per item): o_done(r + 1) needs the
 //     tile's first PV of item r + 1, which waits o_free(r), which the epilogue
-//     arrives only after it waited o_done(r) and l_ready(r) and read O and l(r);
-//     the softmax writes l(r + 2) only after S_0(r + 2), i.e. after that PV, so
-//     the two l buffers (item parity) never collide.
+//     arrives only after it waited o_done(r) and l_ready(r) and read O and l(r).
+//     l_ready is NOT gated by the MMA chain (a one-step item's softmax needs no
+//     PV of its own), so the softmax waits o_free(r) before it writes l(r + 1)
+//     and arrives l_ready(r + 1): at most one phase ahead, and the two l
+//     buffers (item parity) never collide.  o_free has two waiters (MMA and
+//     softmax), each waiting every phase in order.
 //   K / V rings (2 stages) and v_conv: a stage is refilled only after the
 //     previous occupant's consumers committed its `empty` barrier, and v_conv of
 //     a tile needs all 8 converting warps, so no warp runs two tiles ahead.
@@ -1219,8 +1243,10 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
       for (int j = 0; j < nt; ++j) {
         if (NEO_PF_CONV_EPI)
           convert_v_rows<32>(sb, bar(s2::kBarVFull), bar(s2::kBarVConv), vidx++, it.ctx - j * kBN, row0, lane);
-        if (j == 0 && rd > 0)
+        if (j == 0 && rd > 0) {
+          for (int d = a.epi_delay_ns; d > 0; d -= 500000) __nanosleep(min(d, 500000));
           for (int t = 0; t < kTiles; ++t) epilogue(rd - 1, prev, t, steps_done - 1);
+        }
       }
       steps_done += nt;
       prev = it;
@@ -1385,6 +1411,12 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
       // row sum to the epilogue (its O wait is on o_done, committed after the
       // last PV, which follows this item's last p_full)
       const float2 lp = unf2(l2);
+      // l_ready may run only one item ahead of the epilogue's wait on it (a
+      // second completion would alias the parity it waits on): wait until the
+      // epilogue released the previous item's O (o_free, arrived after it
+      // waited l_ready of that item).  Without this, a one-step item right
+      // after a slow epilogue lets the softmax complete l_ready twice.
+      if (rd > 0) mbar_wait(bar(s2::kBarOFree + t), (rd - 1) & 1);
       lbuf[t][rd & 1][r] = lp.x + lp.y;
       __syncwarp();
       if (lane == 0) mbar_arrive(bar(s2::kBarLReady + t));
@@ -1394,6 +1426,7 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
   __syncthreads();
   if (warp == s2::kMmaWarp) umma::tmem_dealloc(tmem, kTmemCols);
 }
+
 
 }  // namespace
 
@@ -1424,8 +1457,9 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   const int64_t n_items = static_cast<int64_t>(n_ct_max) * L.batch * L.hkv;   // upper bound
   if (L.batch > kMaxSchedBatch || n_ct_max > kMaxSchedLevels)
     return fail(NEO_ERR_UNSUPPORTED, "prefill: batch <= 512 and max_q_len * G <= 262144 per call");
+  const char* dly = std::getenv("NEO_PREFILL_EPI_DELAY_NS");   // test knob: a slow epilogue (barrier-phase test)
   PArgs a{static_cast<uint16_t*>(L.out), L.block_table, L.seq_lens, L.q_offsets, L.batch, L.hq, L.hkv, G,
-          L.page_size, L.max_blocks, n_ct_max, L.scale * 1.4426950408889634f};
+          L.page_size, L.max_blocks, n_ct_max, L.scale * 1.4426950408889634f, dly ? std::atoi(dly) : 0};
 #ifdef NEO_PREFILL_TRACE
   static long long* trace = nullptr;
   if (!trace) cudaMalloc(&trace, 2 * 64 * 16 * sizeof(long long));

@@ -238,3 +238,24 @@ def test_prefill_both_pv_paths(pv, kernel, monkeypatch):
     check_prefill(PrefillCase([500, 200, 129, 1500, 33], [100, 1, 64, 257, 33], 32, 8, P=32, seed=901),
                   f"{pv} P=32")
     check_prefill(PrefillCase([77, 2100], [77, 2100], 16, 1, seed=902, variant=ni.VARIANT_PEAKED), f"{pv} G=16")
+
+
+def test_prefill_slow_epilogue_one_step_items():
+    """Barrier-phase regression (stream kernel): with the epilogue slowed down
+    (NEO_PREFILL_EPI_DELAY_NS sleeps before each item's epilogue), the softmax
+    warps of a CTA working through one-step items would complete l_ready twice
+    before the epilogue waits on it and alias its parity -- a hang -- unless
+    they wait o_free of the previous item first.  Run in a subprocess with a
+    timeout, so a regression fails the test instead of hanging the suite."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    ctx = ",".join(["300"] + ["64"] * 60 + ["1", "17"])
+    env = dict(os.environ, NEO_PREFILL_KERNEL="stream", NEO_PREFILL_EPI_DELAY_NS="200000")
+    try:
+        r = subprocess.run([sys.executable, os.path.join(here, "_prefill_slow_epilogue.py"), ctx], env=env,
+                           capture_output=True, text=True, timeout=180)
+    except subprocess.TimeoutExpired:
+        pytest.fail("stream prefill kernel hung with a slow epilogue (l_ready parity aliasing)")
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
