@@ -848,8 +848,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   * every CTA's item list is decoded once in the prologue into shared memory;
 //   * setmaxnreg: 168 registers for the softmax warpgroups, 96 for the epilogue,
 //     80 for the producer / MMA warpgroup (sum = the 128 x 512 launch pool).
-//   warps 0-3 / 4-7  softmax of tile 0 / 1 (thread = row = TMEM lane)
-//   warps 8-11       V bf16 -> fp16 conversion (32 rows each) and the epilogue
+//   warps 0-3 / 4-7  softmax of tile 0 / 1 (thread = row = TMEM lane); all 8
+//                    convert each V tile bf16 -> fp16 in place, 16 rows each
+//   warps 8-11       epilogue
 //   warp 12          K/V TMA producer      warp 13  MMA issuer
 //   warp 14          Q TMA producer        warp 15  idle
 //
@@ -882,12 +883,6 @@ constexpr int kMaxCtaItems = 512;   // items decoded in the prologue (later ones
 }  // namespace s2
 
 
-#ifndef NEO_PF_PINGPONG
-#define NEO_PF_PINGPONG 0   // stream kernel (measured slower, kept for A/B): the two tiles' softmax phases alternate (named barriers 1, 2)
-#endif
-#ifndef NEO_PF_CONV_EPI
-#define NEO_PF_CONV_EPI 0   // stream kernel: 0 = the softmax warps convert V (16 rows each), 1 = the epilogue warps (32 rows)
-#endif
 // V tile vi (ring stage vi % kStages): rows [row0, row0 + NR) bf16 -> fp16 in
 // place once the tile has landed; rows past the context are zeroed (P = 0
 // there, but 0 * NaN = NaN); then one arrival on the conversion barrier.
@@ -1002,7 +997,7 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
       mbar_init(bar(s2::kBarVFull + s), 1);
       mbar_init(bar(s2::kBarKEmpty + s), 1);
       mbar_init(bar(s2::kBarVEmpty + s), 1);
-      mbar_init(bar(s2::kBarVConv + s), NEO_PF_CONV_EPI ? 4 : 8);   // converting warps
+      mbar_init(bar(s2::kBarVConv + s), 8);   // the 8 softmax warps convert V
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1189,11 +1184,8 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
     }
   } else if (warp >= s2::kEpiWarp0) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
-    // ------------------------------------------------- epilogue + V conversion
-    // One warp per TMEM lane quarter.  In ring order it converts its 32 rows of
-    // every V tile bf16 -> fp16 in place (rows past the context zeroed: P = 0
-    // there, but 0 * NaN = NaN) and, after the next item's first V tile, drains
-    // the previous item's O / l of both tiles to global.
+    // ------------------------------------------------------------ epilogue
+    // One warp per TMEM lane quarter drains each item's O / l of both tiles.
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const int row0 = quarter * 32;
@@ -1233,26 +1225,14 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
       }
       if (quarter == 0 && lane == 0) TRACE(t, trace_row, 10);
     };
-    uint32_t vidx = 0;
-    int steps_done = 0;                              // trace row of the previous item's last step
-    Item prev;
+    int steps_done = 0;                              // trace row of the item's last step
     for (int rd = 0; rd < n_rounds; ++rd) {
       Item it;
       get_item(rd, it);
-      const int nt = steps_of(it);
-      for (int j = 0; j < nt; ++j) {
-        if (NEO_PF_CONV_EPI)
-          convert_v_rows<32>(sb, bar(s2::kBarVFull), bar(s2::kBarVConv), vidx++, it.ctx - j * kBN, row0, lane);
-        if (j == 0 && rd > 0) {
-          for (int d = a.epi_delay_ns; d > 0; d -= 500000) __nanosleep(min(d, 500000));
-          for (int t = 0; t < kTiles; ++t) epilogue(rd - 1, prev, t, steps_done - 1);
-        }
-      }
-      steps_done += nt;
-      prev = it;
+      steps_done += steps_of(it);
+      for (int d = a.epi_delay_ns; d > 0; d -= 500000) __nanosleep(min(d, 500000));   // test knob
+      for (int t = 0; t < kTiles; ++t) epilogue(rd, it, t, steps_done - 1);
     }
-    if (n_rounds > 0)
-      for (int t = 0; t < kTiles; ++t) epilogue(n_rounds - 1, prev, t, steps_done - 1);
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory");
     // ------------------------------------------------------------ softmax warps
@@ -1262,18 +1242,6 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
     const uint32_t tO = tS + kColO;
     const float sl = a.scale_log2;
     uint32_t sc = 0, vidx = 0;
-    // ping-pong: the two tiles' softmax phases alternate (named barrier 1 + t =
-    // "tile t's turn", granted by the other warpgroup), so each runs with the
-    // SMSPs' MUFU pipes to itself while the tensor core works on the other tile
-    int total_steps = 0;
-    if (NEO_PF_PINGPONG) {
-      for (int rd = 0; rd < n_rounds; ++rd) {
-        Item it;
-        get_item(rd, it);
-        total_steps += steps_of(it);
-      }
-      if (t == 1 && total_steps > 0) asm volatile("bar.arrive 1, 256;" ::: "memory");   // tile 0 goes first
-    }
     for (int rd = 0; rd < n_rounds; ++rd) {
       Item it;
       get_item(rd, it);
@@ -1285,8 +1253,7 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
       for (int j = 0; j < nt; ++j, ++sc) {
         if (quarter == 0 && lane == 0) TRACE(t, sc, 0);
         if (quarter == 0 && lane == 0 && j == 0) TRACE(t, sc, 7);
-        if (!NEO_PF_CONV_EPI)
-          convert_v_rows<16>(sb, bar(s2::kBarVFull), bar(s2::kBarVConv), vidx++, it.ctx - j * kBN, (t * 4 + quarter) * 16,
+        convert_v_rows<16>(sb, bar(s2::kBarVFull), bar(s2::kBarVConv), vidx++, it.ctx - j * kBN, (t * 4 + quarter) * 16,
                              lane);
         mbar_wait(bar(s2::kBarSFull + t), sc & 1);
         umma::fence_after_sync();
@@ -1301,7 +1268,6 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
           for (int c = 0; c < kBN; ++c) s[c] = __uint_as_float(u[c / 32][c % 32]);
         }
         if (NEO_PF_EXP == 2 || NEO_PF_EXP == 3) {
-          if (NEO_PF_PINGPONG) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
           uint32_t hw[16];
 #pragma unroll
           for (int w = 0; w < 16; ++w) hw[w] = __float_as_uint(s[w] * 0.f);
@@ -1310,8 +1276,6 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
           l2 = f2(1.f, 1.f);
           umma::wait_st();
           umma::fence_before_sync();
-          if (NEO_PF_PINGPONG && !(t == 1 && static_cast<int>(sc) == total_steps - 1))
-            asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(bar(s2::kBarPFull + t));
           continue;
@@ -1329,8 +1293,6 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
 #pragma unroll
           for (int c = 0; c < 32; ++c) s[c0 + c] = c0 + c > lim ? -INFINITY : s[c0 + c];
         }
-        // ping-pong turn: the MUFU-heavy max / exp / P phase (S already in registers)
-        if (NEO_PF_PINGPONG) asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
         if (quarter == 0 && lane == 0) TRACE(t, sc, 2);
         // row max: four independent chains per chunk
         float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -1402,8 +1364,6 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
         }
         umma::wait_st();
         umma::fence_before_sync();
-        if (NEO_PF_PINGPONG && !(t == 1 && static_cast<int>(sc) == total_steps - 1))
-          asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");   // the other tile's turn
         __syncwarp();
         if (quarter == 0 && lane == 0) TRACE(t, sc, 3);
         if (lane == 0) mbar_arrive(bar(s2::kBarPFull + t));
