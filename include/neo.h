@@ -239,6 +239,10 @@ NEO_API neo_status neo_rope_append(void* q_inout, int32_t num_q_heads, const flo
  * rounded to fp16 (RNE; V saturates beyond fp16's range, so V entries must lie
  * within |v| <= 65504) with fp32 accumulation; shorter calls apply P as bf16
  * hi + lo against bf16 V (DESIGN "prefill P.V").  Output RNE to bf16.
+ * Kernels (DESIGN NEXT-3): fp16-path calls with max_q_len <= 3072 run the
+ * warp-specialised stream kernel (all exponentials on MUFU), longer calls the
+ * item-major kernel (a quarter of the exponentials by a degree-4 polynomial,
+ * relative error <= 4.3e-5); both within the tolerance rule, selected by shape.
  * Deterministic for a fixed call shape.
  * Page-tail slots beyond seq_lens are never read into the result (NaN-safe).
  * Errors: NEO_ERR_INVALID_ARG, NEO_ERR_UNSUPPORTED, NEO_ERR_CUDA; NEO_DEBUG_VALIDATE=1
