@@ -66,6 +66,27 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
   const uint32_t r1 = __float_as_uint(tt.y) * (1u << 23) + __float_as_uint(pv.y);
   return f2(__uint_as_float(r0), __uint_as_float(r1));
 }
+#ifndef DEG3
+#define DEG3 0   // 1: degree-3 minimax polynomial (8 instructions per pair) instead of the kernel's degree-4
+#endif
+__device__ __forceinline__ uint64_t exp2_poly3(uint64_t x2) {
+  // 2^x = 2^j * 2^f, j = rint(x) by the 1.5 * 2^23 shifter, f in [-0.5, 0.5],
+  // 2^f ~ 1 + f (c1 + f (c2 + f c3)); exponent added with one IMAD per element
+  float2 x = unf2(x2);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const uint64_t xc = f2(x.x, x.y);
+  const uint64_t magic = f2(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(xc, magic);
+  const uint64_t fr = fsub2(xc, fsub2(t, magic));
+  uint64_t p = ffma2(fr, f2(0.0558755f, 0.0558755f), f2(0.2401536f, 0.2401536f));
+  p = ffma2(p, fr, f2(0.6931182f, 0.6931182f));
+  p = ffma2(p, fr, f2(1.0000000f, 1.0000000f));
+  const float2 tt = unf2(t), pv = unf2(p);
+  const uint32_t r0 = __float_as_uint(tt.x) * (1u << 23) + __float_as_uint(pv.x);
+  const uint32_t r1 = __float_as_uint(tt.y) * (1u << 23) + __float_as_uint(pv.y);
+  return f2(__uint_as_float(r0), __uint_as_float(r1));
+}
 template <int kVariant>
 #ifndef LB
 #define LB 256
@@ -125,7 +146,7 @@ __global__ void __launch_bounds__(LB, 1) k(const float* in, uint32_t* out, long 
       const uint64_t xx = ffma2(f2(s[2 * w], s[2 * w + 1]), sl2, nm2);
       float p0, p1;
       if ((w & 3) < POLY) {
-        const float2 pp = unf2(exp2_poly2(xx));
+        const float2 pp = unf2(DEG3 ? exp2_poly3(xx) : exp2_poly2(xx));
         p0 = pp.x;
         p1 = pp.y;
       } else {
