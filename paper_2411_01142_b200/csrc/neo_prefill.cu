@@ -1005,8 +1005,10 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
     umma::tmem_alloc(smem_u32(&tmem_sh), kTmemCols);
     umma::tmem_relinquish();
   }
+  if (threadIdx.x == 0) TRACE(0, 63, 13);                    // kernel entry (trace builds)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");   // metadata and q may come from the previous kernel
+  if (threadIdx.x == 0) TRACE(0, 63, 14);
   build_sched(a, rows_tok, sched, nct_tmp);
   const int n_items = sched.pref[a.n_ct_max];
   int n_rounds = 0;                                   // items of this CTA
@@ -1027,6 +1029,7 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tmem = tmem_sh;
+  if (threadIdx.x == 0) TRACE(0, 63, 15);                    // prologue done
   auto get_item = [&](int r, Item& it) {
     if (r < s2::kMaxCtaItems) unpack_item(a, sched, citems[r], rows_tok, it);
     else make_item(a, sched, first_item(r), rows_tok, it);
@@ -1233,6 +1236,7 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
       for (int d = a.epi_delay_ns; d > 0; d -= 500000) __nanosleep(min(d, 500000));   // test knob
       for (int t = 0; t < kTiles; ++t) epilogue(rd, it, t, steps_done - 1);
     }
+    if (quarter == 0 && lane == 0) TRACE(1, 63, 13);             // last store issued
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 168;" ::: "memory");
     // ------------------------------------------------------------ softmax warps

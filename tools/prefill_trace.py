@@ -39,10 +39,16 @@ import cuda.bindings.runtime as rt  # noqa: E402
 rt.cudaMemcpy(buf.data_ptr(), ptr, buf.numel() * 8, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
 tr = buf.cpu().numpy().reshape(2, 64, 16)
 t0 = tr[tr > 0].min()
+if tr[0, 63, 13]:
+    e = tr[0, 63]
+    print(f"stream kernel prologue: entry -> PDL wait done {e[14] - e[13]}, -> schedule built {e[15] - e[14]} cycles; "
+          f"first S ready {tr[0, 0, 1] - e[13]} after entry; last store issued {tr[1, 63, 13] - e[13]} after entry")
 print("step  tile | wait->S ready  ldS  softmax  | MMA: wait p  issue | period")
 for j in range(64):
     for t in range(2):
         r = tr[t, j]
+        if j == 63 and tr[0, 63, 13]:
+            continue
         if r[0] == 0:
             continue
         per = tr[t, j + 1, 1] - r[1] if j + 1 < 64 and tr[t, j + 1, 1] else 0
