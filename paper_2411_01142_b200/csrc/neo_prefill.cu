@@ -1011,8 +1011,8 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
   if (threadIdx.x == 0) TRACE(0, 63, 14);
   build_sched(a, rows_tok, sched, nct_tmp);
   const int n_items = sched.pref[a.n_ct_max];
-  int n_rounds = 0;                                   // items of this CTA
-  while (first_item(n_rounds) < n_items) ++n_rounds;
+  // items of this CTA: every full round, plus the last partial one if it reaches this CTA
+  const int n_rounds = n_items / grid + (first_item(n_items / grid) < n_items ? 1 : 0);
   for (int r = threadIdx.x; r < min(n_rounds, s2::kMaxCtaItems); r += blockDim.x) {
     Item it;
     const int k = first_item(r);
