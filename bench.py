@@ -270,7 +270,11 @@ def run_neo(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     wl = WORKLOADS[args.config]
     ctx_all, req_ids, kvh, qh, scaling, par = shard_plan(wl, rank, world, args.fraction)
-    gb = GpuBatch(wl, ctx=ctx_all, req_ids=req_ids, kv_heads=kvh, q_heads=qh)
+    # harness only (with NEO_BENCH_SHARE_GPU=1): fewer distinct layer pools, cycled,
+    # so several full-size ranks fit on one GPU; never set for a measurement
+    max_pools = os.environ.get("NEO_BENCH_MAX_POOLS") if os.environ.get("NEO_BENCH_SHARE_GPU") == "1" else None
+    gb = GpuBatch(wl, ctx=ctx_all, req_ids=req_ids, kv_heads=kvh, q_heads=qh,
+                  layers=min(wl.layers_built, int(max_pools)) if max_pools else None)
     L = layers_per_step(wl)
     stream = torch.cuda.current_stream()
     # a0 plan from the host-known lengths (NEO's scheduler holds them)

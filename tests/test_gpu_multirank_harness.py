@@ -52,6 +52,31 @@ def test_bench_two_ranks_on_one_gpu(cfg):
         assert j["config"]["parallelism"].startswith("dp2") and j["config"]["batch"] == 1024
 
 
+def test_bench_default_config_two_ranks_on_one_gpu():
+    """The driver's scaling run launches bench.py with NO --config: c3 (weak
+    scaling, every rank its own 128 requests) with the swap leg and rank 0's
+    prefill leg.  Two ranks on one GPU with 4 cycled layer pools per rank
+    (NEO_BENCH_MAX_POOLS, harness only) so both fit in HBM."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    env = dict(os.environ, NEO_BENCH_DIST_BACKEND="gloo", NEO_BENCH_SHARE_GPU="1", NEO_BENCH_MAX_POOLS="4")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3"]
+    res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["value"] > 0 and j["scaling"] == "weak"
+    assert j["config"]["batch"] == 256 and j["config"]["batch_per_rank"] == 128
+    assert j["config"]["parallelism"].startswith("dp2")
+    assert j["swap"] is not None and j["swap"]["swap_out_gbs"] > 0
+    assert j["prefill"] is not None and j["prefill"]["attn_us"] > 0
+    assert j["e2e"]["value"] > 0 and len(j["per_rank_ms_per_step"]) == 2
+
+
 WORK_CTX = {}
 
 
