@@ -1392,452 +1392,6 @@ __global__ void __launch_bounds__(s2::kThreads, 1)
 }
 
 
-
-// ============================================================================
-// Pair kernel (`prefill_attn_pair_kernel`, experimental: NEO_PREFILL_KERNEL=pair).
-//
-// A 2-CTA cluster (one TPC) runs one item: CTA rank t holds tile t's 128 query
-// rows.  With one tile per SM, TMEM holds TWO S buffers (S 2 x 128 + O 128
-// columns), so S_{j+2} is computed into the buffer PV_j just read while the
-// softmax of S_{j+1} runs: the softmax warps never wait for the tensor core,
-// and the tensor core never waits for a softmax.  K and V tiles are TMA-
-// multicast to both CTAs (each CTA loads one dim-half of every box), so the
-// L2 -> SM traffic per item is that of the two-tile kernels; a stage is
-// refilled once BOTH CTAs released it (their MMA warps commit to both CTAs'
-// empty barriers, count 2).  Eight softmax warps split each row in two
-// 64-column halves (warp w: lane quarter w & 3, half w >> 2) and exchange the
-// half-row maxima through shared memory every step; each keeps its own partial
-// row sum, which the epilogue adds.
-//   warps 0-7 softmax (+ V bf16 -> fp16 of their 16 rows of the local copy)
-//   warps 8-11 epilogue   warp 12 K producer   warp 13 MMA   warp 14 Q   warp 15 V producer
-// Barrier phases: s_full / p_full per S buffer (S_{g+2} follows p_full(g));
-// pv_done waited by the softmax every step (before an O rescale); the K / V
-// stages (2 each) of step g are refilled for step g + 2 only after both CTAs'
-// S_g (K) / PV_g (V) completed; q buffers by item parity; o_done / l_ready /
-// o_free as the stream kernel (l_ready gated on o_free).
-// ============================================================================
-namespace s4 {
-constexpr int kThreads = 512;
-constexpr int kEpiWarp0 = 8, kKProdWarp = 12, kMmaWarp = 13, kQWarp = 14, kVProdWarp = 15;
-constexpr int kQBytes = 2 * kQHalf;                 // one 128-row tile, both dim-halves: 32 KiB
-constexpr int kOffK = 2 * kQBytes;                  // two Q buffers (item parity)
-constexpr int kKStage = 2 * kKVHalf;                // 32 KiB
-constexpr int kOffV = kOffK + 2 * kKStage;
-constexpr int kSmem = kOffV + 2 * kKStage;          // 192 KiB
-static_assert(kSmem == kSmemBytes, "same footprint as the other prefill kernels");
-constexpr uint32_t kColS1 = 128, kColO = 256;
-constexpr int kBarQFull = 0, kBarQEmpty = 2, kBarKFull = 4, kBarVFull = 6, kBarKEmpty = 8, kBarVEmpty = 10,
-              kBarVConv = 12, kBarSFull = 14, kBarPFull = 16, kBarPVDone = 18, kBarODone = 19, kBarOFree = 20,
-              kBarLReady = 21, kNumBars = 22;
-}  // namespace s4
-
-__device__ __forceinline__ uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_5d_mc(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
-                                               int c4, uint32_t bar, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar), "h"(mask)
-      : "memory");
-}
-// commit (one elected lane) arriving on the barrier at this offset in both CTAs of the pair
-__device__ __forceinline__ void commit_pair(uint32_t bar) {
-  asm volatile(
-      "{\n"
-      ".reg .pred e;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
-      "}\n" ::"r"(bar),
-      "h"(static_cast<uint16_t>(3))
-      : "memory");
-}
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(s4::kThreads, 1)
-    prefill_attn_pair_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
-                             const __grid_constant__ CUtensorMap tmv, const PArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t bars[s4::kNumBars];
-  __shared__ uint32_t tmem_sh;
-  __shared__ Sched sched;
-  __shared__ int nct_tmp[kMaxSchedBatch];
-  __shared__ uint32_t citems[s2::kMaxCtaItems];
-  __shared__ float lbuf[2][2][kBM];                   // [half][item parity][row]: partial row sums
-  __shared__ float xmax[2][2][kBM];                   // [step parity][half][row]: half-row maxima
-  constexpr float kPBias = 7.f;
-  constexpr uint32_t kIdescO = umma::idesc_f16_f32(kBM, 128, false, true);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = a.G, rows_tok = kBM / G;
-  const int rank = static_cast<int>(cluster_ctarank());          // = this CTA's tile
-  const int cid = static_cast<int>(blockIdx.x) >> 1, ncl = static_cast<int>(gridDim.x) >> 1;
-  auto first_item = [&](int round) { return round * ncl + ((round & 1) ? ncl - 1 - cid : cid); };
-
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t sb = smem_u32(smem);
-  const uint32_t bar0 = smem_u32(bars);
-  auto bar = [bar0](int i) { return bar0 + 8u * static_cast<uint32_t>(i); };
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(s4::kBarQFull + i), 1);
-      mbar_init(bar(s4::kBarQEmpty + i), 1);
-      mbar_init(bar(s4::kBarKFull + i), 1);
-      mbar_init(bar(s4::kBarVFull + i), 1);
-      mbar_init(bar(s4::kBarKEmpty + i), 2);          // both CTAs' S
-      mbar_init(bar(s4::kBarVEmpty + i), 2);          // both CTAs' PV
-      mbar_init(bar(s4::kBarVConv + i), 8);
-      mbar_init(bar(s4::kBarSFull + i), 1);
-      mbar_init(bar(s4::kBarPFull + i), 8);
-    }
-    mbar_init(bar(s4::kBarPVDone), 1);
-    mbar_init(bar(s4::kBarODone), 1);
-    mbar_init(bar(s4::kBarOFree), 4);
-    mbar_init(bar(s4::kBarLReady), 8);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == s4::kMmaWarp) {
-    umma::tmem_alloc(smem_u32(&tmem_sh), kTmemCols);
-    umma::tmem_relinquish();
-  }
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  build_sched(a, rows_tok, sched, nct_tmp);
-  const int n_items = sched.pref[a.n_ct_max];
-  const int n_rounds = n_items / ncl + (first_item(n_items / ncl) < n_items ? 1 : 0);
-  for (int r = threadIdx.x; r < min(n_rounds, s2::kMaxCtaItems); r += blockDim.x) {
-    Item it;
-    const int k = first_item(r);
-    make_item(a, sched, k, rows_tok, it);
-    int lo = 0, hi = a.n_ct_max - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (sched.pref[mid] <= k) lo = mid;
-      else hi = mid - 1;
-    }
-    citems[r] = pack_item(it, a.n_ct_max - 1 - lo);
-  }
-  umma::fence_before_sync();
-  cluster_sync_all();                                  // both CTAs' barriers initialised before any multicast
-  umma::fence_after_sync();
-  const uint32_t tmem = tmem_sh;
-  auto get_item = [&](int r, Item& it) {
-    if (r < s2::kMaxCtaItems) unpack_item(a, sched, citems[r], rows_tok, it);
-    else make_item(a, sched, first_item(r), rows_tok, it);
-  };
-  auto steps_of = [](const Item& it) { return it.nt0 > it.nt1 ? it.nt0 : it.nt1; };
-
-  if (warp >= s4::kEpiWarp0 + 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
-    if (warp == s4::kKProdWarp || warp == s4::kVProdWarp) {
-      // ------------------------------------------------ K or V producer (multicast)
-      const bool is_k = warp == s4::kKProdWarp;
-      const CUtensorMap* tm = is_k ? &tmk : &tmv;
-      if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tm)) : "memory");
-      const int full = is_k ? s4::kBarKFull : s4::kBarVFull, empty = is_k ? s4::kBarKEmpty : s4::kBarVEmpty;
-      const uint32_t base = sb + (is_k ? s4::kOffK : s4::kOffV);
-      uint32_t kc = 0;
-      for (int r = 0; r < n_rounds; ++r) {
-        Item it;
-        get_item(r, it);
-        const int nt = steps_of(it);
-        const int32_t* bt = a.block_table + static_cast<int64_t>(it.b) * a.max_blocks;
-        for (int j = 0; j < nt; ++j, ++kc) {
-          const int st = kc & 1;
-          const int kv0 = j * kBN;
-          const int groups = min(kBN / 16, (it.ctx - kv0 + 15) / 16);
-          int page = 0, slot = 0;
-          if (lane < groups) {
-            const int t = kv0 + 16 * lane;
-            page = bt[t / a.page_size];
-            slot = t % a.page_size;
-          }
-          if (kc >= 2) mbar_wait(bar(empty + st), ((kc >> 1) - 1) & 1);   // both CTAs released the stage
-          if (lane == 0) mbar_expect_tx(bar(full + st), static_cast<uint32_t>(groups) * 2 * 2048);
-          __syncwarp();
-          // this CTA loads dim-half `rank` of every box, into both CTAs
-          if (lane < groups)
-            tma_load_5d_mc(base + st * s4::kKStage + rank * kKVHalf + lane * 2048, tm, 0, slot, rank, it.g, page,
-                           bar(full + st), 3);
-        }
-      }
-    } else if (warp == s4::kQWarp) {
-      // ---------------------------------------------------------- Q producer
-      if (lane == 0) {
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmq)) : "memory");
-        for (int r = 0; r < n_rounds; ++r) {
-          Item it;
-          get_item(r, it);
-          const int qb = r & 1;
-          if (r >= 2) mbar_wait(bar(s4::kBarQEmpty + qb), ((r >> 1) - 1) & 1);
-          mbar_expect_tx(bar(s4::kBarQFull + qb), s4::kQBytes);
-          for (int h = 0; h < 2; ++h)
-            tma_load_4d(sb + qb * s4::kQBytes + h * kQHalf, &tmq, 0, it.g * G, it.q0 + it.i0 + rank * rows_tok, h,
-                        bar(s4::kBarQFull + qb));
-        }
-      }
-    } else if (warp == s4::kMmaWarp) {
-      // ---------------------------------------------------------- MMA issuer
-      const uint64_t dq0 = umma::desc_sw128(sb, 16, 1024);
-      const uint64_t dk0 = umma::desc_sw128(sb + s4::kOffK, 16, 1024);
-      const uint64_t dv0 = umma::desc_sw128(sb + s4::kOffV, kKVHalf, 1024);
-      constexpr uint64_t kQDesc = s4::kQBytes / 16, kKDesc = s4::kKStage / 16;
-      // S cursor (two steps ahead of PV)
-      int sr = 0, sj = 0, snt = 0;
-      Item sit;
-      if (n_rounds > 0) {
-        get_item(0, sit);
-        snt = steps_of(sit);
-      }
-      uint32_t sg = 0;
-      auto issue_next_s = [&]() {
-        const int st = static_cast<int>(sg & 1), buf = st, qb = sr & 1;
-        mbar_wait(bar(s4::kBarKFull + st), (sg >> 1) & 1);
-        if (sj == 0) mbar_wait(bar(s4::kBarQFull + qb), (sr >> 1) & 1);
-        umma::fence_after_sync();
-        umma::mma_block_k128<kQHalf, kKVHalf>(tmem + (buf ? s4::kColS1 : 0u), dq0 + qb * kQDesc, dk0 + st * kKDesc,
-                                              kIdescS);
-        umma::commit_elect(bar(s4::kBarSFull + buf));
-        commit_pair(bar(s4::kBarKEmpty + st));                    // K tile consumed here (both CTAs count)
-        if (sj == snt - 1) umma::commit_elect(bar(s4::kBarQEmpty + qb));   // the item's last S
-        __syncwarp();
-        ++sg;
-        if (++sj == snt) {
-          sj = 0;
-          if (++sr < n_rounds) {
-            get_item(sr, sit);
-            snt = steps_of(sit);
-          }
-        }
-      };
-      if (n_rounds > 0) {
-        issue_next_s();
-        if (sr < n_rounds) issue_next_s();
-      }
-      uint32_t g = 0;
-      for (int r = 0; r < n_rounds; ++r) {
-        Item it;
-        get_item(r, it);
-        const int nt = steps_of(it);
-        for (int j = 0; j < nt; ++j, ++g) {
-          const int st = static_cast<int>(g & 1), buf = st;
-          const int nvalid = min(kBN, it.ctx - j * kBN);
-          const int ksteps = (nvalid + 15) / 16;
-          mbar_wait(bar(s4::kBarVConv + st), (g >> 1) & 1);
-          mbar_wait(bar(s4::kBarPFull + buf), (g >> 1) & 1);
-          if (j == 0 && r > 0) mbar_wait(bar(s4::kBarOFree), (r - 1) & 1);
-          umma::fence_after_sync();
-          const uint32_t tp = tmem + (buf ? s4::kColS1 : 0u);
-          const uint64_t bv = dv0 + st * kKDesc;
-          if (ksteps == 8) {
-            umma::mma_block_pv128_single(tmem + s4::kColO, tp, bv, kIdescO, j > 0);
-          } else if (lane == 0) {
-            for (int kq = 0; kq < ksteps; ++kq)
-              umma::mma_bf16_ts(tmem + s4::kColO, tp + kq * 8, bv + (kq * 2048) / 16, kIdescO, kq > 0 || j > 0);
-          }
-          __syncwarp();
-          umma::commit_elect(bar(s4::kBarPVDone));
-          commit_pair(bar(s4::kBarVEmpty + st));
-          if (j == nt - 1) umma::commit_elect(bar(s4::kBarODone));
-          __syncwarp();
-          if (sr < n_rounds) issue_next_s();                    // into the buffer this PV just read
-        }
-      }
-    }
-  } else if (warp >= s4::kEpiWarp0) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;" ::: "memory");
-    // ------------------------------------------------------------ epilogue
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;
-    const uint32_t tO = tmem + s4::kColO + (static_cast<uint32_t>(quarter * 32) << 16);
-    for (int rd = 0; rd < n_rounds; ++rd) {
-      Item it;
-      get_item(rd, it);
-      for (int d = a.epi_delay_ns; d > 0; d -= 500000) __nanosleep(min(d, 500000));   // test knob
-      mbar_wait(bar(s4::kBarODone), rd & 1);
-      mbar_wait(bar(s4::kBarLReady), rd & 1);
-      umma::fence_after_sync();
-      const float inv_l = 1.f / (lbuf[0][rd & 1][r] + lbuf[1][rd & 1][r]);
-      const int tok = it.i0 + rank * rows_tok + r / G;
-      uint16_t* orow = a.out + (static_cast<int64_t>(it.q0 + min(tok, it.q_len - 1)) * a.hq + it.g * G + r % G) * 128;
-#pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t o[32];
-        umma::ld32(tO + c0, o);
-        umma::wait_ld();
-        if (c0 == 96) {
-          umma::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar(s4::kBarOFree));
-        }
-        if (tok < it.q_len) {
-#pragma unroll
-          for (int c = 0; c < 32; c += 16) {
-            uint32_t w[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              w[e] = pack_bf16(__uint_as_float(o[c + 2 * e]) * inv_l, __uint_as_float(o[c + 2 * e + 1]) * inv_l);
-            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orow + c0 + c), "r"(w[0]),
-                         "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                         : "memory");
-          }
-        }
-      }
-    }
-  } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
-    // ------------------------------------------------------------ softmax warps
-    const int quarter = warp & 3, hf = warp >> 2;      // lane quarter, column half
-    const int r = quarter * 32 + lane;
-    const uint32_t lanes = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tO = tmem + s4::kColO + lanes + 64 * hf;
-    const float sl = a.scale_log2;
-    uint32_t g = 0;
-    for (int rd = 0; rd < n_rounds; ++rd) {
-      Item it;
-      get_item(rd, it);
-      const int nt = steps_of(it);
-      const int i_row = it.i0 + rank * rows_tok + r / G;
-      const int pos = it.ctx - it.q_len + min(i_row, it.q_len - 1);
-      float m = -INFINITY;
-      uint64_t l2 = f2(0.f, 0.f);                      // this half-row's partial sum
-      for (int j = 0; j < nt; ++j, ++g) {
-        const int buf = static_cast<int>(g & 1);
-        const uint32_t tS = tmem + (buf ? s4::kColS1 : 0u) + lanes;
-        // V of this step: rows (warp * 16) .. + 16 of the local copy
-        {
-          const int st = buf;
-          const int nvalid = min(kBN, it.ctx - j * kBN);
-          const int row0 = warp * 16;
-          const uint32_t vb = sb + s4::kOffV + st * s4::kKStage;
-          mbar_wait(bar(s4::kBarVFull + st), (g >> 1) & 1);
-          uint32_t w[8][4];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int e = 32 * i + lane;
-            const int row = row0 + (e >> 4);
-            w[i][0] = w[i][1] = w[i][2] = w[i][3] = 0;
-            if (row < nvalid)
-              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
-                           : "r"(vb + ((e >> 3) & 1) * kKVHalf + row * 128 + (e & 7) * 16));
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int e = 32 * i + lane;
-            const int row = row0 + (e >> 4);
-            if (row < 16 * ((nvalid + 15) / 16))
-              sts128(vb + ((e >> 3) & 1) * kKVHalf + row * 128 + (e & 7) * 16, bf16x2_to_f16x2(w[i][0]),
-                     bf16x2_to_f16x2(w[i][1]), bf16x2_to_f16x2(w[i][2]), bf16x2_to_f16x2(w[i][3]));
-          }
-          umma::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar(s4::kBarVConv + st));
-        }
-        mbar_wait(bar(s4::kBarSFull + buf), (g >> 1) & 1);
-        umma::fence_after_sync();
-        float s[64];
-        {
-          uint32_t u[2][32];
-          umma::ld32(tS + 64 * hf, u[0]);
-          umma::ld32(tS + 64 * hf + 32, u[1]);
-          umma::wait_ld();
-#pragma unroll
-          for (int c = 0; c < 64; ++c) s[c] = __uint_as_float(u[c / 32][c % 32]);
-        }
-        const int lim = pos - j * kBN - 64 * hf;       // last visible column of this half
-        const bool any_mask = __any_sync(0xffffffffu, lim < 63);
-        const int lo_lim = any_mask ? __reduce_min_sync(0xffffffffu, lim) : 64;
-        const int hi_lim = any_mask ? __reduce_max_sync(0xffffffffu, lim) : 64;
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          if (c0 + 31 <= lo_lim || c0 > hi_lim) continue;
-#pragma unroll
-          for (int c = 0; c < 32; ++c) s[c0 + c] = c0 + c > lim ? -INFINITY : s[c0 + c];
-        }
-        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          if (c0 > hi_lim) continue;
-#pragma unroll
-          for (int c = 0; c < 32; c += 8)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) mq[q] = fmaxf(mq[q], fmaxf(s[c0 + c + 2 * q], s[c0 + c + 2 * q + 1]));
-        }
-        const float mloc = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-        // exchange the half-row maxima with the partner warp (same lane quarter)
-        xmax[g & 1][hf][r] = mloc;
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-        const float mx = fmaxf(mloc, xmax[g & 1][hf ^ 1][r]);
-        const float m_new = fmaxf(m, mx);
-        bool resc = false;
-        float alpha = 1.f;
-        if (j == 0) {
-          m = m_new;
-        } else if ((m_new - m) * sl > 8.f) {
-          resc = true;
-          alpha = ex2((m - m_new) * sl);
-          l2 = fmul2(l2, f2(alpha, alpha));
-          m = m_new;
-        }
-        const uint64_t sl2 = f2(sl, sl), nm2 = f2(kPBias - m * sl, kPBias - m * sl);
-        uint64_t la = f2(0.f, 0.f), lb = f2(0.f, 0.f);
-        uint32_t hw[32];
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          if (c0 > hi_lim) {
-#pragma unroll
-            for (int w = 0; w < 16; ++w) hw[c0 / 2 + w] = 0u;
-          } else {
-#pragma unroll
-            for (int w = 0; w < 16; ++w) {
-              const float2 x = unf2(ffma2(f2(s[c0 + 2 * w], s[c0 + 2 * w + 1]), sl2, nm2));
-              const float p0 = ex2(x.x), p1 = ex2(x.y);
-              if (w & 1) lb = fadd2(lb, f2(p0, p1));
-              else la = fadd2(la, f2(p0, p1));
-              hw[c0 / 2 + w] = pack_f16(p0, p1);
-            }
-          }
-        }
-        l2 = fadd2(l2, fadd2(la, lb));
-        if (g > 0) mbar_wait(bar(s4::kBarPVDone), (g - 1) & 1);   // every step: phases stay in step
-        if (__any_sync(0xffffffffu, resc)) {
-          umma::fence_after_sync();
-#pragma unroll 1
-          for (int c0 = 0; c0 < 64; c0 += 32) {
-            uint32_t o[32];
-            umma::ld32(tO + c0, o);
-            umma::wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-            umma::st32(tO + c0, o);
-          }
-        }
-        umma::st16(tS + 32 * hf, *reinterpret_cast<const uint32_t(*)[16]>(&hw[0]));
-        umma::st16(tS + 32 * hf + 16, *reinterpret_cast<const uint32_t(*)[16]>(&hw[16]));
-        umma::wait_st();
-        umma::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(s4::kBarPFull + buf));
-      }
-      const float2 lp = unf2(l2);
-      if (rd > 0) mbar_wait(bar(s4::kBarOFree), (rd - 1) & 1);   // l_ready at most one phase ahead
-      lbuf[hf][rd & 1][r] = lp.x + lp.y;
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(s4::kBarLReady));
-    }
-  }
-  umma::fence_before_sync();
-  __syncthreads();
-  cluster_sync_all();                                  // the peer sends no more multicast data / arrivals
-  if (warp == s4::kMmaWarp) umma::tmem_dealloc(tmem, kTmemCols);
-}
-
 }  // namespace
 
 neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, const CUtensorMap& tmk,
@@ -1851,8 +1405,6 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
       e = cudaFuncSetAttribute(prefill_attn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(prefill_attn_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(prefill_attn_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemAlloc);
     if (e != cudaSuccess) return cuda_fail(e, "prefill smem attribute");
     int n = 0;
     e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -1904,24 +1456,7 @@ neo_status launch_prefill_attn(const PrefillLaunch& L, const CUtensorMap& tmq, c
   // prompts -- 8 x 1024 -6 %, 16 x 512 -11 %, ragged 8 x ~1000 -6..9 % -- and
   // loses 2-5 % from 4096 on, where item boundaries are rare)
   const bool stream = !hilo && L.hkv <= 64 && (kn ? kn[0] == 's' : L.max_q_len <= kStreamMaxQLen);
-  if (stream && kn && kn[0] == 'p') {                     // NEO_PREFILL_KERNEL=pair (experimental)
-    static std::atomic<int> pair_clusters[64];
-    int cur = 0;
-    cudaGetDevice(&cur);
-    int ncl = pair_clusters[cur & 63].load(std::memory_order_relaxed);
-    if (ncl == 0) {
-      cudaLaunchConfig_t oc = cfg;
-      oc.gridDim = dim3(static_cast<unsigned>(2 * (num_sms / 2)));
-      oc.blockDim = dim3(s4::kThreads);
-      oc.numAttrs = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, prefill_attn_pair_kernel, &oc) != cudaSuccess || ncl < 1)
-        ncl = num_sms / 2;
-      pair_clusters[cur & 63].store(ncl, std::memory_order_relaxed);
-    }
-    cfg.gridDim = dim3(static_cast<unsigned>(2 * std::min<int64_t>(n_items, ncl)));
-    cfg.blockDim = dim3(s4::kThreads);
-    cudaLaunchKernelEx(&cfg, prefill_attn_pair_kernel, tmq, tmk, tmv, a);
-  } else if (stream) {
+  if (stream) {
     cfg.blockDim = dim3(s2::kThreads);
     cudaLaunchKernelEx(&cfg, prefill_attn_stream_kernel, tmq, tmk, tmv, a);
   } else if (hilo) {
