@@ -219,11 +219,16 @@ def measure_read_ceiling(gb, stream):
     try:
         lib = ctypes.CDLL(build_readbw())
     except Exception:
-        return None
+        return None, "unavailable (tools/readbw.cu did not build)"
     lib.readbw.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                            ctypes.c_int, ctypes.c_void_p]
     flat = gb.pool.view(-1)
     nbytes = min(4 << 30, flat.numel() * flat.element_size()) // 16 * 16
+    source = "the KV pool"
+    if nbytes < (1 << 30):       # a small pool (c1: 8 MB) would measure latency, not bandwidth
+        flat = torch.ones(1 << 30, dtype=torch.int32, device="cuda")
+        nbytes = flat.numel() * flat.element_size()
+        source = "a 4 GiB scratch buffer (the KV pool is < 1 GiB)"
     sink = torch.zeros(4096, dtype=torch.int32, device="cuda")
     best = 0.0
     for rep in range(7):
@@ -234,7 +239,7 @@ def measure_read_ceiling(gb, stream):
         torch.cuda.synchronize()
         if rep >= 2:
             best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
-    return round(best, 1) if best > 0 else None
+    return (round(best, 1), source) if best > 0 else (None, source)
 
 
 # --------------------------------------------------------------------- neo arm
@@ -369,7 +374,7 @@ def run_neo(args):
     # above breaks that overlap; it is reported only as `isolated_launch_us`.
     avg_launch = t_ms / 1e3 / (L * args.steps)
     hbm_peak, peak_src = peaks()
-    read_ceiling = measure_read_ceiling(gb, stream)
+    read_ceiling, rc_source = measure_read_ceiling(gb, stream)
     algo = gb.kv_bytes_per_call() + gb.other_bytes_per_call()
     achieved = algo / avg_launch / 1e9
     traffic = None
@@ -451,8 +456,8 @@ def run_neo(args):
                          "read_ceiling_gbs": read_ceiling,
                          "frac_of_read_ceiling": round(achieved / read_ceiling, 4) if read_ceiling else None,
                          "frac_of_nominal": round(achieved / NOMINAL_HBM_GBS, 4),
-                         "read_ceiling_source": "measured in this run: 16-byte non-allocating loads over 4 GiB of "
-                                                "the KV pool, 1184 CTAs x 512 threads, best of 5 (tools/readbw.cu)"},
+                         "read_ceiling_source": "measured in this run: 16-byte non-allocating loads over up to 4 GiB "
+                                                f"of {rc_source}, 1184 CTAs x 512 threads, best of 5 (tools/readbw.cu)"},
             "per_rank_ms_per_step": None if per_rank is None else [round(x, 4) for x in per_rank],
             "rank_imbalance": None if per_rank is None else rank_imbalance(per_rank),
             "gpu_launches": L * args.steps,
