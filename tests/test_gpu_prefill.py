@@ -259,3 +259,14 @@ def test_prefill_slow_epilogue_one_step_items():
     except subprocess.TimeoutExpired:
         pytest.fail("stream prefill kernel hung with a slow epilogue (l_ready parity aliasing)")
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_prefill_stream_item_list_overflow(monkeypatch):
+    """The stream kernel decodes at most 512 items per CTA into shared memory in
+    its prologue and decodes later ones on the fly: a grid capped to 2 CTAs
+    (NEO_PREFILL_CTAS, the SM-budget knob) over 1152 items runs 576 rounds per
+    CTA, so the on-the-fly path is exercised; parity against the oracle."""
+    monkeypatch.setenv("NEO_PREFILL_KERNEL", "stream")
+    monkeypatch.setenv("NEO_PREFILL_CTAS", "2")
+    ctx = [1000] * 9
+    check_prefill(PrefillCase(ctx, ctx, 32, 8, seed=960), "stream, 2 CTAs, 576 rounds each")
