@@ -1,5 +1,10 @@
 // Causal paged GQA prefill attention for sm_100a on the 5th-generation tensor
-// cores (the prefill half of batch-0).
+// cores (the prefill half of batch-0).  Two kernels
+// share the tiles, the math and the TMEM layout described here:
+//   prefill_attn_kernel         item-major (this header), prompts > 3072 tokens
+//                               and the bf16 hi + lo P path (< 256 tokens);
+//   prefill_attn_stream_kernel  warp-specialised stream (its own header below),
+//                               fp16 P.V for prompts of 256 .. 3072 tokens.
 //
 // CTA = (request b, kv-head g, two M tiles of 128 query rows).  Row r of a tile
 // is (query token, q-head g*G + r % G): the G heads sharing a KV head are packed
