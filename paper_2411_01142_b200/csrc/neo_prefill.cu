@@ -68,9 +68,8 @@ constexpr int kStreamMaxQLen = 3072;             // fp16 path: stream kernel up 
 #ifndef NEO_PF_EXP
 #define NEO_PF_EXP 0   // timing experiments only (results wrong): 1 no V conversion, 2 no softmax math + no conversion, 3 no softmax math, 4 (stream kernel) no MMAs (softmax math and conversion kept)
 #endif
-constexpr int kConvWarps = 0;
 constexpr uint32_t kIdescS = umma::idesc_bf16_f32(kBM, kBN, false, false);
-constexpr int kThreads = 320 + 32 * kConvWarps;
+constexpr int kThreads = 320;
 constexpr int kProducerWarp = 8, kMmaWarp = 9;
 
 // barrier slots
